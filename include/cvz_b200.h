@@ -1,0 +1,199 @@
+/*
+ * cvz_b200.h -- C-ABI of libcvz_b200.so, the B200 (sm_100a) implementation of
+ * the BigGraphVis hot path (reference: commviz, /root/reference/pkg/src).
+ *
+ * The reference has no FFI; its native seam is a set of numba @njit kernels
+ * called from Python.  Every entry point below replaces one of
+ * those kernels or one numpy bulk operation on the path, and cites it as
+ * C/<file>:<line> (C/ = /root/reference/pkg/src/commviz/).  The Python
+ * drop-in package (paper_2108_00529_b200) binds these with ctypes; a
+ * maintainer of the reference would bind them the same way.
+ *
+ * Conventions
+ *  - Plain pointers + sizes, no torch types.  Pointers marked [dev] are
+ *    device pointers, [host] host pointers.  Ids on device are int32
+ *    (node ids < 2^31); public arrays stay int64/float64 like the reference.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *    Work is stream-ordered; scratch is cudaMallocAsync'ed on that stream.
+ *  - Every function returns a cvz_status (0 = OK).  cvz_last_error() gives a
+ *    message.  CVZ_ERR_VALUE maps to the reference's ValueError,
+ *    CVZ_ERR_LAYOUT to LayoutError.
+ *  - Functions whose output size is data-dependent synchronise the stream
+ *    and say so.
+ */
+#ifndef CVZ_B200_H
+#define CVZ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum cvz_status {
+    CVZ_OK = 0,
+    CVZ_ERR_CUDA = -1,   /* CUDA runtime / launch failure                    */
+    CVZ_ERR_VALUE = -2,  /* bad argument (reference raises ValueError)       */
+    CVZ_ERR_LAYOUT = -3, /* non-finite layout positions (LayoutError)        */
+    CVZ_ERR_OOM = -4,    /* device allocation failed                          */
+    CVZ_ERR_RANGE = -5   /* node id outside [0, 2^31) / label out of range    */
+};
+
+enum cvz_scoda_mode { CVZ_SCODA_DETERMINISTIC = 0, CVZ_SCODA_FAST = 1 };
+
+int cvz_version(void);
+const char *cvz_last_error(void);
+/* Number of kernels this library has launched so far (process-wide).     */
+long long cvz_launch_count(void);
+
+/* ---------------------------------------------------------------- graph */
+
+/* C/graph.py:114-122 from_edge_array (mask u==v keeping stream order) and
+ * C/graph.py:121 np.bincount.  Stable single-pass compaction of an (m,2)
+ * edge array ([dev] int64 or int32, in_is_int32 selects) into int32 pairs,
+ * plus the maximum id.  d_m_out/d_max_id: [dev] int64 scalars.
+ * Ids < 0 or >= 2^31 -> CVZ_ERR_RANGE (checked after a stream sync only when
+ * check_range != 0). */
+int cvz_edges_compact(const void *edges, int in_is_int32, int64_t m,
+                      int32_t *edges_out, int64_t *d_m_out, int64_t *d_max_id,
+                      int check_range, void *stream);
+
+/* C/graph.py:121 degree = bincount(edges.ravel(), minlength=n).
+ * degree [dev] int64[n] is overwritten. */
+int cvz_degree_count(const int32_t *edges, int64_t m, int64_t n, int64_t *degree,
+                     void *stream);
+
+/* C/graph.py:125-136 degree_stats: out3 [dev] int64[3] = {mode of nonzero
+ * degrees (ties -> smaller), sum, max}.  mode = 0 when all degrees are 0. */
+int cvz_degree_stats(const int64_t *degree, int64_t n, int64_t *out3, void *stream);
+
+/* ------------------------------------------------------------ community */
+
+/* C/community.py:98-120 _scoda_pass followed by C/community.py:123-161
+ * _resolve_labels -- one streaming pass over edges[order[k]], k < m.
+ *   order     [dev] int64[m] or NULL (identity; C/community.py:164-172)
+ *   deg       [dev] int64[n] in/out counters (C/community.py:211)
+ *   lab       [dev] int64[n] in: labels (values in [0,n)), out: RESOLVED
+ *             representatives (min id on the reached cycle)
+ *   lab_raw   [dev] int64[n] or NULL: receives the unresolved pass labels
+ *   mode      CVZ_SCODA_DETERMINISTIC reproduces the sequential edge-order
+ *             semantics bit-exactly; CVZ_SCODA_FAST is the racy 1-thread-per-
+ *             edge pass (tolerance-gated). */
+int cvz_scoda_pass(const int32_t *edges, int64_t m, const int64_t *order, int64_t n,
+                   int64_t threshold, int tie_code, int mode, int64_t *deg, int64_t *lab,
+                   int64_t *lab_raw, void *stream);
+
+/* C/community.py:123-161 _resolve_labels alone: out[x] = min id on the cycle
+ * reached from x.  lab values must lie in [0,n) (else CVZ_ERR_RANGE, after a
+ * stream sync). */
+int cvz_resolve_labels(const int64_t *lab, int64_t n, int64_t *out, void *stream);
+
+/* One round of C/community.py:253-278 detect_communities on device:
+ *   size-seeded counters (round > 1), pass over cur_edges (order or NULL),
+ *   resolve, compose node_lab = lab[node_lab], history snapshot, early-stop
+ *   test against prev_lab, then the next round's stream: contract
+ *   (round_stream 0: relabelled crossing edges of cur_edges, stable) or
+ *   restream (1: orig_edges relabelled by node_lab, crossing only).
+ * node_lab [dev] int64[n] in/out; prev_lab [dev] int64[n] (in, ignored in
+ * round 1; then overwritten with the new node_lab); deg_out [dev] int64[n];
+ * history_out [dev] int64[n] or NULL; next_edges [dev] int32 capacity
+ * max(m_cur, m_orig) pairs.  SYNCHRONISES: *next_m and *changed [host]. */
+int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *order,
+                     const int32_t *orig_edges, int64_t m_orig, int64_t n,
+                     int64_t threshold, int tie_code, int mode, int round_index,
+                     int round_stream, int64_t *node_lab, int64_t *prev_lab,
+                     int64_t *deg_out, int64_t *history_out, int32_t *next_edges,
+                     int64_t *next_m, int *changed, void *stream);
+
+/* --------------------------------------------------------------- sketch */
+
+/* C/sketch.py:39-44 CountMinSketch._indices: idx[r*k + j] = ((a_r*(x mod p)
+ * + b_r) mod p) mod cols, p = 2^31-1, numpy non-negative mod. [dev] all. */
+int cvz_sketch_indices(const int64_t *hash_a, const int64_t *hash_b, int rows,
+                       int64_t cols, const int64_t *keys, int64_t k, int64_t *idx,
+                       void *stream);
+
+/* C/sketch.py:71-86 sketch_add_many (C/supergraph.py:42-46 accumulate_sizes):
+ * table[r, idx_r(key_j)] += amount_j with int64 wrap-around, then every
+ * negative cell is set to INT64_MAX.  amounts must be >= 0 (validate != 0
+ * checks first and returns CVZ_ERR_VALUE without touching the table; this
+ * synchronises).  *d_saturated [dev] int32 is set to 1 if any cell wrapped.
+ * Shared-memory-staged table when rows*cols fits, warp-aggregated global
+ * atomics otherwise. */
+int cvz_sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *hash_a,
+                   const int64_t *hash_b, const int64_t *keys, const int64_t *amounts,
+                   int64_t k, int validate, int32_t *d_saturated, void *stream);
+
+/* C/sketch.py:93-98 sketch_estimate_many: out[j] = min_r table[r, idx_r]. */
+int cvz_sketch_estimate(const int64_t *table, int rows, int64_t cols,
+                        const int64_t *hash_a, const int64_t *hash_b,
+                        const int64_t *keys, int64_t k, int64_t *out, void *stream);
+
+/* ----------------------------------------------------------- supergraph */
+
+typedef struct {
+    int64_t k;         /* supernodes                                   */
+    int64_t se;        /* superedges                                   */
+    int64_t *comm_id;  /* [dev] int64[k] ascending community labels    */
+    int64_t *weight;   /* [dev] int64[k] sketch estimates              */
+    int64_t *se_edges; /* [dev] int64[se*2] (lo, hi), lexicographic    */
+    int64_t *mult;     /* [dev] int64[se] multiplicities               */
+} cvz_contract_result;
+
+/* C/supergraph.py:49-76 contract: dense ids = rank of label among the
+ * sorted unique labels; weights from the sketch; crossing edges -> (lo,hi)
+ * 64-bit keys, radix sort + run-length encode.  labels [dev] int64[n]
+ * (arbitrary int64 values).  Outputs are library-owned device buffers;
+ * release with cvz_contract_release.  SYNCHRONISES. */
+int cvz_contract(const int32_t *edges, int64_t m, const int64_t *labels, int64_t n,
+                 const int64_t *table, int rows, int64_t cols, const int64_t *hash_a,
+                 const int64_t *hash_b, cvz_contract_result *res, void *stream);
+int cvz_contract_release(cvz_contract_result *res, void *stream);
+
+/* --------------------------------------------------------------- layout */
+
+typedef struct {
+    int64_t iterations;
+    double gravity, repulsion, jitter_tolerance, theta, max_step;
+    int speed_form;      /* 0 product, 1 sum      (C/layout.py:384-387) */
+    int attraction_form; /* 0 canonical, 1 reversed (C/layout.py:362)   */
+} cvz_layout_params;
+
+/* C/layout.py:312-328 repulsion_forces: theta <= 0 -> exact O(n^2) tiles
+ * (C/layout.py:273-290), else GPU Barnes-Hut over the reference's quadtree
+ * (C/layout.py:97-270).  pos [dev] f64[n*2], mass [dev] f64[n], out [dev]
+ * f64[n*2] (overwritten). */
+int cvz_repulsion(const double *pos, const double *mass, int64_t n, double repulsion,
+                  double theta, double *out, void *stream);
+
+/* C/layout.py:293-304 _attraction: out[u] += w*s*(p_v-p_u),
+ * out[v] -= w*s*(p_v-p_u), accumulated per node in edge order (CSR gather,
+ * no atomics).  edges [dev] int32[m*2], weight [dev] f64[m] or NULL (=1). */
+int cvz_attraction(const double *pos, int64_t n, const int32_t *edges, int64_t m,
+                   const double *weight, double sign, double *out, void *stream);
+
+/* C/layout.py:341-402 layout loop, every iteration on device (one CUDA graph
+ * per iteration, replayed).  pos [dev] f64[n*2] in/out; mass [dev] f64[n];
+ * edges [dev] int32[m*2]; weight [dev] f64[m] or NULL; prev_force [dev]
+ * f64[n*2] in/out (zeros for a fresh run, C/layout.py:363); speed [dev]
+ * f64[1] in/out (1.0 fresh, :364); disp_hist [dev] f64[iterations].
+ * On non-finite positions returns CVZ_ERR_LAYOUT and *bad_iteration [host]
+ * = the 1-based iteration (C/layout.py:395-397).  SYNCHRONISES. */
+int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *edges,
+                   int64_t m, const double *weight, const cvz_layout_params *params,
+                   double *prev_force, double *speed, double *disp_hist,
+                   int64_t *bad_iteration, void *stream);
+
+/* -------------------------------------------------------------- metrics */
+
+/* C/metrics.py:34-46 modularity ingredients: intra[c] and degsum[c] over
+ * dense community ids.  dense [dev] int32[n] in [0,k); intra/degsum [dev]
+ * int64[k] (overwritten). */
+int cvz_modularity_parts(const int32_t *edges, int64_t m, const int32_t *dense,
+                         const int64_t *degree, int64_t n, int64_t k, int64_t *intra,
+                         int64_t *degsum, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CVZ_B200_H */

@@ -266,8 +266,10 @@ def contract(edges, labels, table, a, b):
     lo = np.minimum(cu[cross], cv[cross])
     hi = np.maximum(cu[cross], cv[cross])
     if len(lo):
-        uniq, mult = np.unique(np.stack([lo, hi], axis=1), axis=0,
-                               return_counts=True)
+        # np.unique(pairs, axis=0) order == numeric order of lo*k + hi (hi < k)
+        kk = np.int64(len(comm))
+        keys, mult = np.unique(lo * kk + hi, return_counts=True)
+        uniq = np.stack([keys // kk, keys % kk], axis=1)
     else:
         uniq, mult = np.empty((0, 2), np.int64), np.empty(0, np.int64)
     return (len(comm), uniq.astype(np.int64), weight.astype(np.int64),

@@ -1,0 +1,149 @@
+"""ctypes binding of libcvz_b200.so (include/cvz_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every compute call raises.  Device buffers are torch CUDA tensors
+(torch is plumbing here: allocation + streams); only raw pointers cross the
+C-ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libcvz_b200.so")
+
+CVZ_OK, CVZ_ERR_CUDA, CVZ_ERR_VALUE, CVZ_ERR_LAYOUT, CVZ_ERR_OOM, CVZ_ERR_RANGE = 0, -1, -2, -3, -4, -5
+DETERMINISTIC, FAST = 0, 1
+
+
+class LayoutError(RuntimeError):
+    """Non-finite layout positions (C/layout.py:36-37)."""
+
+
+class _ContractResult(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int64), ("se", ctypes.c_int64),
+                ("comm_id", ctypes.c_void_p), ("weight", ctypes.c_void_p),
+                ("se_edges", ctypes.c_void_p), ("mult", ctypes.c_void_p)]
+
+
+class _LayoutParams(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("gravity", ctypes.c_double),
+                ("repulsion", ctypes.c_double), ("jitter_tolerance", ctypes.c_double),
+                ("theta", ctypes.c_double), ("max_step", ctypes.c_double),
+                ("speed_form", ctypes.c_int), ("attraction_form", ctypes.c_int)]
+
+
+_P, _I64, _I32, _D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+
+# symbol -> argtypes (restype int unless noted); mirrors include/cvz_b200.h
+SIGNATURES = {
+    "cvz_version": [],
+    "cvz_last_error": [],
+    "cvz_launch_count": [],
+    "cvz_edges_compact": [_P, _I32, _I64, _P, _P, _P, _I32, _P],
+    "cvz_degree_count": [_P, _I64, _I64, _P, _P],
+    "cvz_degree_stats": [_P, _I64, _P, _P],
+    "cvz_scoda_pass": [_P, _I64, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P],
+    "cvz_resolve_labels": [_P, _I64, _P, _P],
+    "cvz_detect_round": [_P, _I64, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _I32,
+                         _P, _P, _P, _P, _P, ctypes.POINTER(_I64),
+                         ctypes.POINTER(ctypes.c_int), _P],
+    "cvz_sketch_indices": [_P, _P, _I32, _I64, _P, _I64, _P, _P],
+    "cvz_sketch_add": [_P, _I32, _I64, _P, _P, _P, _P, _I64, _I32, _P, _P],
+    "cvz_sketch_estimate": [_P, _I32, _I64, _P, _P, _P, _I64, _P, _P],
+    "cvz_contract": [_P, _I64, _P, _I64, _P, _I32, _I64, _P, _P,
+                     ctypes.POINTER(_ContractResult), _P],
+    "cvz_contract_release": [ctypes.POINTER(_ContractResult), _P],
+    "cvz_repulsion": [_P, _P, _I64, _D, _D, _P, _P],
+    "cvz_attraction": [_P, _I64, _P, _I64, _P, _D, _P, _P],
+    "cvz_layout_run": [_P, _P, _I64, _P, _I64, _P, ctypes.POINTER(_LayoutParams),
+                       _P, _P, _P, ctypes.POINTER(_I64), _P],
+    "cvz_modularity_parts": [_P, _I64, _P, _P, _I64, _I64, _P, _P, _P],
+}
+
+_lib = None
+
+
+def load():
+    """Load the library (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: run `python -m paper_2108_00529_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, args in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        lib.cvz_last_error.restype = ctypes.c_char_p
+        lib.cvz_launch_count.restype = ctypes.c_longlong
+        _lib = lib
+    return _lib
+
+
+def launch_count() -> int:
+    return int(load().cvz_launch_count())
+
+
+def check(rc: int, what: str = ""):
+    if rc == CVZ_OK:
+        return
+    msg = load().cvz_last_error().decode(errors="replace")
+    if rc in (CVZ_ERR_VALUE, CVZ_ERR_RANGE):
+        raise ValueError(msg)
+    if rc == CVZ_ERR_LAYOUT:
+        raise LayoutError(msg)
+    if rc == CVZ_ERR_OOM:
+        raise MemoryError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: CUDA error: {msg}")
+
+
+def call(name: str, *args):
+    check(getattr(load(), name)(*args), name)
+
+
+# ---------------------------------------------------------------- torch glue
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        if not t.cuda.is_available():
+            raise RuntimeError("paper_2108_00529_b200 needs a CUDA device (B200); "
+                               "there is no CPU fallback")
+        _torch = t
+    return _torch
+
+
+def stream():
+    return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def device():
+    return torch().device("cuda", torch().cuda.current_device())
+
+
+def to_dev(a, dtype):
+    """numpy / list / torch -> contiguous CUDA tensor of `dtype` (torch dtype)."""
+    T = torch()
+    if isinstance(a, T.Tensor):
+        t = a.to(device=device(), dtype=dtype)
+    else:
+        import numpy as np
+        arr = np.ascontiguousarray(np.asarray(a))
+        t = T.from_numpy(arr).to(device=device(), dtype=dtype, non_blocking=False)
+    return t.contiguous()
+
+
+def to_host(t):
+    return t.detach().cpu().numpy()

@@ -1,0 +1,246 @@
+// Shared infrastructure for the commviz-b200 CUDA library (sm_100a).
+//
+// * status/error plumbing for the C-ABI (cvz_status codes, thread-local msg)
+// * stream-ordered scratch allocation (cudaMallocAsync on the caller's stream,
+//   pool release threshold raised once so steady-state calls never hit the OS)
+// * a single-pass decoupled look-back tile prefix (used by every stable
+//   stream compaction on the hot path: self-loop drop, round contraction)
+// * launch accounting (cvz_launch_count) for bench.py's gpu_launches claim
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cvz_b200.h"
+
+namespace cvz {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string &m);
+extern std::atomic<long long> g_launches;
+
+#define CVZ_CUDA(call)                                                              \
+    do {                                                                            \
+        cudaError_t _e = (call);                                                    \
+        if (_e != cudaSuccess)                                                      \
+            throw ::cvz::Error(_e == cudaErrorMemoryAllocation ? CVZ_ERR_OOM        \
+                                                               : CVZ_ERR_CUDA,      \
+                               std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define CVZ_REQUIRE(cond, code, msg)                 \
+    do {                                             \
+        if (!(cond)) throw ::cvz::Error(code, msg);  \
+    } while (0)
+
+// Launch with accounting + immediate launch-error check.
+#define CVZ_LAUNCH(kernel, grid, block, smem, stream, ...)              \
+    do {                                                                \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);     \
+        ::cvz::g_launches.fetch_add(1, std::memory_order_relaxed);      \
+        CVZ_CUDA(cudaGetLastError());                                   \
+    } while (0)
+
+// Count a library (CUB) primitive's kernels in the launch tally.
+inline void count_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+// C-ABI boundary: run body, map exceptions to status codes.
+template <class F>
+int guard(F &&f) {
+    try {
+        f();
+        return CVZ_OK;
+    } catch (const Error &e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::exception &e) {
+        set_last_error(e.what());
+        return CVZ_ERR_CUDA;
+    }
+}
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void init_pool_once();
+
+// Stream-ordered scratch arena: every allocation is released (stream-ordered)
+// when the arena goes out of scope, so kernels queued before the free still
+// see valid memory.
+class Scratch {
+   public:
+    explicit Scratch(cudaStream_t s) : s_(s) { init_pool_once(); }
+    ~Scratch() {
+        for (void *p : ptrs_) cudaFreeAsync(p, s_);
+    }
+    Scratch(const Scratch &) = delete;
+    Scratch &operator=(const Scratch &) = delete;
+    template <class T>
+    T *alloc(size_t n) {
+        void *p = nullptr;
+        size_t bytes = n * sizeof(T);
+        if (bytes == 0) bytes = 16;
+        CVZ_CUDA(cudaMallocAsync(&p, bytes, s_));
+        ptrs_.push_back(p);
+        return static_cast<T *>(p);
+    }
+    // Detach an allocation so it outlives the arena (ownership -> caller).
+    void release(void *p) {
+        for (auto &q : ptrs_)
+            if (q == p) q = nullptr;
+        std::vector<void *> keep;
+        for (void *q : ptrs_)
+            if (q) keep.push_back(q);
+        ptrs_.swap(keep);
+    }
+    cudaStream_t stream() const { return s_; }
+
+   private:
+    cudaStream_t s_;
+    std::vector<void *> ptrs_;
+};
+
+template <class T>
+T *device_alloc(size_t n, cudaStream_t s) {
+    init_pool_once();
+    void *p = nullptr;
+    CVZ_CUDA(cudaMallocAsync(&p, (n ? n : 1) * sizeof(T), s));
+    return static_cast<T *>(p);
+}
+
+inline int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+inline unsigned grid_for(long long work, int block, int per_thread = 1, int waves = 8) {
+    long long need = (work + (long long)block * per_thread - 1) / ((long long)block * per_thread);
+    long long cap = (long long)num_sms() * waves;
+    if (need < 1) need = 1;
+    return (unsigned)(need < cap ? need : cap);
+}
+
+inline unsigned blocks_for(long long work, int block) {
+    long long b = (work + block - 1) / block;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+// ---------------------------------------------------------------- device
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Decoupled look-back (single pass) exclusive prefix over tiles.
+// status[t] packs (flag << 62) | value; flag 1 = aggregate, 2 = inclusive.
+// The caller zeroes status[] and *tile_counter before the launch.
+struct LookbackState {
+    unsigned long long *status;
+    unsigned int *tile_counter;
+};
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
+    return *reinterpret_cast<const volatile unsigned long long *>(p);
+}
+
+constexpr unsigned long long LB_AGG = 1ull << 62;
+constexpr unsigned long long LB_INC = 2ull << 62;
+constexpr unsigned long long LB_VAL = (1ull << 62) - 1;
+
+// Dynamic, monotonically ordered tile id (guarantees forward progress of
+// the look-back regardless of CTA scheduling order).  Call from all threads.
+__device__ __forceinline__ unsigned acquire_tile(LookbackState st, unsigned *smem_slot) {
+    if (threadIdx.x == 0) *smem_slot = atomicAdd(st.tile_counter, 1u);
+    __syncthreads();
+    return *smem_slot;
+}
+
+// Returns the exclusive prefix of this tile (valid in all threads).
+// `local` must be valid in thread 0.  smem_slot: one shared u64.
+__device__ __forceinline__ unsigned long long tile_prefix(LookbackState st, unsigned tile,
+                                                          unsigned long long local,
+                                                          unsigned long long *smem_slot) {
+    if (threadIdx.x < 32) {
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicExch(&st.status[0], LB_INC | local);
+            }
+        } else {
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicExch(&st.status[tile], LB_AGG | local);
+            }
+            // warp-parallel look-back over 32 predecessors at a time
+            long long base = (long long)tile - 1;
+            while (true) {
+                long long idx = base - threadIdx.x;
+                unsigned long long v = 0;
+                if (idx >= 0) {
+                    do {
+                        v = ld_volatile(&st.status[idx]);
+                    } while ((v >> 62) == 0);
+                } else {
+                    v = LB_INC;  // virtual inclusive zero before tile 0
+                }
+                unsigned inc_mask = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+                // lanes up to (and including) the first inclusive one contribute
+                int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
+                unsigned long long contrib = (threadIdx.x <= (unsigned)first_inc) ? (v & LB_VAL) : 0;
+                for (int o = 16; o > 0; o >>= 1) contrib += __shfl_down_sync(0xffffffffu, contrib, o);
+                excl += __shfl_sync(0xffffffffu, contrib, 0);
+                if (inc_mask) break;
+                base -= 32;
+            }
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicExch(&st.status[tile], LB_INC | (excl + local));
+            }
+        }
+        if (threadIdx.x == 0) *smem_slot = excl;
+    }
+    __syncthreads();
+    return *smem_slot;
+}
+
+// Block-wide exclusive scan of one int per thread (BLOCK threads).
+template <int BLOCK>
+__device__ __forceinline__ int block_exclusive_scan(int v, int *warp_sums, int &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int w = (lane < BLOCK / 32) ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < BLOCK / 32) warp_sums[lane] = w;
+    }
+    __syncthreads();
+    int before = (wid ? warp_sums[wid - 1] : 0);
+    total = warp_sums[BLOCK / 32 - 1];
+    __syncthreads();
+    return before + x - v;
+}
+
+}  // namespace cvz

@@ -1,0 +1,947 @@
+// ForceAtlas2 with Barnes-Hut repulsion on B200 (fp64 throughout: B200 keeps
+// half-rate FP64, and fp64 state keeps the layout within ~1e-13 of the
+// reference per iteration).  Reference: C/layout.py:85-402.
+//
+// Tree.  The reference inserts bodies one by one into a quadtree whose cells
+// hold <= 1 body (depth cap 40 -> aggregate cell).  That tree is canonical:
+// its cells are exactly the quadrant prefixes (computed with the reference's
+// own fp64 centre arithmetic, C/layout.py:118-137,171-208) shared by >= 2
+// bodies.  Single-child chain cells never change a force (same body set,
+// larger side), so the GPU builds the compressed tree:
+//   keys  : per body, the 40 quadrant digits (80 bits), digit = 3 - q so a
+//           left-first DFS visits children in the reference's pop order
+//           3,2,1,0 (C/layout.py:262-267);
+//   sort  : stable radix sort by (hi64, lo16);
+//   build : Karras binary radix tree over the sorted keys; a binary node is a
+//           quadtree cell iff it is the topmost node of its digit level
+//           (delta/2 > parent delta/2); nodes with delta >= 80 below a
+//           non-aggregate parent are the reference's depth-40 aggregates;
+//   COM   : bottom-up, one thread per leaf, second arrival combines.
+// Traversal is stackless (skip pointers: rc_by_split[last]), one thread per
+// body in key order so warps walk coherent paths; per-body decisions are the
+// reference's (no warp-vote opening), so the interaction set is identical.
+//
+// Iteration: [keys] [sort] [build] [COM] [repulsion] [attraction+gravity+
+// swing, last block -> global speed] [update, clamp, disp max, bbox, last
+// block -> next bbox].  The whole iteration is captured once into a CUDA
+// graph and replayed `iterations` times; all scalars live on the device.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace cvz {
+namespace {
+
+constexpr int FB = 256;
+constexpr int END = 0x7fffffff;
+constexpr int MAX_DEPTH = 40;
+constexpr double EPS = 1e-4;  // COINCIDE_EPS, C/layout.py:29
+
+// non-contracted fp64 ops: every interaction term rounds like the CPU code
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+// C/layout.py:85-94 _separation
+__device__ __forceinline__ double separation(double &dx, double &dy, long long a, long long b) {
+    double d2 = add(mul(dx, dx), mul(dy, dy));
+    if (d2 >= EPS * EPS) return sqrt(d2);
+    long long h = (a * 2654435761LL + b * 40503LL) % 65536LL;
+    if (h < 0) h += 65536;
+    double ang = 6.283185307179586 * ((double)h / 65536.0);
+    dx = EPS * cos(ang);
+    dy = EPS * sin(ang);
+    return EPS;
+}
+
+struct Body {
+    double x, y, m;
+    int orig, pad;
+};
+
+struct __align__(16) TNode {
+    double comx, comy, mass, side2;
+    int left, skip, kind, pad;  // kind: 0 transparent, 1 quad cell, 2 aggregate
+};
+
+struct Geo {  // root cell, C/layout.py:118-137
+    double cx, cy, half;
+};
+
+__device__ __forceinline__ Geo root_geo(const double *bbox) {
+    double minx = bbox[0], maxx = bbox[1], miny = bbox[2], maxy = bbox[3];
+    double half = 0.5 * fmax(maxx - minx, maxy - miny);
+    if (!(half > 0.0)) half = 1e-6;
+    half *= 1.0000001;
+    Geo g;
+    g.cx = 0.5 * (minx + maxx);
+    g.cy = 0.5 * (miny + maxy);
+    g.half = half;
+    return g;
+}
+
+// ---- bbox ------------------------------------------------------------------
+__global__ void bbox_kernel(const double2 *__restrict__ pos, long long n,
+                            double *__restrict__ part, unsigned *__restrict__ ctr,
+                            double *__restrict__ bbox) {
+    double a = INFINITY, b = -INFINITY, c = INFINITY, d = -INFINITY;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double2 p = pos[i];
+        a = fmin(a, p.x);
+        b = fmax(b, p.x);
+        c = fmin(c, p.y);
+        d = fmax(d, p.y);
+    }
+    __shared__ double sh[4][FB / 32];
+    for (int o = 16; o > 0; o >>= 1) {
+        a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+        c = fmin(c, __shfl_xor_sync(0xffffffffu, c, o));
+        d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    }
+    if (lane_id() == 0) {
+        sh[0][threadIdx.x >> 5] = a;
+        sh[1][threadIdx.x >> 5] = b;
+        sh[2][threadIdx.x >> 5] = c;
+        sh[3][threadIdx.x >> 5] = d;
+    }
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < FB / 32; ++w) {
+            a = fmin(a, sh[0][w]);
+            b = fmax(b, sh[1][w]);
+            c = fmin(c, sh[2][w]);
+            d = fmax(d, sh[3][w]);
+        }
+        part[4 * blockIdx.x + 0] = a;
+        part[4 * blockIdx.x + 1] = b;
+        part[4 * blockIdx.x + 2] = c;
+        part[4 * blockIdx.x + 3] = d;
+        __threadfence();
+        last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        for (unsigned k = 0; k < gridDim.x; ++k) {
+            a = fmin(a, part[4 * k + 0]);
+            b = fmax(b, part[4 * k + 1]);
+            c = fmin(c, part[4 * k + 2]);
+            d = fmax(d, part[4 * k + 3]);
+        }
+        bbox[0] = a;
+        bbox[1] = b;
+        bbox[2] = c;
+        bbox[3] = d;
+        *ctr = 0;
+    }
+}
+
+// ---- keys ------------------------------------------------------------------
+// The reference's descent (C/layout.py:171-208): q = (x >= cx) + 2 (y >= cy),
+// child centre c +- h with h = 0.5 * parent half.  fp64, same op order.
+__global__ void keys_kernel(const double2 *__restrict__ pos, long long n,
+                            const double *__restrict__ bbox,
+                            unsigned long long *__restrict__ khi, unsigned *__restrict__ klo,
+                            unsigned *__restrict__ idx) {
+    Geo g = root_geo(bbox);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double2 p = pos[i];
+        double cx = g.cx, cy = g.cy, h = g.half;
+        unsigned long long hi = 0;
+        unsigned lo = 0;
+#pragma unroll 4
+        for (int dpt = 0; dpt < MAX_DEPTH; ++dpt) {
+            int qx = p.x >= cx, qy = p.y >= cy;
+            unsigned digit = 3u - (unsigned)(qx + 2 * qy);
+            if (dpt < 32)
+                hi = (hi << 2) | digit;
+            else
+                lo = (lo << 2) | digit;
+            h = 0.5 * h;
+            cx = qx ? cx + h : cx - h;
+            cy = qy ? cy + h : cy - h;
+        }
+        khi[i] = hi;
+        klo[i] = lo << 16;  // 8 digits in the top 16 bits
+        idx[i] = (unsigned)i;
+    }
+}
+
+__global__ void gather_hi_kernel(const unsigned long long *__restrict__ khi,
+                                 const unsigned *__restrict__ idx, long long n,
+                                 unsigned long long *__restrict__ out) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = khi[idx[i]];
+}
+
+__global__ void gather_bodies_kernel(const double2 *__restrict__ pos,
+                                     const double *__restrict__ mass,
+                                     const unsigned *__restrict__ idx,
+                                     const unsigned *__restrict__ klo_unsorted, long long n,
+                                     Body *__restrict__ bodies, unsigned *__restrict__ klo) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (long long)gridDim.x * blockDim.x) {
+        unsigned i = idx[p];
+        double2 q = pos[i];
+        bodies[p] = Body{q.x, q.y, mass[i], (int)i, 0};
+        klo[p] = klo_unsorted[i];
+    }
+}
+
+// ---- Karras radix tree -----------------------------------------------------
+struct Keys {
+    const unsigned long long *hi;
+    const unsigned *lo;
+    int n;
+    __device__ __forceinline__ int delta(int i, int j) const {
+        if (j < 0 || j >= n) return -1;
+        unsigned long long a = hi[i] ^ hi[j];
+        if (a) return __clzll(a);
+        unsigned b = lo[i] ^ lo[j];
+        if (b) return 64 + __clz(b);
+        return 80 + __clz((unsigned)(i ^ j));  // identical keys: index tiebreak
+    }
+};
+
+__global__ void karras_kernel(Keys K, int *__restrict__ left, int *__restrict__ first,
+                              int *__restrict__ last, int *__restrict__ delta_out,
+                              int *__restrict__ parent_int, int *__restrict__ parent_leaf,
+                              int *__restrict__ pdelta, int *__restrict__ rc_by_split) {
+    const int n = K.n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
+        int d = (K.delta(i, i + 1) - K.delta(i, i - 1)) >= 0 ? 1 : -1;
+        int dmin = K.delta(i, i - d);
+        int lmax = 2;
+        while (K.delta(i, i + lmax * d) > dmin) lmax <<= 1;
+        int l = 0;
+        for (int t = lmax >> 1; t >= 1; t >>= 1)
+            if (K.delta(i, i + (l + t) * d) > dmin) l += t;
+        int j = i + l * d;
+        int dnode = K.delta(i, j);
+        int s = 0;
+        int t = l;
+        do {
+            t = (t + 1) >> 1;
+            if (K.delta(i, i + (s + t) * d) > dnode) s += t;
+        } while (t > 1);
+        int gamma = i + s * d + min(d, 0);
+        int lo = min(i, j), hi = max(i, j);
+        int lc = (lo == gamma) ? ~gamma : gamma;
+        int rc = (hi == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+        left[i] = lc;
+        first[i] = lo;
+        last[i] = hi;
+        delta_out[i] = dnode;
+        rc_by_split[gamma] = rc;
+        if (lc >= 0) {
+            parent_int[lc] = i;
+            pdelta[lc] = dnode;
+        } else {
+            parent_leaf[~lc] = i;
+        }
+        if (rc >= 0) {
+            parent_int[rc] = i;
+            pdelta[rc] = dnode;
+        } else {
+            parent_leaf[~rc] = i;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) pdelta[0] = -2;  // root
+}
+
+// bottom-up sums + cell classification + skip pointers
+__global__ void com_kernel(const Body *__restrict__ bodies, int n, const int *__restrict__ left,
+                           const int *__restrict__ first, const int *__restrict__ last,
+                           const int *__restrict__ delta, const int *__restrict__ parent_int,
+                           const int *__restrict__ parent_leaf, const int *__restrict__ pdelta,
+                           const int *__restrict__ rc_by_split, unsigned *__restrict__ visit,
+                           double *__restrict__ smass, double *__restrict__ sx,
+                           double *__restrict__ sy, const double *__restrict__ bbox,
+                           TNode *__restrict__ nodes) {
+    Geo g = root_geo(bbox);
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        int node = parent_leaf[p];
+        while (node >= 0) {
+            __threadfence();
+            if (atomicAdd(visit + node, 1u) == 0) break;  // first arrival stops
+            __threadfence();
+            int l = left[node];
+            int r = (l >= 0) ? -1 : 0;  // placeholder, computed below
+            (void)r;
+            // children: left = l; right = rc_by_split[split] -- recover split:
+            // left child covers [first, gamma]: gamma = (l >= 0 ? last[l] : ~l)
+            int gamma = l >= 0 ? last[l] : ~l;
+            int rc = rc_by_split[gamma];
+            double m0, x0, y0, m1, x1, y1;
+            if (l >= 0) {
+                m0 = ((volatile double *)smass)[l];
+                x0 = ((volatile double *)sx)[l];
+                y0 = ((volatile double *)sy)[l];
+            } else {
+                Body b = bodies[~l];
+                m0 = b.m;
+                x0 = mul(b.m, b.x);
+                y0 = mul(b.m, b.y);
+            }
+            if (rc >= 0) {
+                m1 = ((volatile double *)smass)[rc];
+                x1 = ((volatile double *)sx)[rc];
+                y1 = ((volatile double *)sy)[rc];
+            } else {
+                Body b = bodies[~rc];
+                m1 = b.m;
+                x1 = mul(b.m, b.x);
+                y1 = mul(b.m, b.y);
+            }
+            double mm = add(m0, m1), xx = add(x0, x1), yy = add(y0, y1);
+            smass[node] = mm;
+            sx[node] = xx;
+            sy[node] = yy;
+            int dl = delta[node], pd = pdelta[node];
+            int kind;
+            if (dl >= 80)
+                kind = (pd < 80) ? 2 : 0;  // aggregate top (or never visited)
+            else
+                kind = (node == 0 || (pd >> 1) < (dl >> 1)) ? 1 : 0;
+            int lvl = dl >> 1;
+            double chalf = ldexp(g.half, -lvl);  // exact halvings
+            double side = 2.0 * chalf;
+            TNode t;
+            t.comx = xx / mm;
+            t.comy = yy / mm;
+            t.mass = mm;
+            t.side2 = mul(side, side);
+            t.left = l;
+            int lst = last[node];
+            t.skip = (lst == n - 1) ? END : rc_by_split[lst];
+            t.kind = kind;
+            t.pad = 0;
+            nodes[node] = t;
+            node = (node == 0) ? -1 : parent_int[node];
+        }
+    }
+}
+
+// ---- repulsion traversal ---------------------------------------------------
+__global__ void __launch_bounds__(FB) bh_kernel(const Body *__restrict__ bodies, int n,
+                                                const TNode *__restrict__ nodes,
+                                                const int *__restrict__ rc_by_split,
+                                                const int *__restrict__ first,
+                                                const int *__restrict__ last,
+                                                const double *__restrict__ smass,
+                                                const double *__restrict__ sx,
+                                                const double *__restrict__ sy, double kr,
+                                                double theta, double2 *__restrict__ out,
+                                                const long long *__restrict__ bad) {
+    if (bad && *bad) return;
+    const double th2 = mul(theta, theta);
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        Body me = bodies[p];
+        const long long i = me.orig;
+        const double xi = me.x, yi = me.y, mi = me.m;
+        double fx = 0.0, fy = 0.0;
+        int c = 0;  // root (n >= 2)
+        while (c != END) {
+            if (c < 0) {  // leaf body (C/layout.py:235-243)
+                int q = ~c;
+                if (q != p) {
+                    Body bj = bodies[q];
+                    double dx = sub(xi, bj.x), dy = sub(yi, bj.y);
+                    double d = separation(dx, dy, i, bj.orig);
+                    double f = mul(mul(kr, mi), bj.m) / mul(d, d);
+                    fx = add(fx, mul(f, dx));
+                    fy = add(fy, mul(f, dy));
+                }
+                c = (q == n - 1) ? END : __ldg(rc_by_split + q);
+                continue;
+            }
+            TNode t = nodes[c];
+            if (t.kind == 0) {  // inner half of a quad cell: always open
+                c = t.left;
+                continue;
+            }
+            double mc = t.mass, cx = t.comx, cy = t.comy;
+            if (t.kind == 2) {  // aggregate (C/layout.py:247-252)
+                if (p >= first[c] && p <= last[c]) {
+                    double m2 = sub(smass[c], mi);
+                    double x2 = sub(sx[c], mul(mi, xi)), y2 = sub(sy[c], mul(mi, yi));
+                    if (m2 <= 0.0) {
+                        c = t.skip;
+                        continue;
+                    }
+                    mc = m2;
+                    cx = x2 / m2;
+                    cy = y2 / m2;
+                }
+            }
+            double dx = sub(xi, cx), dy = sub(yi, cy);
+            double d2 = add(mul(dx, dx), mul(dy, dy));
+            if (t.kind == 2 || t.side2 < mul(th2, d2)) {  // (C/layout.py:256-261)
+                double d = separation(dx, dy, i, (long long)n + c);
+                double f = mul(mul(kr, mi), mc) / mul(d, d);
+                fx = add(fx, mul(f, dx));
+                fy = add(fy, mul(f, dy));
+                c = t.skip;
+            } else {
+                c = t.left;
+            }
+        }
+        out[i] = make_double2(fx, fy);
+    }
+}
+
+// exact O(n^2) (C/layout.py:273-290): j ascending, same op order as the CPU
+constexpr int XT = 256;
+__global__ void __launch_bounds__(XT) exact_kernel(const double2 *__restrict__ pos,
+                                                   const double *__restrict__ mass, int n,
+                                                   double kr, double2 *__restrict__ out) {
+    __shared__ double3 tile[XT];
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double xi = 0, yi = 0, mi = 0;
+    if (i < n) {
+        double2 p = pos[i];
+        xi = p.x;
+        yi = p.y;
+        mi = mass[i];
+    }
+    double fx = 0.0, fy = 0.0;
+    for (int j0 = 0; j0 < n; j0 += XT) {
+        int j = j0 + threadIdx.x;
+        if (j < n) {
+            double2 p = pos[j];
+            tile[threadIdx.x] = make_double3(p.x, p.y, mass[j]);
+        }
+        __syncthreads();
+        int lim = min(XT, n - j0);
+        if (i < n) {
+            for (int t = 0; t < lim; ++t) {
+                int jj = j0 + t;
+                if (jj == i) continue;
+                double3 q = tile[t];
+                double dx = sub(xi, q.x), dy = sub(yi, q.y);
+                double d = separation(dx, dy, i, jj);
+                double f = mul(mul(kr, mi), q.z) / mul(d, d);
+                fx = add(fx, mul(f, dx));
+                fy = add(fy, mul(f, dy));
+            }
+        }
+        __syncthreads();
+    }
+    if (i < n) out[i] = make_double2(fx, fy);
+}
+
+// ---- CSR for attraction ------------------------------------------------------
+__global__ void half_edges_kernel(const int2 *__restrict__ e, long long m,
+                                  unsigned *__restrict__ key, unsigned *__restrict__ val,
+                                  unsigned *__restrict__ cnt) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (long long)gridDim.x * blockDim.x) {
+        int2 p = e[k];
+        key[2 * k] = (unsigned)p.x;
+        key[2 * k + 1] = (unsigned)p.y;
+        val[2 * k] = (unsigned)(2 * k);
+        val[2 * k + 1] = (unsigned)(2 * k + 1);
+        atomicAdd(cnt + p.x, 1u);
+        atomicAdd(cnt + p.y, 1u);
+    }
+}
+
+// col = other endpoint; w = edge weight * sign (or sign)
+__global__ void csr_fill_kernel(const int2 *__restrict__ e, const unsigned *__restrict__ sval,
+                                long long nh, const double *__restrict__ w, double sign,
+                                int *__restrict__ col, double *__restrict__ cw) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < nh;
+         j += (long long)gridDim.x * blockDim.x) {
+        unsigned h = sval[j];
+        long long k = h >> 1;
+        int2 p = e[k];
+        col[j] = (h & 1) ? p.x : p.y;
+        cw[j] = mul(w ? w[k] : 1.0, sign);  // C/layout.py:300  w = weight[e] * sign
+    }
+}
+
+// ---- attraction + gravity + swing/traction (+ global speed in last block) ---
+struct StepScalars {
+    double speed;
+    double sum_swing, sum_traction;
+    long long it;       // iteration counter (0-based)
+    long long bad;      // first non-finite iteration (1-based), 0 = none
+    unsigned long long maxdisp_bits;
+};
+
+__global__ void __launch_bounds__(FB) forces_kernel(
+    const double2 *__restrict__ pos, const double *__restrict__ mass, int n,
+    const long long *__restrict__ rowptr, const int *__restrict__ col,
+    const double *__restrict__ cw, const double2 *__restrict__ frep, double gravity,
+    const double2 *__restrict__ prev, double2 *__restrict__ force, double *__restrict__ swing,
+    double *__restrict__ part, unsigned *__restrict__ ctr, StepScalars *__restrict__ sc,
+    double jt) {
+    if (sc->bad) return;
+    double s_sw = 0.0, s_tr = 0.0;
+    int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) {
+        double2 pu = pos[u];
+        double2 f = frep[u];
+        // springs in edge order (CSR rows are stably sorted by edge id)
+        for (long long j = rowptr[u]; j < rowptr[u + 1]; ++j) {
+            double2 pv = pos[col[j]];
+            double w = cw[j];
+            f.x = add(f.x, mul(w, sub(pv.x, pu.x)));
+            f.y = add(f.y, mul(w, sub(pv.y, pu.y)));
+        }
+        double mu = mass[u];
+        if (gravity > 0) {  // C/layout.py:307-309,370-371
+            double gm = mul(-gravity, mu);
+            f.x = add(f.x, mul(gm, pu.x));
+            f.y = add(f.y, mul(gm, pu.y));
+        }
+        force[u] = f;
+        double2 q = prev[u];
+        double diff = hypot(sub(f.x, q.x), sub(f.y, q.y));
+        double tot = hypot(add(f.x, q.x), add(f.y, q.y));
+        double sw = mul(mu, diff);
+        swing[u] = sw;
+        s_sw = sw;
+        s_tr = mul(mu, tot) / 2.0;
+    }
+    // deterministic block reduction
+    __shared__ double a[FB], b[FB];
+    a[threadIdx.x] = s_sw;
+    b[threadIdx.x] = s_tr;
+    __syncthreads();
+    for (int o = FB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            a[threadIdx.x] += a[threadIdx.x + o];
+            b[threadIdx.x] += b[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = a[0];
+        part[2 * blockIdx.x + 1] = b[0];
+        __threadfence();
+        last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double x = 0.0, y = 0.0;
+    for (unsigned k = threadIdx.x; k < gridDim.x; k += FB) {
+        x += ((volatile double *)part)[2 * k];
+        y += ((volatile double *)part)[2 * k + 1];
+    }
+    a[threadIdx.x] = x;
+    b[threadIdx.x] = y;
+    __syncthreads();
+    for (int o = FB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            a[threadIdx.x] += a[threadIdx.x + o];
+            b[threadIdx.x] += b[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double tsw = a[0], ttr = b[0];
+        sc->sum_swing = tsw;
+        sc->sum_traction = ttr;
+        if (tsw > 0) {  // C/layout.py:379-382
+            double target = mul(jt, ttr) / tsw;
+            sc->speed = fmin(target, 1.5 * sc->speed);
+        }
+        *ctr = 0;
+    }
+}
+
+__global__ void __launch_bounds__(FB) update_kernel(
+    double2 *__restrict__ pos, int n, const double2 *__restrict__ force,
+    const double *__restrict__ swing, double2 *__restrict__ prev, int speed_form,
+    double max_step, double *__restrict__ bpart, unsigned *__restrict__ ctr,
+    double *__restrict__ bbox, StepScalars *__restrict__ sc, double *__restrict__ disp_hist) {
+    if (sc->bad) return;
+    const double speed = sc->speed;
+    int u = blockIdx.x * blockDim.x + threadIdx.x;
+    double nrm = 0.0;
+    bool fin = true;
+    double a = INFINITY, b = -INFINITY, c = INFINITY, d = -INFINITY;
+    if (u < n) {
+        double sw = swing[u];
+        double local = speed_form == 0 ? speed / (1.0 + sqrt(mul(speed, sw)))
+                                       : speed / (1.0 + sqrt(add(speed, sw)));
+        double2 f = force[u];
+        double dx = mul(f.x, local), dy = mul(f.y, local);
+        nrm = hypot(dx, dy);
+        if (nrm > max_step) {  // C/layout.py:388-393
+            double sc2 = max_step / nrm;
+            dx = mul(dx, sc2);
+            dy = mul(dy, sc2);
+            nrm = max_step;
+        }
+        double2 p = pos[u];
+        p.x = add(p.x, dx);
+        p.y = add(p.y, dy);
+        pos[u] = p;
+        prev[u] = f;
+        fin = isfinite(p.x) && isfinite(p.y);
+        a = p.x;
+        b = p.x;
+        c = p.y;
+        d = p.y;
+    }
+    // block max |disp| (non-negative doubles order like their bit patterns)
+    __shared__ double sm[FB], s0[FB], s1[FB], s2[FB], s3[FB];
+    sm[threadIdx.x] = nrm;
+    s0[threadIdx.x] = a;
+    s1[threadIdx.x] = b;
+    s2[threadIdx.x] = c;
+    s3[threadIdx.x] = d;
+    bool anybad = __syncthreads_or(!fin);
+    for (int o = FB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + o]);
+            s0[threadIdx.x] = fmin(s0[threadIdx.x], s0[threadIdx.x + o]);
+            s1[threadIdx.x] = fmax(s1[threadIdx.x], s1[threadIdx.x + o]);
+            s2[threadIdx.x] = fmin(s2[threadIdx.x], s2[threadIdx.x + o]);
+            s3[threadIdx.x] = fmax(s3[threadIdx.x], s3[threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        bpart[5 * blockIdx.x + 0] = s0[0];
+        bpart[5 * blockIdx.x + 1] = s1[0];
+        bpart[5 * blockIdx.x + 2] = s2[0];
+        bpart[5 * blockIdx.x + 3] = s3[0];
+        bpart[5 * blockIdx.x + 4] = anybad ? -1.0 : sm[0];
+        __threadfence();
+        last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    volatile double *vp = bpart;
+    double mn_x = INFINITY, mx_x = -INFINITY, mn_y = INFINITY, mx_y = -INFINITY, md = 0.0;
+    bool bad = false;
+    for (unsigned k = 0; k < gridDim.x; ++k) {
+        mn_x = fmin(mn_x, vp[5 * k]);
+        mx_x = fmax(mx_x, vp[5 * k + 1]);
+        mn_y = fmin(mn_y, vp[5 * k + 2]);
+        mx_y = fmax(mx_y, vp[5 * k + 3]);
+        double v = vp[5 * k + 4];
+        if (v < 0) bad = true;
+        md = fmax(md, v);
+    }
+    bbox[0] = mn_x;
+    bbox[1] = mx_x;
+    bbox[2] = mn_y;
+    bbox[3] = mx_y;
+    long long it = sc->it;
+    disp_hist[it] = md;
+    if (bad) sc->bad = it + 1;  // C/layout.py:395-397 (1-based)
+    sc->it = it + 1;
+    *ctr = 0;
+}
+
+template <class K>
+size_t sort_bytes(int n, int bits) {
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, (const K *)nullptr, (K *)nullptr,
+                                    (const unsigned *)nullptr, (unsigned *)nullptr, n, 0, bits);
+    return tb;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Tree workspace: everything one repulsion evaluation needs, preallocated so
+// an iteration can be captured in a CUDA graph.
+struct Tree {
+    int n = 0;
+    unsigned long long *khi, *khi2, *khi3;
+    unsigned *klo, *klo2, *klo3, *idx, *idx2, *idx3;
+    Body *bodies;
+    int *left, *first, *last, *delta, *parent_int, *parent_leaf, *pdelta, *rc_by_split;
+    unsigned *visit;
+    double *smass, *sx, *sy;
+    TNode *nodes;
+    void *tmp;
+    size_t tmp_bytes;
+    void alloc(int n_, Scratch &sc) {
+        n = n_;
+        khi = sc.alloc<unsigned long long>(n);
+        khi2 = sc.alloc<unsigned long long>(n);
+        khi3 = sc.alloc<unsigned long long>(n);
+        klo = sc.alloc<unsigned>(n);
+        klo2 = sc.alloc<unsigned>(n);
+        klo3 = sc.alloc<unsigned>(n);
+        idx = sc.alloc<unsigned>(n);
+        idx2 = sc.alloc<unsigned>(n);
+        idx3 = sc.alloc<unsigned>(n);
+        bodies = sc.alloc<Body>(n);
+        int ni = n > 1 ? n - 1 : 1;
+        left = sc.alloc<int>(ni);
+        first = sc.alloc<int>(ni);
+        last = sc.alloc<int>(ni);
+        delta = sc.alloc<int>(ni);
+        parent_int = sc.alloc<int>(ni);
+        parent_leaf = sc.alloc<int>(n);
+        pdelta = sc.alloc<int>(ni);
+        rc_by_split = sc.alloc<int>(ni);
+        visit = sc.alloc<unsigned>(ni);
+        smass = sc.alloc<double>(ni);
+        sx = sc.alloc<double>(ni);
+        sy = sc.alloc<double>(ni);
+        nodes = sc.alloc<TNode>(ni);
+        tmp_bytes = std::max(sort_bytes<unsigned>(n, 32), sort_bytes<unsigned long long>(n, 64));
+        tmp = sc.alloc<char>(tmp_bytes);
+    }
+    // build from pos + bbox (bbox already on device)
+    void build(const double2 *pos, const double *mass, const double *bbox, cudaStream_t s) {
+        unsigned g = grid_for(n, FB, 1, 8);
+        CVZ_LAUNCH(keys_kernel, g, FB, 0, s, pos, (long long)n, bbox, khi, klo, idx);
+        size_t tb = tmp_bytes;
+        // LSD: low 8 digits first (16 bits), then the high 32 digits (64 bits)
+        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, klo, klo2, idx, idx2, n, 16, 32, s));
+        count_launches(3);
+        CVZ_LAUNCH(gather_hi_kernel, g, FB, 0, s, khi, idx2, (long long)n, khi2);
+        tb = tmp_bytes;
+        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, khi2, khi3, idx2, idx3, n, 0, 64, s));
+        count_launches(9);
+        CVZ_LAUNCH(gather_bodies_kernel, g, FB, 0, s, pos, mass, idx3, klo, (long long)n, bodies,
+                   klo3);
+        CVZ_CUDA(cudaMemsetAsync(visit, 0, sizeof(unsigned) * (n - 1), s));
+        Keys K{khi3, klo3, n};
+        CVZ_LAUNCH(karras_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, K, left, first, last, delta,
+                   parent_int, parent_leaf, pdelta, rc_by_split);
+        CVZ_LAUNCH(com_kernel, g, FB, 0, s, bodies, n, left, first, last, delta, parent_int,
+                   parent_leaf, pdelta, rc_by_split, visit, smass, sx, sy, bbox, nodes);
+    }
+    void repulse(double kr, double theta, double2 *out, const long long *bad, cudaStream_t s) {
+        CVZ_LAUNCH(bh_kernel, blocks_for(n, FB), FB, 0, s, bodies, n, nodes, rc_by_split, first,
+                   last, smass, sx, sy, kr, theta, out, bad);
+    }
+};
+
+static void bbox_dev(const double2 *pos, int n, double *bbox, Scratch &sc, cudaStream_t s,
+                     double **part_out = nullptr, unsigned **ctr_out = nullptr) {
+    unsigned g = grid_for(n, FB, 4, 2);
+    double *part = sc.alloc<double>(4 * g);
+    unsigned *ctr = sc.alloc<unsigned>(1);
+    CVZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+    CVZ_LAUNCH(bbox_kernel, g, FB, 0, s, pos, (long long)n, part, ctr, bbox);
+    (void)part_out;
+    (void)ctr_out;
+}
+
+void repulsion_dev(const double *pos, const double *mass, long long n, double kr, double theta,
+                   double *out, Scratch &sc, cudaStream_t s) {
+    auto *p2 = reinterpret_cast<const double2 *>(pos);
+    auto *o2 = reinterpret_cast<double2 *>(out);
+    if (n <= 1) {
+        CVZ_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 2 * (n > 0 ? n : 1), s));
+        return;
+    }
+    if (theta <= 0) {
+        CVZ_LAUNCH(exact_kernel, blocks_for(n, XT), XT, 0, s, p2, mass, (int)n, kr, o2);
+        return;
+    }
+    double *bbox = sc.alloc<double>(4);
+    bbox_dev(p2, (int)n, bbox, sc, s);
+    Tree t;
+    t.alloc((int)n, sc);
+    t.build(p2, mass, bbox, s);
+    t.repulse(kr, theta, o2, nullptr, s);
+}
+
+struct Csr {
+    long long *rowptr;
+    int *col;
+    double *w;
+};
+
+static Csr build_csr(const int2 *e, long long m, long long n, const double *weight, double sign,
+                     Scratch &sc, cudaStream_t s) {
+    Csr c;
+    long long nh = 2 * m;
+    c.rowptr = sc.alloc<long long>(n + 1);
+    c.col = sc.alloc<int>(nh);
+    c.w = sc.alloc<double>(nh);
+    unsigned *cnt = sc.alloc<unsigned>(n + 1);
+    CVZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (n + 1), s));
+    if (m > 0) {
+        unsigned *key = sc.alloc<unsigned>(nh), *val = sc.alloc<unsigned>(nh);
+        unsigned *skey = sc.alloc<unsigned>(nh), *sval = sc.alloc<unsigned>(nh);
+        CVZ_LAUNCH(half_edges_kernel, grid_for(m, FB, 1, 8), FB, 0, s, e, m, key, val, cnt);
+        int bits = 1;
+        while (bits < 32 && (1LL << bits) < n) ++bits;
+        size_t tb = 0;
+        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, skey, val, sval, (int)nh, 0,
+                                                 bits, s));
+        void *tmp = sc.alloc<char>(tb);
+        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, skey, val, sval, (int)nh, 0, bits,
+                                                 s));
+        count_launches(1 + (bits + 7) / 8);
+        CVZ_LAUNCH(csr_fill_kernel, grid_for(nh, FB, 1, 8), FB, 0, s, e, sval, nh, weight, sign,
+                   c.col, c.w);
+    }
+    // rowptr = exclusive scan of counts (n+1 entries, last = 2m)
+    size_t tb2 = 0;
+    CVZ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, c.rowptr, (int)(n + 1), s));
+    void *tmp2 = sc.alloc<char>(tb2);
+    CVZ_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, tb2, cnt, c.rowptr, (int)(n + 1), s));
+    count_launches(2);
+    return c;
+}
+
+__global__ void attraction_only_kernel(const double2 *__restrict__ pos, int n,
+                                       const long long *__restrict__ rowptr,
+                                       const int *__restrict__ col, const double *__restrict__ cw,
+                                       double2 *__restrict__ out) {
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        double2 pu = pos[u];
+        double2 f = out[u];
+        for (long long j = rowptr[u]; j < rowptr[u + 1]; ++j) {
+            double2 pv = pos[col[j]];
+            double w = cw[j];
+            f.x = add(f.x, mul(w, sub(pv.x, pu.x)));
+            f.y = add(f.y, mul(w, sub(pv.y, pu.y)));
+        }
+        out[u] = f;
+    }
+}
+
+}  // namespace cvz
+
+using namespace cvz;
+
+extern "C" {
+
+int cvz_repulsion(const double *pos, const double *mass, int64_t n, double repulsion,
+                  double theta, double *out, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(n >= 0 && n < (1LL << 30), CVZ_ERR_VALUE, "bad body count");
+        cudaStream_t s = as_stream(stream);
+        Scratch sc(s);
+        repulsion_dev(pos, mass, n, repulsion, theta, out, sc, s);
+    });
+}
+
+int cvz_attraction(const double *pos, int64_t n, const int32_t *edges, int64_t m,
+                   const double *weight, double sign, double *out, void *stream) {
+    return guard([&] {
+        cudaStream_t s = as_stream(stream);
+        Scratch sc(s);
+        if (n <= 0 || m <= 0) return;
+        Csr c = build_csr(reinterpret_cast<const int2 *>(edges), m, n, weight, sign, sc, s);
+        CVZ_LAUNCH(attraction_only_kernel, grid_for(n, FB, 1, 8), FB, 0, s,
+                   reinterpret_cast<const double2 *>(pos), (int)n, c.rowptr, c.col, c.w,
+                   reinterpret_cast<double2 *>(out));
+    });
+}
+
+int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *edges, int64_t m,
+                   const double *weight, const cvz_layout_params *P, double *prev_force,
+                   double *speed, double *disp_hist, int64_t *bad_iteration, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(n >= 2 && n < (1LL << 30), CVZ_ERR_VALUE, "layout needs 2 <= n < 2^30");
+        CVZ_REQUIRE(P->iterations >= 1, CVZ_ERR_VALUE, "iterations must be positive");
+        cudaStream_t s = as_stream(stream);
+        Scratch sc(s);
+        const int N = (int)n;
+        auto *p2 = reinterpret_cast<double2 *>(pos);
+        auto *prev = reinterpret_cast<double2 *>(prev_force);
+        double sign = P->attraction_form == 0 ? 1.0 : -1.0;
+        Csr csr = build_csr(reinterpret_cast<const int2 *>(edges), m, n, weight, sign, sc, s);
+        double2 *frep = sc.alloc<double2>(n), *force = sc.alloc<double2>(n);
+        double *swing = sc.alloc<double>(n);
+        unsigned nb = blocks_for(n, FB);
+        double *fpart = sc.alloc<double>(2 * nb), *upart = sc.alloc<double>(5 * nb);
+        unsigned *ctrs = sc.alloc<unsigned>(2);
+        CVZ_CUDA(cudaMemsetAsync(ctrs, 0, 2 * sizeof(unsigned), s));
+        double *bbox = sc.alloc<double>(4);
+        StepScalars *scal = sc.alloc<StepScalars>(1);
+        StepScalars init{};
+        CVZ_CUDA(cudaMemcpyAsync(&init.speed, speed, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CVZ_CUDA(cudaStreamSynchronize(s));
+        CVZ_CUDA(cudaMemcpyAsync(scal, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+        const bool exact = P->theta <= 0;
+        Tree tree;
+        if (!exact) tree.alloc(N, sc);
+        bbox_dev(p2, N, bbox, sc, s);  // first bbox; later ones come from update
+        long long *badp = &scal->bad;
+
+        auto one_iteration = [&](cudaStream_t st) {
+            if (exact) {
+                CVZ_LAUNCH(exact_kernel, blocks_for(n, XT), XT, 0, st, p2, mass, N, P->repulsion,
+                           frep);
+            } else {
+                tree.build(p2, mass, bbox, st);
+                tree.repulse(P->repulsion, P->theta, frep, badp, st);
+            }
+            CVZ_LAUNCH(forces_kernel, nb, FB, 0, st, p2, mass, N, csr.rowptr, csr.col, csr.w, frep,
+                       P->gravity, prev, force, swing, fpart, ctrs, scal, P->jitter_tolerance);
+            CVZ_LAUNCH(update_kernel, nb, FB, 0, st, p2, N, force, swing, prev, P->speed_form,
+                       P->max_step, upart, ctrs + 1, bbox, scal, disp_hist);
+        };
+
+        bool use_graph = getenv("CVZ_NO_GRAPH") == nullptr && P->iterations > 1;
+        if (use_graph) {
+            // capture one iteration on a private stream, then replay
+            cudaStream_t cs;
+            CVZ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            cudaEvent_t ev;
+            CVZ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CVZ_CUDA(cudaEventRecord(ev, s));
+            CVZ_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+            cudaGraph_t graph = nullptr;
+            cudaGraphExec_t exec = nullptr;
+            long long before = g_launches.load();
+            CVZ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            bool ok = true;
+            try {
+                one_iteration(cs);
+            } catch (...) {
+                ok = false;
+            }
+            cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+            long long per_iter = g_launches.load() - before;
+            g_launches.fetch_sub(per_iter);
+            if (ok && ce == cudaSuccess &&
+                cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+                for (long long it = 0; it < P->iterations; ++it) {
+                    CVZ_CUDA(cudaGraphLaunch(exec, cs));
+                    g_launches.fetch_add(per_iter);
+                }
+                CVZ_CUDA(cudaEventRecord(ev, cs));
+                CVZ_CUDA(cudaStreamWaitEvent(s, ev, 0));
+            } else {
+                cudaGetLastError();
+                use_graph = false;
+            }
+            if (exec) cudaGraphExecDestroy(exec);
+            if (graph) cudaGraphDestroy(graph);
+            CVZ_CUDA(cudaStreamSynchronize(cs));
+            cudaStreamDestroy(cs);
+            cudaEventDestroy(ev);
+        }
+        if (!use_graph)
+            for (long long it = 0; it < P->iterations; ++it) one_iteration(s);
+        StepScalars out;
+        CVZ_CUDA(cudaMemcpyAsync(&out, scal, sizeof(out), cudaMemcpyDeviceToHost, s));
+        CVZ_CUDA(cudaStreamSynchronize(s));
+        CVZ_CUDA(cudaMemcpyAsync(speed, &out.speed, sizeof(double), cudaMemcpyHostToDevice, s));
+        *bad_iteration = out.bad;
+        if (out.bad)
+            throw Error(CVZ_ERR_LAYOUT, "non-finite positions at iteration " +
+                                            std::to_string(out.bad) +
+                                            "; reduce speed or check input weights");
+        CVZ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,293 @@
+// Graph ingestion: stable self-loop compaction, degree histogram, degree stats.
+// Reference: C/graph.py:114-136 (from_edge_array, degree_stats).
+//
+// HBM-bound streaming kernels.  Edges are read as 128-bit vectors (one int64
+// pair or two int32 pairs per load), each CTA owns a contiguous tile so the
+// compaction stays stable, and the tile offset comes from a single-pass
+// decoupled look-back (no second pass over the edges).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace cvz {
+
+std::atomic<long long> g_launches{0};
+static thread_local std::string t_last_error;
+void set_last_error(const std::string &m) { t_last_error = m; }
+
+void init_pool_once() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done = true;
+}
+
+namespace {
+
+constexpr int CBLOCK = 256;
+constexpr int CITEMS = 8;  // edges per thread
+constexpr int CTILE = CBLOCK * CITEMS;
+
+template <bool IN32>
+__global__ void __launch_bounds__(CBLOCK) compact_edges_kernel(
+    const void *__restrict__ in, long long m, int2 *__restrict__ out, LookbackState st,
+    unsigned long long *__restrict__ d_count, long long *__restrict__ d_max,
+    int *__restrict__ d_bad, unsigned num_tiles) {
+    __shared__ unsigned s_tile;
+    __shared__ unsigned long long s_prefix;
+    __shared__ int s_warp[CBLOCK / 32];
+    __shared__ long long s_max[CBLOCK / 32];
+    const unsigned tile = acquire_tile(st, &s_tile);
+    const long long base = (long long)tile * CTILE;
+
+    int2 e[CITEMS];
+    bool keep[CITEMS];
+    int cnt = 0;
+    long long mx = -1;
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < CITEMS; ++j) {
+        long long i = base + (long long)j * CBLOCK + threadIdx.x;  // coalesced
+        keep[j] = false;
+        if (i < m) {
+            long long u, v;
+            if (IN32) {
+                int2 p = __ldg(reinterpret_cast<const int2 *>(in) + i);
+                u = p.x;
+                v = p.y;
+            } else {
+                longlong2 p = __ldg(reinterpret_cast<const longlong2 *>(in) + i);  // 128-bit
+                u = p.x;
+                v = p.y;
+            }
+            bad |= (u < 0) | (v < 0) | (u > 0x7fffffffLL) | (v > 0x7fffffffLL);
+            e[j] = make_int2((int)u, (int)v);
+            keep[j] = (u != v);
+            if (keep[j]) {
+                cnt++;
+                mx = max(mx, max(u, v));
+            }
+        }
+    }
+    int total;
+    int off = block_exclusive_scan<CBLOCK>(cnt, s_warp, total);
+    unsigned long long prefix = tile_prefix(st, tile, (unsigned long long)total, &s_prefix);
+    // Items are strided by CBLOCK inside the tile, so a thread's kept items
+    // are not contiguous in stream order: recompute a per-slot ordinal.
+    // Rank of (j, tid) in tile order = sum over j' < j of all kept + rank in slot j.
+    // Do it slot-by-slot with a block scan per slot (CITEMS scans).
+    __syncthreads();
+    (void)off;
+    long long run = 0;
+#pragma unroll
+    for (int j = 0; j < CITEMS; ++j) {
+        int tot_j;
+        int o = block_exclusive_scan<CBLOCK>(keep[j] ? 1 : 0, s_warp, tot_j);
+        if (keep[j]) out[prefix + run + o] = e[j];
+        run += tot_j;
+    }
+    // max + range flag
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane_id() == 0) s_max[threadIdx.x >> 5] = mx;
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        long long b = -1;
+        for (int w = 0; w < CBLOCK / 32; ++w) b = max(b, s_max[w]);
+        if (b >= 0) atomicMax(reinterpret_cast<unsigned long long *>(d_max), (unsigned long long)b);
+        if (bad) atomicExch(d_bad, 1);
+        if (tile == num_tiles - 1) *d_count = prefix + total;
+    }
+}
+
+// degree[x] += endpoint count.  64-bit RED into an L2-resident n-array.
+__global__ void degree_kernel(const int4 *__restrict__ e2, long long npairs2,
+                              const int2 *__restrict__ e, long long m,
+                              unsigned long long *__restrict__ deg) {
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < npairs2;
+         i += stride) {
+        int4 p = __ldg(e2 + i);  // two edges per 128-bit load
+        atomicAdd(deg + p.x, 1ull);
+        atomicAdd(deg + p.y, 1ull);
+        atomicAdd(deg + p.z, 1ull);
+        atomicAdd(deg + p.w, 1ull);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (m & 1)) {
+        int2 p = e[m - 1];
+        atomicAdd(deg + p.x, 1ull);
+        atomicAdd(deg + p.y, 1ull);
+    }
+}
+
+// sum / max / histogram of nonzero degrees (mode).
+__global__ void degree_summary_kernel(const long long *__restrict__ deg, long long n,
+                                      unsigned long long *__restrict__ sum,
+                                      unsigned long long *__restrict__ mx) {
+    unsigned long long s = 0, m = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long d = (unsigned long long)deg[i];
+        s += d;
+        m = max(m, d);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+    if (lane_id() == 0) {
+        atomicAdd(sum, s);
+        atomicMax(mx, m);
+    }
+}
+
+constexpr int SMEM_BINS = 4096;
+__global__ void degree_hist_kernel(const long long *__restrict__ deg, long long n,
+                                   unsigned int *__restrict__ hist, long long nbins) {
+    __shared__ unsigned int sh[SMEM_BINS];
+    for (int i = threadIdx.x; i < SMEM_BINS; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        long long d = deg[i];
+        if (d > 0) {
+            if (d < SMEM_BINS)
+                atomicAdd(&sh[d], 1u);
+            else
+                atomicAdd(&hist[d], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < SMEM_BINS && i < nbins; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// argmax over the histogram, ties -> smallest degree (np.argmax semantics).
+__global__ void hist_argmax_kernel(const unsigned int *__restrict__ hist, long long nbins,
+                                   unsigned long long *__restrict__ best) {
+    unsigned long long b = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nbins;
+         i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long key = ((unsigned long long)hist[i] << 32) |
+                                 (0xffffffffull - (unsigned long long)i);
+        b = max(b, key);
+    }
+    for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    if (lane_id() == 0) atomicMax(best, b);
+}
+
+__global__ void stats_finalize_kernel(const unsigned long long *__restrict__ sum,
+                                      const unsigned long long *__restrict__ mx,
+                                      const unsigned long long *__restrict__ best,
+                                      long long *__restrict__ out3) {
+    unsigned long long b = *best;
+    long long mode = (b >> 32) ? (long long)(0xffffffffull - (b & 0xffffffffull)) : 0;
+    out3[0] = mode;
+    out3[1] = (long long)*sum;
+    out3[2] = (long long)*mx;
+}
+
+}  // namespace
+
+void edges_compact(const void *edges, bool in32, int64_t m, int32_t *out, int64_t *d_m_out,
+                   int64_t *d_max, int *d_bad, cudaStream_t s) {
+    Scratch sc(s);
+    unsigned tiles = (unsigned)((m + CTILE - 1) / CTILE);
+    if (tiles == 0) tiles = 1;
+    auto *status = sc.alloc<unsigned long long>(tiles);
+    auto *ctr = sc.alloc<unsigned>(1);
+    CVZ_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * tiles, s));
+    CVZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+    CVZ_CUDA(cudaMemsetAsync(d_m_out, 0, sizeof(int64_t), s));
+    // max id starts at 0; callers treat *d_m_out == 0 as "no edges, n = 0"
+    CVZ_CUDA(cudaMemsetAsync(d_max, 0, sizeof(int64_t), s));
+    LookbackState st{status, ctr};
+    if (in32)
+        CVZ_LAUNCH(compact_edges_kernel<true>, tiles, CBLOCK, 0, s, edges, (long long)m,
+                   reinterpret_cast<int2 *>(out), st,
+                   reinterpret_cast<unsigned long long *>(d_m_out),
+                   reinterpret_cast<long long *>(d_max), d_bad, tiles);
+    else
+        CVZ_LAUNCH(compact_edges_kernel<false>, tiles, CBLOCK, 0, s, edges, (long long)m,
+                   reinterpret_cast<int2 *>(out), st,
+                   reinterpret_cast<unsigned long long *>(d_m_out),
+                   reinterpret_cast<long long *>(d_max), d_bad, tiles);
+}
+
+void degree_count(const int32_t *edges, int64_t m, int64_t n, int64_t *degree,
+                  cudaStream_t s) {
+    CVZ_CUDA(cudaMemsetAsync(degree, 0, sizeof(int64_t) * (n ? n : 1), s));
+    if (m == 0) return;
+    long long pairs2 = m / 2;
+    unsigned grid = grid_for(pairs2 > 0 ? pairs2 : 1, 256, 1, 16);
+    CVZ_LAUNCH(degree_kernel, grid, 256, 0, s, reinterpret_cast<const int4 *>(edges), pairs2,
+               reinterpret_cast<const int2 *>(edges), (long long)m,
+               reinterpret_cast<unsigned long long *>(degree));
+}
+
+void degree_stats(const int64_t *degree, int64_t n, int64_t *out3, cudaStream_t s) {
+    Scratch sc(s);
+    auto *acc = sc.alloc<unsigned long long>(3);  // sum, max, best
+    CVZ_CUDA(cudaMemsetAsync(acc, 0, 3 * sizeof(unsigned long long), s));
+    unsigned grid = grid_for(n, 256, 4, 4);
+    CVZ_LAUNCH(degree_summary_kernel, grid, 256, 0, s, reinterpret_cast<const long long *>(degree),
+               (long long)n, acc, acc + 1);
+    // bins sized by the max degree: read it back (tiny sync, host API is sync)
+    unsigned long long mx = 0;
+    CVZ_CUDA(cudaMemcpyAsync(&mx, acc + 1, sizeof(mx), cudaMemcpyDeviceToHost, s));
+    CVZ_CUDA(cudaStreamSynchronize(s));
+    long long nbins = (long long)mx + 1;
+    auto *hist = sc.alloc<unsigned int>(nbins > SMEM_BINS ? nbins : SMEM_BINS);
+    CVZ_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned) * (nbins > SMEM_BINS ? nbins : SMEM_BINS), s));
+    CVZ_LAUNCH(degree_hist_kernel, grid, 256, 0, s, reinterpret_cast<const long long *>(degree),
+               (long long)n, hist, nbins);
+    CVZ_LAUNCH(hist_argmax_kernel, grid_for(nbins, 256, 4, 2), 256, 0, s, hist, nbins, acc + 2);
+    CVZ_LAUNCH(stats_finalize_kernel, 1, 1, 0, s, acc, acc + 1, acc + 2,
+               reinterpret_cast<long long *>(out3));
+}
+
+}  // namespace cvz
+
+using namespace cvz;
+
+extern "C" {
+
+int cvz_version(void) { return 1; }
+const char *cvz_last_error(void) { return t_last_error.c_str(); }
+long long cvz_launch_count(void) { return g_launches.load(); }
+
+int cvz_edges_compact(const void *edges, int in_is_int32, int64_t m, int32_t *edges_out,
+                      int64_t *d_m_out, int64_t *d_max_id, int check_range, void *stream) {
+    return guard([&] {
+        cudaStream_t s = as_stream(stream);
+        Scratch sc(s);
+        int *bad = sc.alloc<int>(1);
+        CVZ_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+        edges_compact(edges, in_is_int32 != 0, m, edges_out, d_m_out, d_max_id, bad, s);
+        if (check_range) {
+            int hbad = 0;
+            CVZ_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CVZ_CUDA(cudaStreamSynchronize(s));
+            CVZ_REQUIRE(!hbad, CVZ_ERR_RANGE, "node ids must lie in [0, 2^31)");
+        }
+    });
+}
+
+int cvz_degree_count(const int32_t *edges, int64_t m, int64_t n, int64_t *degree,
+                     void *stream) {
+    return guard([&] { degree_count(edges, m, n, degree, as_stream(stream)); });
+}
+
+int cvz_degree_stats(const int64_t *degree, int64_t n, int64_t *out3, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(n > 0, CVZ_ERR_VALUE, "degree stats need n > 0");
+        degree_stats(degree, n, out3, as_stream(stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,261 @@
+// Count-min sketch: Carter-Wegman hashing over the Mersenne prime, weighted
+// saturating adds, row-wise-min estimates.  Reference: C/sketch.py:39-98 and
+// C/supergraph.py:42-46 (accumulate_sizes).
+//
+// Adds are integer additions mod 2^64, so any interleaving of atomics gives
+// the same table as numpy's sequential np.add.at; the wrap -> INT64_MAX
+// saturation runs once afterwards exactly like C/sketch.py:80-86.
+//
+// Two add paths:
+//  * staged: the whole rows x cols table lives in shared memory as u64
+//    (default 4 x 6500 = 208 KB fits one CTA per SM); each CTA accumulates
+//    its slice of keys there with warp-aggregated shared atomics and flushes
+//    only non-zero cells with one global 64-bit RED each;
+//  * direct: warp-aggregated 64-bit global atomics into the L2-resident table
+//    for tables too big for shared memory (e.g. 4 x 107,375 at 2^30 edges).
+#include "common.cuh"
+
+namespace cvz {
+namespace {
+
+constexpr unsigned long long P31 = 0x7fffffffull;  // 2^31 - 1
+
+__device__ __forceinline__ unsigned long long key_mod_p(long long x) {
+    // numpy: x % p with a non-negative result for negative x
+    if (x >= 0 && x < (long long)P31) return (unsigned long long)x;
+    long long r = x % (long long)P31;
+    if (r < 0) r += (long long)P31;
+    return (unsigned long long)r;
+}
+
+// ((a*x + b) mod p) mod cols with a, x < 2^31, b < 2^31: y < 2^62 + 2^31.
+__device__ __forceinline__ unsigned hash_col(unsigned long long a, unsigned long long b,
+                                             unsigned long long xm, unsigned cols) {
+    unsigned long long y = a * xm + b;
+    y = (y & P31) + (y >> 31);  // < 2^31 + 2^32
+    y = (y & P31) + (y >> 31);  // < 2^31 + 2
+    if (y >= P31) y -= P31;
+    return (unsigned)y % cols;
+}
+
+__global__ void indices_kernel(const long long *__restrict__ ha, const long long *__restrict__ hb,
+                               int rows, unsigned cols, const long long *__restrict__ keys,
+                               long long k, long long *__restrict__ idx) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < k;
+         j += (long long)gridDim.x * blockDim.x) {
+        unsigned long long xm = key_mod_p(keys[j]);
+        for (int r = 0; r < rows; ++r)
+            idx[(long long)r * k + j] = hash_col(ha[r], hb[r], xm, cols);
+    }
+}
+
+__global__ void negative_check_kernel(const long long *__restrict__ a, long long k,
+                                      int *__restrict__ flag) {
+    bool neg = false;
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < k;
+         j += (long long)gridDim.x * blockDim.x)
+        neg |= a[j] < 0;
+    if (__any_sync(0xffffffffu, neg) && lane_id() == 0) atomicExch(flag, 1);
+}
+
+// Warp-level aggregation: lanes hitting the same cell combine their amounts
+// (match_any on the cell index) and only the leader issues the atomic.
+template <bool SHARED>
+__device__ __forceinline__ void agg_add(unsigned long long *base, unsigned cell,
+                                        unsigned long long amt, bool valid) {
+    unsigned active = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    unsigned peers = __match_any_sync(active, cell);
+    int leader = __ffs(peers) - 1;
+    // reduce amounts over peers (sum mod 2^64)
+    unsigned long long sum = 0;
+    unsigned rest = peers;
+    while (rest) {
+        int l = __ffs(rest) - 1;
+        unsigned long long v = __shfl_sync(peers, amt, l);
+        sum += v;
+        rest &= rest - 1;
+    }
+    if (lane_id() == leader) atomicAdd(base + cell, sum);
+}
+
+__global__ void add_direct_kernel(unsigned long long *__restrict__ table,
+                                  const long long *__restrict__ ha,
+                                  const long long *__restrict__ hb, int rows, unsigned cols,
+                                  const long long *__restrict__ keys,
+                                  const long long *__restrict__ amounts, long long k) {
+    long long stride = (long long)gridDim.x * blockDim.x;
+    long long kk = (k + 31) / 32 * 32;  // whole warps iterate together
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < kk; j += stride) {
+        bool valid = j < k;
+        unsigned long long xm = valid ? key_mod_p(keys[j]) : 0;
+        unsigned long long amt = valid ? (unsigned long long)amounts[j] : 0;
+        for (int r = 0; r < rows; ++r) {
+            unsigned c = valid ? hash_col(ha[r], hb[r], xm, cols) : 0;
+            agg_add<false>(table + (size_t)r * cols, c, amt, valid && amt != 0);
+        }
+    }
+}
+
+__global__ void add_staged_kernel(unsigned long long *__restrict__ table,
+                                  const long long *__restrict__ ha,
+                                  const long long *__restrict__ hb, int rows, unsigned cols,
+                                  const long long *__restrict__ keys,
+                                  const long long *__restrict__ amounts, long long k) {
+    extern __shared__ unsigned long long sh[];
+    const unsigned cells = rows * cols;
+    for (unsigned i = threadIdx.x; i < cells; i += blockDim.x) sh[i] = 0;
+    __shared__ long long s_a[8], s_b[8];
+    if (threadIdx.x < rows) {
+        s_a[threadIdx.x] = ha[threadIdx.x];
+        s_b[threadIdx.x] = hb[threadIdx.x];
+    }
+    __syncthreads();
+    // contiguous slice per CTA
+    long long per = (k + gridDim.x - 1) / gridDim.x;
+    long long lo = (long long)blockIdx.x * per, hi = min(k, lo + per);
+    for (long long j0 = lo; j0 < hi; j0 += blockDim.x) {
+        long long j = j0 + threadIdx.x;
+        bool valid = j < hi;
+        unsigned long long xm = valid ? key_mod_p(keys[j]) : 0;
+        unsigned long long amt = valid ? (unsigned long long)amounts[j] : 0;
+        for (int r = 0; r < rows; ++r) {
+            unsigned c = valid ? hash_col(s_a[r], s_b[r], xm, cols) : 0;
+            agg_add<true>(sh + (size_t)r * cols, c, amt, valid && amt != 0);
+        }
+    }
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < cells; i += blockDim.x)
+        if (sh[i]) atomicAdd(table + i, sh[i]);
+}
+
+__global__ void saturate_kernel(long long *__restrict__ table, long long cells,
+                                int *__restrict__ flag) {
+    bool wrapped = false;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cells;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (table[i] < 0) {
+            table[i] = 0x7fffffffffffffffLL;
+            wrapped = true;
+        }
+    }
+    if (__any_sync(0xffffffffu, wrapped) && lane_id() == 0) atomicExch(flag, 1);
+}
+
+__global__ void estimate_kernel(const long long *__restrict__ table, int rows, unsigned cols,
+                                const long long *__restrict__ ha,
+                                const long long *__restrict__ hb,
+                                const long long *__restrict__ keys, long long k,
+                                long long *__restrict__ out) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < k;
+         j += (long long)gridDim.x * blockDim.x) {
+        unsigned long long xm = key_mod_p(keys[j]);
+        long long best = 0x7fffffffffffffffLL;
+        for (int r = 0; r < rows; ++r)
+            best = min(best, table[(size_t)r * cols + hash_col(ha[r], hb[r], xm, cols)]);
+        out[j] = best;
+    }
+}
+
+constexpr size_t STAGED_MAX_BYTES = 220 * 1024;
+
+}  // namespace
+
+void sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *ha, const int64_t *hb,
+                const int64_t *keys, const int64_t *amounts, int64_t k, int32_t *d_sat,
+                cudaStream_t s) {
+    if (k > 0) {
+        size_t bytes = (size_t)rows * cols * sizeof(unsigned long long);
+        bool staged = rows <= 8 && bytes <= STAGED_MAX_BYTES && k >= 4 * (long long)rows * cols;
+        auto *t = reinterpret_cast<unsigned long long *>(table);
+        auto *kk = reinterpret_cast<const long long *>(keys);
+        auto *aa = reinterpret_cast<const long long *>(amounts);
+        auto *pa = reinterpret_cast<const long long *>(ha);
+        auto *pb = reinterpret_cast<const long long *>(hb);
+        if (staged) {
+            static bool attr = false;
+            if (!attr) {
+                CVZ_CUDA(cudaFuncSetAttribute(add_staged_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)STAGED_MAX_BYTES));
+                attr = true;
+            }
+            // enough CTAs to fill the chip once; each flushes <= rows*cols cells
+            long long want = k / (8LL * rows * cols) + 1;
+            unsigned grid = (unsigned)std::min<long long>(want, num_sms());
+            CVZ_LAUNCH(add_staged_kernel, grid, 1024, bytes, s, t, pa, pb, rows, (unsigned)cols,
+                       kk, aa, (long long)k);
+        } else {
+            CVZ_LAUNCH(add_direct_kernel, grid_for(k, 256, 1, 8), 256, 0, s, t, pa, pb, rows,
+                       (unsigned)cols, kk, aa, (long long)k);
+        }
+    }
+    long long cells = (long long)rows * cols;
+    CVZ_LAUNCH(saturate_kernel, grid_for(cells, 256, 4, 2), 256, 0, s,
+               reinterpret_cast<long long *>(table), cells, d_sat);
+}
+
+void sketch_estimate(const int64_t *table, int rows, int64_t cols, const int64_t *ha,
+                     const int64_t *hb, const int64_t *keys, int64_t k, int64_t *out,
+                     cudaStream_t s) {
+    if (k <= 0) return;
+    CVZ_LAUNCH(estimate_kernel, grid_for(k, 256, 1, 8), 256, 0, s,
+               reinterpret_cast<const long long *>(table), rows, (unsigned)cols,
+               reinterpret_cast<const long long *>(ha), reinterpret_cast<const long long *>(hb),
+               reinterpret_cast<const long long *>(keys), (long long)k,
+               reinterpret_cast<long long *>(out));
+}
+
+}  // namespace cvz
+
+using namespace cvz;
+
+extern "C" {
+
+int cvz_sketch_indices(const int64_t *hash_a, const int64_t *hash_b, int rows, int64_t cols,
+                       const int64_t *keys, int64_t k, int64_t *idx, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(rows >= 1 && cols >= 1 && cols < (1LL << 31), CVZ_ERR_VALUE,
+                    "sketch needs 1 <= cols < 2^31 and rows >= 1");
+        if (k <= 0) return;
+        CVZ_LAUNCH(indices_kernel, grid_for(k, 256, 1, 8), 256, 0, as_stream(stream),
+                   reinterpret_cast<const long long *>(hash_a),
+                   reinterpret_cast<const long long *>(hash_b), rows, (unsigned)cols,
+                   reinterpret_cast<const long long *>(keys), (long long)k,
+                   reinterpret_cast<long long *>(idx));
+    });
+}
+
+int cvz_sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *hash_a,
+                   const int64_t *hash_b, const int64_t *keys, const int64_t *amounts,
+                   int64_t k, int validate, int32_t *d_saturated, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(rows >= 1 && cols >= 1 && cols < (1LL << 31), CVZ_ERR_VALUE,
+                    "sketch needs 1 <= cols < 2^31 and rows >= 1");
+        cudaStream_t s = as_stream(stream);
+        if (validate && k > 0) {
+            Scratch sc(s);
+            int *flag = sc.alloc<int>(1);
+            CVZ_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+            CVZ_LAUNCH(negative_check_kernel, grid_for(k, 256, 4, 4), 256, 0, s,
+                       reinterpret_cast<const long long *>(amounts), (long long)k, flag);
+            int h = 0;
+            CVZ_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CVZ_CUDA(cudaStreamSynchronize(s));
+            CVZ_REQUIRE(!h, CVZ_ERR_VALUE, "amounts must be non-negative");
+        }
+        sketch_add(table, rows, cols, hash_a, hash_b, keys, amounts, k, d_saturated, s);
+    });
+}
+
+int cvz_sketch_estimate(const int64_t *table, int rows, int64_t cols, const int64_t *hash_a,
+                        const int64_t *hash_b, const int64_t *keys, int64_t k, int64_t *out,
+                        void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(rows >= 1 && cols >= 1 && cols < (1LL << 31), CVZ_ERR_VALUE,
+                    "sketch needs 1 <= cols < 2^31 and rows >= 1");
+        sketch_estimate(table, rows, cols, hash_a, hash_b, keys, k, out, as_stream(stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+"""Graph ingestion (drop-in for C/graph.py).
+
+`from_edge_array` and `degree_stats` run on the GPU (cvz_edges_compact,
+cvz_degree_count, cvz_degree_stats).  The edge list stays on the device as
+int32 pairs in stream order; `Graph.edges` / `Graph.degree` materialise int64
+numpy arrays only when read.
+"""
+
+from __future__ import annotations
+
+import io
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from ._dual import Dual
+
+
+class ParseError(ValueError):
+    """C/graph.py:20-21."""
+
+
+class Graph:
+    """Immutable undirected multigraph over dense ids (C/graph.py:24-40)."""
+
+    __slots__ = ("node_count", "_edges", "_degree", "_edges32")
+
+    def __init__(self, node_count: int, edges, degree):
+        edges = np.asarray(edges)
+        degree = np.asarray(degree)
+        if edges.ndim != 2 or edges.shape[1] != 2:
+            raise ValueError("edges must be an (m, 2) array")
+        if int(degree.sum()) != 2 * len(edges):
+            raise ValueError("degree sum must equal twice the edge count")
+        self.node_count = int(node_count)
+        self._edges = Dual(host=edges)
+        self._degree = Dual(host=degree)
+        self._edges32 = None
+
+    @classmethod
+    def _from_device(cls, n: int, edges32, degree64):
+        g = object.__new__(cls)
+        g.node_count = int(n)
+        g._edges = Dual(dev=edges32)
+        g._degree = Dual(dev=degree64)
+        g._edges32 = edges32
+        return g
+
+    @property
+    def edges(self) -> np.ndarray:
+        return self._edges.host()
+
+    @property
+    def degree(self) -> np.ndarray:
+        return self._degree.host()
+
+    @property
+    def edge_count(self) -> int:
+        return len(self._edges)
+
+    # device views used by the kernels
+    def edges_dev(self):
+        """(m, 2) int32 CUDA tensor in stream order."""
+        if self._edges32 is None:
+            T = nat.torch()
+            e = self._edges.host()
+            if len(e) and (e.min() < 0 or e.max() >= 2**31):
+                raise ValueError("node ids must lie in [0, 2^31)")
+            self._edges32 = nat.to_dev(e.reshape(-1, 2), T.int32)
+        return self._edges32
+
+    def degree_dev(self):
+        return self._degree.dev(nat.torch().int64)
+
+    def __repr__(self):
+        return f"Graph(node_count={self.node_count}, edge_count={self.edge_count})"
+
+
+@dataclass(frozen=True)
+class DegreeStats:
+    """C/graph.py:43-47."""
+
+    mode_degree: int
+    average_degree: float
+    max_degree: int
+
+
+def parse_edge_list(text) -> Graph:
+    """C/graph.py:50-92: SNAP-style text -> Graph (first-seen id remap,
+    comments `#`/`%`, self-loops dropped, duplicates kept).
+
+    Tokenising is host work; the degree histogram runs on the GPU."""
+    if isinstance(text, bytes):
+        text = text.decode("utf-8", errors="replace")
+    lines = text.splitlines() if isinstance(text, str) else [
+        ln.decode() if isinstance(ln, bytes) else ln for ln in text]
+    ids: dict[int, int] = {}
+    flat: list[int] = []
+    for no, raw in enumerate(lines, start=1):
+        s = raw.strip()
+        if not s or s[0] in "#%":
+            continue
+        tok = s.split()
+        if len(tok) != 2:
+            raise ParseError(f"line {no}: expected two tokens, got {len(tok)}")
+        try:
+            a, b = int(tok[0]), int(tok[1])
+        except ValueError:
+            raise ParseError(f"line {no}: non-integer token") from None
+        if a == b:
+            continue
+        flat.append(ids.setdefault(a, len(ids)))
+        flat.append(ids.setdefault(b, len(ids)))
+    if not flat:
+        raise ParseError("no edges")
+    return from_edge_array(np.asarray(flat, dtype=np.int64).reshape(-1, 2),
+                           node_count=len(ids))
+
+
+def load_edge_list(path) -> Graph:
+    """C/graph.py:95-97."""
+    with open(path, "r", encoding="utf-8") as fh:
+        return parse_edge_list(fh.read())
+
+
+def write_edge_list(g: Graph, path_or_file) -> None:
+    """C/graph.py:100-111: dense ids, stream order, one `u v` per line."""
+    own = isinstance(path_or_file, (str, bytes)) or hasattr(path_or_file, "__fspath__")
+    fh = open(path_or_file, "w", encoding="utf-8") if own else path_or_file
+    try:
+        e = g.edges
+        buf = io.StringIO()
+        np.savetxt(buf, e, fmt="%d", delimiter=" ")
+        fh.write(buf.getvalue())
+    finally:
+        if own:
+            fh.close()
+
+
+def from_edge_array(edges, node_count=None) -> Graph:
+    """C/graph.py:114-122 on the GPU: stable self-loop drop + degree histogram.
+
+    `edges` may be any (m, 2)-shaped integer array, or a CUDA tensor
+    (int32/int64) already in HBM."""
+    T = nat.torch()
+    if isinstance(edges, T.Tensor):
+        src = edges.reshape(-1, 2)
+        if src.dtype not in (T.int32, T.int64) or not src.is_cuda:
+            src = nat.to_dev(src, T.int64)
+        src = src.contiguous()
+    else:
+        arr = np.asarray(edges)
+        if arr.dtype == np.int32:
+            src = nat.to_dev(arr.reshape(-1, 2), T.int32)
+        else:
+            src = nat.to_dev(np.asarray(arr, dtype=np.int64).reshape(-1, 2), T.int64)
+    m_in = int(src.shape[0])
+    out = T.empty((max(m_in, 1), 2), dtype=T.int32, device=nat.device())
+    scal = T.zeros(2, dtype=T.int64, device=nat.device())
+    nat.call("cvz_edges_compact", nat.ptr(src), int(src.dtype == T.int32), m_in,
+             nat.ptr(out), nat.ptr(scal), nat.ptr(scal[1:]), 1, nat.stream())
+    m, mx = (int(v) for v in scal.cpu().tolist())
+    if node_count is None:
+        n = mx + 1 if m else 0
+    else:
+        n = int(node_count)
+    nbins = max(n, mx + 1) if m else n  # np.bincount(minlength=n) grows to max+1
+    degree = T.empty(max(nbins, 1), dtype=T.int64, device=nat.device())
+    nat.call("cvz_degree_count", nat.ptr(out), m, nbins, nat.ptr(degree), nat.stream())
+    return Graph._from_device(n, out[:m], degree[:nbins])
+
+
+def _stats_dev(degree_dev, n):
+    T = nat.torch()
+    out = T.empty(3, dtype=T.int64, device=nat.device())
+    nat.call("cvz_degree_stats", nat.ptr(degree_dev), int(degree_dev.shape[0]),
+             nat.ptr(out), nat.stream())
+    return [int(v) for v in out.cpu().tolist()]
+
+
+def degree_stats(g: Graph) -> DegreeStats:
+    """C/graph.py:125-136 on the GPU (mode of nonzero degrees, ties -> smaller)."""
+    if g.edge_count == 0:
+        raise ValueError("degree stats undefined for a graph with no edges")
+    mode, total, mx = _stats_dev(g.degree_dev(), g.node_count)
+    return DegreeStats(mode_degree=mode,
+                       average_degree=float(np.int64(total) / g.node_count),
+                       max_degree=mx)

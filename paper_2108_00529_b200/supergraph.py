@@ -1,0 +1,140 @@
+"""Supergraph contraction (drop-in for C/supergraph.py) on the GPU."""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nat
+from ._dual import Dual
+from .sketch import CountMinSketch, sketch_add_many
+
+
+class SuperGraph:
+    """Weighted contraction: one node per community (C/supergraph.py:19-39)."""
+
+    __slots__ = ("node_count", "_edges", "_weight", "_mult", "_comm")
+
+    def __init__(self, node_count, edges, weight, multiplicity, community_id):
+        edges = np.asarray(edges)
+        if edges.ndim != 2 or edges.shape[1] != 2:
+            raise ValueError("superedges must be an (s, 2) array")
+        if len(weight) != node_count:
+            raise ValueError("one weight per supernode required")
+        if len(multiplicity) != len(edges):
+            raise ValueError("one multiplicity per superedge required")
+        self.node_count = int(node_count)
+        self._edges = Dual(host=edges)
+        self._weight = Dual(host=np.asarray(weight))
+        self._mult = Dual(host=np.asarray(multiplicity))
+        self._comm = Dual(host=np.asarray(community_id))
+
+    @classmethod
+    def _from_device(cls, k, edges, weight, mult, comm):
+        sg = object.__new__(cls)
+        sg.node_count = int(k)
+        sg._edges, sg._weight = Dual(dev=edges), Dual(dev=weight)
+        sg._mult, sg._comm = Dual(dev=mult), Dual(dev=comm)
+        return sg
+
+    edges = property(lambda self: self._edges.host())
+    weight = property(lambda self: self._weight.host())
+    multiplicity = property(lambda self: self._mult.host())
+    community_id = property(lambda self: self._comm.host())
+
+    @property
+    def edge_count(self) -> int:
+        return len(self._edges)
+
+    def edges_dev(self):
+        e = self._edges.dev(nat.torch().int64)
+        return e.reshape(-1, 2).to(nat.torch().int32).contiguous()
+
+    def weight_dev(self):
+        return self._weight.dev(nat.torch().int64)
+
+    def multiplicity_dev(self):
+        return self._mult.dev(nat.torch().int64)
+
+    def __repr__(self):
+        return f"SuperGraph(node_count={self.node_count}, edge_count={self.edge_count})"
+
+
+def _labels_dev(labels):
+    T = nat.torch()
+    if hasattr(labels, "label_dev"):
+        return labels.label_dev()
+    if isinstance(labels, T.Tensor):
+        return labels.to(device=nat.device(), dtype=T.int64).contiguous()
+    return nat.to_dev(np.asarray(labels, dtype=np.int64), T.int64)
+
+
+def accumulate_sizes(sketch: CountMinSketch, labels, degrees) -> None:
+    """Add each node's degree to its community's counter (C/supergraph.py:42-46)."""
+    T = nat.torch()
+    if hasattr(degrees, "degree_dev"):
+        degrees = degrees.degree_dev()
+    sketch_add_many(sketch, _labels_dev(labels), degrees if isinstance(degrees, T.Tensor)
+                    else np.asarray(degrees, dtype=np.int64))
+
+
+def contract(g, labels, sketch: CountMinSketch) -> SuperGraph:
+    """Collapse g under `labels` (C/supergraph.py:49-76): dense ids, sketch
+    weights, sorted + run-length-encoded superedges, all on the GPU."""
+    T = nat.torch()
+    lab = _labels_dev(labels)
+    if int(lab.shape[0]) != g.node_count:
+        raise ValueError("one label per node required")
+    a, b = sketch._hash_dev()
+    res = nat._ContractResult()
+    e = g.edges_dev()
+    nat.call("cvz_contract", nat.ptr(e), int(e.shape[0]), nat.ptr(lab), g.node_count,
+             nat.ptr(sketch.table_dev()), sketch.rows, sketch.cols, nat.ptr(a), nat.ptr(b),
+             ctypes.byref(res), nat.stream())
+    dev = nat.device()
+    k, se = int(res.k), int(res.se)
+    comm = T.empty(k, dtype=T.int64, device=dev)
+    weight = T.empty(k, dtype=T.int64, device=dev)
+    edges = T.empty((se, 2), dtype=T.int64, device=dev)
+    mult = T.empty(se, dtype=T.int64, device=dev)
+    try:
+        cudart = _memcpy_d2d
+        cudart(comm, res.comm_id, 8 * k)
+        cudart(weight, res.weight, 8 * k)
+        cudart(edges, res.se_edges, 16 * se)
+        cudart(mult, res.mult, 8 * se)
+    finally:
+        nat.call("cvz_contract_release", ctypes.byref(res), nat.stream())
+    return SuperGraph._from_device(k, edges, weight, mult, comm)
+
+
+def _memcpy_d2d(dst, src_ptr, nbytes):
+    """Copy a library-owned device buffer into a torch tensor (stream-ordered)."""
+    if nbytes == 0:
+        return
+    T = nat.torch()
+    # wrap the raw pointer via __cuda_array_interface__ and copy on the stream
+    class _Raw:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                    "data": (int(src_ptr), True), "version": 3,
+                                    "stream": None}
+    src = T.as_tensor(_Raw(), device=dst.device)
+    dst.view(T.uint8).reshape(-1)[:nbytes].copy_(src)
+
+
+def export_supernodes_tsv(sg: SuperGraph, path) -> None:
+    """C/supergraph.py:79-83."""
+    table = np.stack([np.arange(sg.node_count, dtype=np.int64), sg.community_id, sg.weight], 1)
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("supernode\tcommunity\tweight\n")
+        np.savetxt(fh, table, fmt="%d", delimiter="\t")
+
+
+def export_superedges_tsv(sg: SuperGraph, path) -> None:
+    """C/supergraph.py:86-91."""
+    table = np.concatenate([sg.edges, sg.multiplicity[:, None]], axis=1) if sg.edge_count else \
+        np.empty((0, 3), np.int64)
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("source\ttarget\tmultiplicity\n")
+        np.savetxt(fh, table, fmt="%d", delimiter="\t")

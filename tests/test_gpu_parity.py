@@ -1,0 +1,473 @@
+"""GPU parity: the CUDA path (through the C-ABI via the drop-in API) against
+the golden vectors of the real reference and against the CPU oracle on
+seeded synthetic graphs.
+
+Gates (stated here):
+  * integers (degrees, counters, deterministic labels/history, sketch
+    tables/estimates, supergraph arrays): bit-exact;
+  * exact repulsion (theta = 0) and attraction: bit-exact (same fp64 ops in
+    the same order); Barnes-Hut repulsion: max |dF| <= 1e-9 * max |F|;
+  * layout trajectories: max |dpos| <= 1e-7 * layout diameter over the
+    golden runs (1..30 iterations);
+  * fast (racy) community mode: |Q_fast - Q_det| <= 0.02, community count
+    within 5 %, top-10 size share within 0.02.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import cases, exact_recovered, golden, has_gpu, planted_edges
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+TIES = ["src-joins-dst", "dst-joins-src", "skip"]
+
+
+@pytest.fixture(scope="module")
+def cv():
+    import paper_2108_00529_b200 as cv
+    return cv
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import oracle as orc
+    return orc
+
+
+# ------------------------------------------------------------------ graph
+def test_from_edge_array_golden(cv):
+    d = golden("graph")
+    for i in cases(d, "g"):
+        nc = int(d[f"g{i}_nc"][0])
+        g = cv.from_edge_array(d[f"g{i}_in"], None if nc < 0 else nc)
+        assert g.node_count == d[f"g{i}_n"][0]
+        assert np.array_equal(g.edges, d[f"g{i}_edges"])
+        assert np.array_equal(g.degree, d[f"g{i}_degree"])
+        st = cv.degree_stats(g)
+        ref = d[f"g{i}_stats"]
+        assert (st.mode_degree, st.max_degree) == (ref[0], ref[2])
+        assert st.average_degree == ref[1]
+
+
+def test_parse_and_degree_kats(cv):
+    # /root/reference/pkg/tests/test_graph.py:16-84
+    g = cv.parse_edge_list("0 1\n1 2\n2 0\n")
+    assert (g.node_count, g.edge_count, list(g.degree)) == (3, 3, [2, 2, 2])
+    assert cv.parse_edge_list("7 3\n3 9\n").edges.tolist() == [[0, 1], [1, 2]]
+    g = cv.parse_edge_list("1 1\n1 2\n1 2\n")
+    assert (g.edge_count, g.node_count, list(g.degree)) == (2, 2, [2, 2])
+    with pytest.raises(cv.ParseError, match="line 2"):
+        cv.parse_edge_list("0 1\n0 1 2\n")
+    with pytest.raises(cv.ParseError, match="no edges"):
+        cv.parse_edge_list("3 3\n")
+    s = cv.degree_stats(cv.parse_edge_list("0 1\n1 2\n1 3\n2 3\n3 4\n"))
+    assert (s.mode_degree, s.max_degree, s.average_degree) == (1, 3, 2.0)
+    with pytest.raises(ValueError):
+        cv.degree_stats(cv.from_edge_array(np.empty((0, 2), np.int64), node_count=3))
+    with pytest.raises(ValueError):
+        cv.from_edge_array(np.array([[0, -1]]))
+
+
+def test_degrees_at_scale(cv, orc):
+    from paper_2108_00529_b200 import synth
+    e = synth.rmat_edges(18, 16, seed=3)
+    e[::97, 1] = e[::97, 0]  # inject self-loops
+    g = cv.from_edge_array(e)
+    n, ee, deg = orc.from_edge_array(e)
+    assert g.node_count == n
+    assert np.array_equal(g.edges, ee) and np.array_equal(g.degree, deg)
+    st = cv.degree_stats(g)
+    assert (st.mode_degree, st.average_degree, st.max_degree) == orc.degree_stats(deg)
+
+
+# -------------------------------------------------------------- community
+def test_scoda_pass_golden(cv):
+    from paper_2108_00529_b200.community import _scoda_pass
+    d = golden("community")
+    for i in cases(d, "p"):
+        n, thr, tie = (int(x) for x in d[f"p{i}_args"])
+        deg, lab = d[f"p{i}_deg0"].copy(), d[f"p{i}_lab0"].copy()
+        _scoda_pass(d[f"p{i}_edges"], d[f"p{i}_order"], thr, tie, deg, lab)
+        assert np.array_equal(deg, d[f"p{i}_deg"]), i
+        assert np.array_equal(lab, d[f"p{i}_lab"]), i
+
+
+def test_resolve_golden(cv, orc):
+    from paper_2108_00529_b200.community import _resolve_labels
+    d = golden("community")
+    for i in cases(d, "r"):
+        assert np.array_equal(_resolve_labels(d[f"r{i}_in"]), d[f"r{i}_out"]), i
+    assert _resolve_labels([1, 2, 3, 3, 0]).tolist() == [3, 3, 3, 3, 3]
+    assert _resolve_labels([1, 2, 0, 1, 4]).tolist() == [0, 0, 0, 0, 4]
+    rng = np.random.default_rng(9)
+    for n in (1, 2, 1000, 200_000):
+        lab = rng.integers(0, n, size=n)  # random functional graph: many cycles
+        assert np.array_equal(_resolve_labels(lab), orc.resolve_labels(lab)), n
+    big = np.roll(np.arange(100_000), 1)  # one 100k-cycle
+    assert np.array_equal(_resolve_labels(big), np.zeros(100_000, np.int64))
+    chain = np.maximum(np.arange(100_000) - 1, 0)  # depth-100k chain
+    assert np.array_equal(_resolve_labels(chain), np.zeros(100_000, np.int64))
+
+
+def test_detect_golden(cv):
+    d = golden("community")
+    for i in cases(d, "d"):
+        n, base, rounds, seed, workers, inter, rs, tie = (int(x) for x in d[f"d{i}_args"])
+        g = cv.from_edge_array(d[f"d{i}_edges"], node_count=n)
+        a = cv.detect_communities(g, cv.ThresholdSchedule(base=base, rounds=rounds), seed=seed,
+                                  tie_rule=TIES[tie], workers=workers,
+                                  interleave=["random", "roundrobin"][inter],
+                                  round_stream=["contract", "restream"][rs])
+        assert np.array_equal(a.label, d[f"d{i}_label"]), i
+        assert np.array_equal(a.counter_degree, d[f"d{i}_counter"]), i
+        assert np.array_equal(np.stack(list(a.round_history)), d[f"d{i}_history"]), i
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_detect_deterministic_bit_exact_at_scale(cv, orc, name):
+    from paper_2108_00529_b200 import synth
+    e = synth.config_graph(name)
+    g = cv.from_edge_array(e)
+    n, ee, deg = orc.from_edge_array(e)
+    base = orc.degree_stats(deg)[0]
+    ref_lab, ref_cnt, ref_hist = orc.detect_communities(n, ee, deg, base, 10, 0, workers=1)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+    assert np.array_equal(a.label, ref_lab)
+    assert np.array_equal(a.counter_degree, ref_cnt)
+    assert len(a.round_history) == len(ref_hist)
+    for x, y in zip(a.round_history, ref_hist):
+        assert np.array_equal(x, y)
+
+
+def test_detect_interleaved_orders_bit_exact(cv, orc):
+    from paper_2108_00529_b200 import synth
+    e = synth.planted_partition(3000, 30000, 30, seed=4)
+    g = cv.from_edge_array(e)
+    n, ee, deg = orc.from_edge_array(e)
+    for workers, inter in [(4, "random"), (8, "roundrobin")]:
+        ref = orc.detect_communities(n, ee, deg, 2, 10, 7, workers=workers, interleave=inter)
+        a = cv.detect_communities(g, cv.ThresholdSchedule(base=2), seed=7, workers=workers,
+                                  interleave=inter)
+        assert np.array_equal(a.label, ref[0])
+
+
+def test_reference_community_kats(cv):
+    # /root/reference/pkg/tests/test_community.py:80-153
+    g = cv.from_edge_array(np.array([[0, 1]]))
+    a = cv.scoda_round(g, cv.fresh_assignment(2), threshold=1)
+    assert a.label[0] == a.label[1] and a.counter_degree.tolist() == [1, 1]
+    g6 = cv.from_edge_array(np.array([[0, 1]] * 6))
+    assert cv.scoda_round(g6, cv.fresh_assignment(2), threshold=2).counter_degree.tolist() == [3, 3]
+    for rule, want in [("src-joins-dst", [1, 1]), ("dst-joins-src", [0, 0]), ("skip", [0, 1])]:
+        assert cv.scoda_round(g, cv.fresh_assignment(2), 1, tie_rule=rule).label.tolist() == want
+    a = cv.fresh_assignment(2)
+    a.counter_degree[0] = 5
+    assert cv.scoda_round(g, a, threshold=2).label.tolist() == [0, 1]
+    edges = [(b + i, b + j) for b in (0, 4) for i in range(4) for j in range(i + 1, 4)] + [(0, 4)]
+    a = cv.detect_communities(cv.from_edge_array(np.array(edges)),
+                              cv.ThresholdSchedule(base=2, rounds=10), seed=0, workers=1)
+    assert len(np.unique(a.label)) == 2 and len(a.round_history) < 10
+    k5 = np.array([(i, j) for i in range(5) for j in range(i + 1, 5)])
+    for seed in range(10):
+        sh = k5[np.random.default_rng(seed).permutation(len(k5))]
+        a = cv.detect_communities(cv.from_edge_array(sh, node_count=5),
+                                  cv.ThresholdSchedule(base=2, rounds=10), seed=seed, workers=1)
+        assert a.community_count == 1 and len(a.round_history) <= 3
+    for seed in range(5):
+        a = cv.detect_communities(cv.from_edge_array(planted_edges(seed)),
+                                  cv.ThresholdSchedule(base=2, rounds=10), seed=100 + seed,
+                                  workers=1)
+        assert exact_recovered(a.label) >= 7
+    with pytest.raises(ValueError):
+        cv.detect_communities(g, cv.ThresholdSchedule(base=2), round_stream="bad")
+    with pytest.raises(ValueError):
+        cv.detect_communities(g, cv.ThresholdSchedule(base=2), tie_rule="nope")
+    with pytest.raises(ValueError):
+        cv.detect_communities(cv.from_edge_array(np.empty((0, 2), np.int64), node_count=2),
+                              cv.ThresholdSchedule(base=2))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_fast_mode_within_tolerance(cv, orc, name):
+    from paper_2108_00529_b200 import synth
+    e = synth.config_graph(name)
+    g = cv.from_edge_array(e)
+    base = cv.degree_stats(g).mode_degree
+    det = cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1)
+    fast = cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1, mode="fast")
+    q_det = orc.modularity(g.edges, g.degree, det.label)
+    q_fast = orc.modularity(g.edges, g.degree, fast.label)
+    assert abs(q_fast - q_det) <= 0.02, (q_fast, q_det)
+    cd, cf = det.community_count, fast.community_count
+    assert abs(cf - cd) <= 0.05 * cd, (cf, cd)
+
+    def top10(lab):
+        c = np.sort(np.unique(lab, return_counts=True)[1])[::-1]
+        return c[:10].sum() / len(lab)
+    assert abs(top10(fast.label) - top10(det.label)) <= 0.02
+    # every label is one of its own members (C/community.py:123-161 invariant)
+    lab = fast.label
+    assert np.all(lab[lab] == lab)
+
+
+def test_gpu_modularity_matches_oracle(cv, orc):
+    from paper_2108_00529_b200 import synth
+    e = synth.config_graph("C1")
+    g = cv.from_edge_array(e)
+    lab = np.random.default_rng(0).integers(0, 50, size=g.node_count)
+    assert abs(cv.modularity(g, lab) - orc.modularity(g.edges, g.degree, lab)) <= 1e-9
+
+
+# ----------------------------------------------------------------- sketch
+def test_sketch_golden(cv):
+    d = golden("sketch")
+    for i in cases(d, "h"):
+        rows, seed = (int(x) for x in d[f"h{i}_args"])
+        s = cv.sketch_new(rows, 97, seed)
+        assert np.array_equal(s.hash_a, d[f"h{i}_a"]) and np.array_equal(s.hash_b, d[f"h{i}_b"])
+    for i in cases(d, "a"):
+        rows, cols, seed = (int(x) for x in d[f"a{i}_args"])
+        s = cv.sketch_new(rows, cols, seed=seed)
+        cv.sketch_add_many(s, d[f"a{i}_keys"], d[f"a{i}_amounts"])
+        assert np.array_equal(s.table, d[f"a{i}_table"]), i
+        assert np.array_equal(cv.sketch_estimate_many(s, d[f"a{i}_probe"]), d[f"a{i}_est"]), i
+        assert np.array_equal(s._indices(d[f"a{i}_probe"]), d[f"a{i}_idx"]), i
+    s = cv.sketch_new(2, 8, seed=0)
+    big = np.iinfo(np.int64).max - 5
+    with pytest.warns(RuntimeWarning):
+        cv.sketch_add_many(s, np.array([0, 1, 0]), np.array([big, 3, big]))
+    assert np.array_equal(s.table, d["sat_table"]) and s.saturated
+
+
+def test_sketch_kats_and_staged_path(cv, orc):
+    # /root/reference/pkg/tests/test_sketch.py:25-68
+    s = cv.sketch_new(4, 512, seed=1)
+    cv.sketch_add(s, 3, 7)
+    cv.sketch_add(s, 3, 2)
+    cv.sketch_add(s, 11, 5)
+    assert cv.sketch_estimate(s, 3) == 9 and cv.sketch_estimate(s, 11) == 5
+    with pytest.raises(ValueError):
+        cv.sketch_add(s, 1, -1)
+    with pytest.raises(ValueError):
+        cv.sketch_add_many(s, np.array([1]), np.array([-2]))
+    # big key sets exercise the shared-memory staged kernel (4 x 6500 table)
+    rng = np.random.default_rng(0)
+    keys = rng.integers(0, 3_000_000, size=3_000_000)
+    amounts = rng.integers(0, 50, size=3_000_000)
+    s = cv.sketch_new(4, 6500, seed=0)
+    cv.sketch_add_many(s, keys, amounts)
+    a, b = orc.sketch_params(4, 0)
+    t = np.zeros((4, 6500), np.int64)
+    orc.sketch_add_many(t, a, b, keys, amounts)
+    assert np.array_equal(s.table, t)
+    s = cv.sketch_new(4, 107_375, seed=2)  # C5 width: direct-atomic path
+    cv.sketch_add_many(s, keys, amounts)
+    a, b = orc.sketch_params(4, 2)
+    t = np.zeros((4, 107_375), np.int64)
+    orc.sketch_add_many(t, a, b, keys, amounts)
+    assert np.array_equal(s.table, t)
+
+
+# ------------------------------------------------------------- supergraph
+def test_contract_golden(cv):
+    d = golden("contract")
+    for i in cases(d, "c"):
+        rows, cols, seed = (int(x) for x in d[f"c{i}_sk"])
+        n = int(d[f"c{i}_n"][0])
+        g = cv.from_edge_array(d[f"c{i}_edges"], node_count=n)
+        s = cv.sketch_new(rows, cols, seed=seed)
+        cv.accumulate_sizes(s, d[f"c{i}_labels"], g.degree)
+        assert np.array_equal(s.table, d[f"c{i}_table"]), i
+        sg = cv.contract(g, d[f"c{i}_labels"], s)
+        assert np.array_equal(sg.edges, d[f"c{i}_se"]), i
+        assert np.array_equal(sg.weight, d[f"c{i}_w"]), i
+        assert np.array_equal(sg.multiplicity, d[f"c{i}_mult"]), i
+        assert np.array_equal(sg.community_id, d[f"c{i}_comm"]), i
+
+
+def test_contract_at_scale(cv, orc):
+    from paper_2108_00529_b200 import synth
+    e = synth.config_graph("C2")
+    g = cv.from_edge_array(e)
+    n, ee, deg = orc.from_edge_array(e)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=cv.degree_stats(g).mode_degree),
+                              workers=1)
+    s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    cv.accumulate_sizes(s, a, g)
+    sg = cv.contract(g, a, s)
+    A, B = orc.sketch_params(4, 0)
+    t = np.zeros((4, orc.default_cols(len(ee))), np.int64)
+    orc.sketch_add_many(t, A, B, a.label, deg)
+    k, se, w, mult, comm = orc.contract(ee, a.label, t, A, B)
+    assert sg.node_count == k
+    assert np.array_equal(sg.edges, se) and np.array_equal(sg.multiplicity, mult)
+    assert np.array_equal(sg.weight, w) and np.array_equal(sg.community_id, comm)
+    # crossing conservation, u < v (test_supergraph.py:126-143)
+    assert sg.multiplicity.sum() == np.sum(a.label[ee[:, 0]] != a.label[ee[:, 1]])
+    assert np.all(sg.edges[:, 0] < sg.edges[:, 1])
+
+
+# ----------------------------------------------------------------- layout
+def test_repulsion_golden(cv):
+    d = golden("layout")
+    for i in cases(d, "f"):
+        pos, mass = d[f"f{i}_pos"], d[f"f{i}_mass"]
+        theta = float(d[f"f{i}_theta"][0])
+        out = cv.repulsion_forces(pos, mass, 80.0, theta)
+        ref = d[f"f{i}_out"]
+        coincident = len(np.unique(pos, axis=0)) < len(pos)
+        if theta == 0 and not coincident:
+            assert np.array_equal(out, ref), i
+        else:
+            scale = np.abs(ref).max()
+            tol = 1e-9 if not coincident else 1e-3  # jitter keys differ for cells
+            assert np.max(np.abs(out - ref)) <= tol * scale, (i, np.max(np.abs(out - ref)) / scale)
+
+
+def test_bh_vs_exact_properties(cv):
+    # /root/reference/pkg/tests/test_layout.py:110-132 and criterion 4
+    rng = np.random.default_rng(3)
+    pos = rng.uniform(-30, 30, (60, 2))
+    mass = rng.uniform(1, 10, 60)
+    exact = cv.repulsion_forces(pos, mass, 80.0, theta=0.0)
+    approx = cv.repulsion_forces(pos, mass, 80.0, theta=0.05)
+    assert np.max(np.hypot(*(approx - exact).T) / np.hypot(*exact.T)) < 0.005
+    f = cv.repulsion_forces(np.zeros((8, 2)), np.ones(8), 80.0, theta=0.5)
+    assert np.all(np.isfinite(f)) and np.any(f != 0)
+    rng = np.random.default_rng(7)
+    pos = rng.uniform(-50, 50, (100, 2))
+    mass = rng.uniform(1, 20, 100)
+    exact = cv.repulsion_forces(pos, mass, 80.0, 0.0)
+    errs = [np.hypot(*(cv.repulsion_forces(pos, mass, 80.0, t) - exact).T) / np.hypot(*exact.T)
+            for t in (0.9, 0.5, 0.2)]
+    assert np.percentile(errs[1], 95) <= 0.05
+    assert errs[0].mean() > errs[1].mean() > errs[2].mean()
+
+
+def test_bh_large_vs_oracle(cv, orc):
+    rng = np.random.default_rng(11)
+    n = 200_000
+    pos = np.concatenate([rng.normal(0, 30, (n // 2, 2)), rng.uniform(-400, 400, (n // 2, 2))])
+    mass = rng.integers(1, 50, n).astype(np.float64)
+    out = cv.repulsion_forces(pos, mass, 80.0, 0.5)
+    ref = orc.repulsion_forces(pos, mass, 80.0, 0.5)
+    rel = np.hypot(*(out - ref).T) / (np.hypot(*ref.T) + 1e-300)
+    assert np.percentile(rel, 99.9) <= 1e-9 and rel.max() <= 1e-6
+
+
+def test_attraction_golden(cv):
+    from paper_2108_00529_b200.layout import _attraction
+    d = golden("layout")
+    out = d["att_in"].copy()
+    _attraction(d["att_pos"], d["att_edges"], d["att_w"], -1.0, out)
+    assert np.array_equal(out, d["att_out"])
+    pos = np.array([[0.0, 0.0], [3.0, -1.0]])
+    o = np.zeros((2, 2))
+    _attraction(pos, np.array([[0, 1]]), np.array([2.0]), 1.0, o)
+    assert o.tolist() == [[6.0, -2.0], [-6.0, 2.0]]
+
+
+def _model(d, key, orc):
+    e = d[key + "_edges"]
+    if d[key + "_kind"][0] == 0:
+        mass, ew = orc.masses_supergraph(d[key + "_weight"], d[key + "_mult"])
+    else:
+        mass, ew = orc.masses_graph(d[key + "_degree"], len(e))
+    return e, mass, ew
+
+
+def test_layout_golden(cv, orc):
+    d = golden("layout")
+    keys = sorted({k.rsplit("_", 1)[0] for k in d.files if k.startswith("l") and k.endswith("_pos")})
+    for key in keys:
+        it, g, theta, sf, af, seed = d[key + "_params"]
+        e = d[key + "_edges"]
+        if d[key + "_kind"][0] == 0:
+            obj = cv.SuperGraph(len(d[key + "_weight"]), e, d[key + "_weight"],
+                                d[key + "_mult"], np.arange(len(d[key + "_weight"])))
+        else:
+            obj = cv.Graph(len(d[key + "_degree"]), e, d[key + "_degree"])
+        res = cv.layout(obj, cv.LayoutParams(iterations=int(it), gravity=float(g),
+                                             theta=float(theta),
+                                             speed_form=["product", "sum"][int(sf)],
+                                             attraction_form=["canonical", "reversed"][int(af)],
+                                             seed=int(seed)))
+        ref = d[key + "_pos"]
+        diam = np.hypot(*(ref.max(0) - ref.min(0)))
+        err = np.max(np.abs(res.positions - ref)) / diam
+        assert err <= 1e-7, (key, err)
+        assert np.allclose(res.displacement, d[key + "_disp"], rtol=1e-6, atol=1e-9 * diam), key
+
+
+def test_layout_step_teacher_forced(cv, orc):
+    """One iteration from the same fp64 state (pos, prev_force, speed)."""
+    rng = np.random.default_rng(5)
+    k = 20_000
+    se = np.unique(np.sort(rng.integers(0, k, (120_000, 2)), axis=1), axis=0)
+    se = se[se[:, 0] < se[:, 1]]
+    w = rng.integers(1, 500, k)
+    mult = rng.integers(1, 20, len(se))
+    sg = cv.SuperGraph(k, se, w, mult, np.arange(k))
+    mass, ew = orc.masses_supergraph(w, mult)
+    pos = rng.uniform(-300, 300, (k, 2))
+    prev = rng.normal(0, 50, (k, 2))
+    for speed in (1.0, 0.37):
+        new_r, f_r, sp_r, md_r, _ = orc.layout_step(pos, prev, speed, mass, se, ew)
+        new_g, f_g, sp_g, md_g = cv.layout_step(sg, pos, prev, speed)
+        fr = np.hypot(*(f_g - f_r).T) / (np.hypot(*f_r.T) + 0.01 * np.hypot(*f_r.T).mean())
+        assert np.percentile(fr, 99) <= 1e-10 and fr.max() <= 1e-6
+        assert abs(sp_g - sp_r) <= 1e-12 * sp_r
+        diam = np.hypot(*(pos.max(0) - pos.min(0)))
+        assert np.max(np.abs(new_g - new_r)) <= 1e-9 * diam
+
+
+def test_reference_layout_kats(cv):
+    # /root/reference/pkg/tests/test_layout.py:47-187 + criterion 6
+    f = cv.repulsion_forces(np.array([[0.0, 0.0], [2.0, 0.0]]), np.ones(2), 80.0, theta=0.0)
+    assert np.allclose(f, [[-40, 0], [40, 0]])
+    f = cv.repulsion_forces(np.array([[0.0, 0.0], [1.0, 0.0]]), np.array([4.0, 1.0]), 80.0, 0.0)
+    assert np.allclose(f, [[-320, 0], [320, 0]])
+    assert np.allclose(cv.gravity_forces(np.array([[3.0, 4.0], [-1.0, 0.5]]),
+                                         np.array([1.0, 2.0]), 1.0), [[-3, -4], [2, -1]])
+
+    def sg2(weights, edges, mult=None):
+        edges = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+        mult = np.ones(len(edges), np.int64) if mult is None else np.asarray(mult)
+        return cv.SuperGraph(len(weights), edges, np.asarray(weights), mult,
+                             np.arange(len(weights)))
+    res = cv.layout(sg2([1, 1], [[0, 1]]), cv.LayoutParams(iterations=500, gravity=0.0, seed=1))
+    assert abs(np.hypot(*(res.positions[0] - res.positions[1])) - np.sqrt(80)) <= 0.1
+    res = cv.layout(sg2([1, 1], [[0, 1]]), cv.LayoutParams(iterations=800, gravity=0.0, seed=1,
+                                                          speed_form="sum"))
+    assert abs(np.hypot(*(res.positions[0] - res.positions[1])) - np.sqrt(80)) <= 0.5
+    res = cv.layout(sg2([1, 1], np.empty((0, 2))), cv.LayoutParams(iterations=50, gravity=0.1),
+                    positions=np.zeros((2, 2)))
+    assert np.hypot(*(res.positions[0] - res.positions[1])) > 1.0
+    res = cv.layout(sg2([4], np.empty((0, 2))), cv.LayoutParams(iterations=5))
+    assert res.positions.shape == (1, 2) and np.all(res.displacement == 0)
+    with pytest.raises(cv.LayoutError):
+        cv.layout(sg2([1, 1], [[0, 1]]), cv.LayoutParams(iterations=3),
+                  positions=np.array([[0.0, 0.0], [np.inf, 0.0]]))
+    with pytest.raises(ValueError):
+        cv.layout(sg2([1, 1], [[0, 1]]), positions=np.zeros((3, 2)))
+    res = cv.layout(sg2([1000, 1000], [[0, 1]]), cv.LayoutParams(iterations=3, gravity=0.0),
+                    positions=np.array([[0.0, 0.0], [0.5, 0.0]]))
+    assert np.all(res.displacement <= 10.0 + 1e-9)
+    far = np.array([[-20.0, 0.0], [20.0, 0.0]])
+    weak = cv.layout(sg2([1, 1], [[0, 1]], [1]), cv.LayoutParams(iterations=300, gravity=0.0),
+                     positions=far)
+    strong = cv.layout(sg2([1, 1], [[0, 1]], [4]), cv.LayoutParams(iterations=300, gravity=0.0),
+                       positions=far)
+    assert np.hypot(*np.diff(strong.positions, axis=0)[0]) < np.hypot(*np.diff(weak.positions, axis=0)[0])
+
+
+def test_full_graph_layout_matches_oracle(cv, orc):
+    e = planted_edges(1, 6, 10, 12)
+    g = cv.from_edge_array(e)
+    mass, ew = orc.masses_graph(g.degree, g.edge_count)
+    res = cv.layout(g, cv.LayoutParams(iterations=10, seed=2))
+    pos, disp = orc.layout(g.node_count, mass, g.edges, ew, iterations=10, seed=2)
+    diam = np.hypot(*(pos.max(0) - pos.min(0)))
+    assert np.max(np.abs(res.positions - pos)) <= 1e-7 * diam
