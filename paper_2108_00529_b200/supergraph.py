@@ -117,7 +117,7 @@ def _memcpy_d2d(dst, src_ptr, nbytes):
     # wrap the raw pointer via __cuda_array_interface__ and copy on the stream
     class _Raw:
         __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
-                                    "data": (int(src_ptr), True), "version": 3,
+                                    "data": (int(src_ptr), False), "version": 3,
                                     "stream": None}
     src = T.as_tensor(_Raw(), device=dst.device)
     dst.view(T.uint8).reshape(-1)[:nbytes].copy_(src)
