@@ -130,7 +130,7 @@ def barrier(ws):
 
 
 # ----------------------------------------------------------------- our arm
-def pipeline(cv, edges_dev, stats=None):
+def pipeline(cv, edges_dev, stats=None, mode="deterministic"):
     """The north-star path, device-resident (public API calls)."""
     import torch
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
@@ -138,7 +138,7 @@ def pipeline(cv, edges_dev, stats=None):
     g = cv.from_edge_array(edges_dev)
     base = cv.degree_stats(g).mode_degree
     ev[1].record()
-    a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1, mode=mode)
     ev[2].record()
     s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
     cv.accumulate_sizes(s, a, g)
@@ -153,7 +153,7 @@ def pipeline(cv, edges_dev, stats=None):
                           contract_ms=ev[2].elapsed_time(ev[3]),
                           layout_ms=ev[3].elapsed_time(ev[4]),
                           m=g.edge_count, n=g.node_count, rounds=len(a.round_history),
-                          k=sg.node_count, se=sg.edge_count))
+                          m_r=list(a.stream_edges), k=sg.node_count, se=sg.edge_count))
     return res
 
 
@@ -168,6 +168,60 @@ def pipeline_e2e(cv, edges_host):
     res = cv.layout(sg, cv.LayoutParams(iterations=ITERS, seed=0))
     label = a.label                               # D2H of the per-node result
     return res.positions, label
+
+
+# Algorithmic (compulsory) bytes per launch: int32 ids,
+# fp64 layout state (our layout keeps the reference's fp64), every array
+# touched once.  st = the instrumented step's stats.
+def kernel_bytes(name, st):
+    n, m, k, se = st["n"], st["m"], st["k"], st["se"]
+    tab = {
+        # per body: Body (x, y, m, id) 32 B read + force 16 B write;
+        # per tree node: TNode 48 B read once
+        "bh_kernel": k * (32 + 16) + (k - 1) * 48,
+        # pos 16 + repulsion 16 + mass 8 + prev 16 + rowptr 8 + force 16 + swing 8
+        # per node; col 4 + weight 8 per half-edge
+        "forces_kernel": k * 88 + 2 * se * 12,
+        # swing 8 + force 16 + pos r/w 32 + prev 16 per node
+        "update_kernel": k * 72,
+        # 1 ms graph replays excluded; per round bytes are in community_pass
+    }
+    return tab.get(name)
+
+
+def community_pass_bytes(st):
+    """SURVEY.md 8(d): per round 16 m_r (pass read + relabel read) + 8 m_{r+1}
+    (compacted write) + 32 n (counters, labels, resolve, compose)."""
+    mr = st["m_r"]
+    tot = 0
+    for i, x in enumerate(mr):
+        nxt = mr[i + 1] if i + 1 < len(mr) else 0
+        tot += 16 * x + 8 * nxt + 32 * st["n"]
+    return tot
+
+
+def roofline(prof, st, peak_gbs):
+    ks = sorted(prof.items(), key=lambda kv: -kv[1][1])
+    total = sum(v[1] for _, v in ks) or 1.0
+    top = [{"kernel": nm, "launches": c, "ms": round(ms, 4), "share": round(ms / total, 4)}
+           for nm, (c, ms) in ks[:12]]
+    name, (cnt, ms) = ks[0]
+    b = kernel_bytes(name, st)
+    per_launch_s = ms / cnt / 1000.0
+    ach = (b / per_launch_s / 1e9) if b is not None else None
+    roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peak_gbs, "unit": "GB/s",
+            "frac": (ach / peak_gbs) if ach is not None else None, "traffic": None,
+            "bytes_per_launch": b, "launch_ms": per_launch_s * 1000.0, "launches": cnt,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
+    return roof, top
+
+
+def peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
 
 
 def run_ours(args, rank, ws):
@@ -199,9 +253,27 @@ def run_ours(args, rank, ws):
     ms = t1.elapsed_time(t0) * -1 if False else t0.elapsed_time(t1)
     ms_step = barrier_max(ms / args.steps, ws)
     barrier(ws)
-    # per-stage breakdown (one extra instrumented step)
-    pipeline(cv, dev, stats)
+    # per-stage breakdown + per-kernel device times (one extra instrumented
+    # step: library kernels bracketed by CUDA events on their own stream)
+    with _native.profile() as prof:
+        pipeline(cv, dev, stats)
     st = stats[0]
+    # fast (racy) community mode, same graph: detect stage only
+    g = cv.from_edge_array(dev)
+    base = cv.degree_stats(g).mode_degree
+    for _ in range(2):
+        cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1, mode="fast")
+    torch.cuda.synchronize()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(args.steps):
+        fa = cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1, mode="fast")
+    f1.record()
+    torch.cuda.synchronize()
+    fast = dict(ms=f0.elapsed_time(f1) / args.steps, rounds=len(fa.round_history),
+                m_r=list(fa.stream_edges), communities=fa.community_count)
+    del g
     # e2e through the public API from pinned host memory
     host_np = host.numpy()
     torch.cuda.synchronize()
@@ -213,7 +285,7 @@ def run_ours(args, rank, ws):
     h2d = host_np.nbytes
     d2h = pos.nbytes + lab.nbytes
     return dict(ms_step=ms_step, m_in=m_in, stage=st, launches=launches, clocks=clk.summary(),
-                e2e_ms=e2e_ms, h2d=h2d, d2h=d2h)
+                e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, prof=prof.kernels, fast=fast)
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -280,6 +352,9 @@ def main():
     if rank != 0:
         return
     st = r["stage"]
+    peak, _src = peak_hbm()
+    roof, top = roofline(r["prof"], st, peak)
+    roof["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs ({_src})"
     value = r["m_in"] * ws / (r["ms_step"] / 1000.0)
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws,
@@ -295,6 +370,14 @@ def main():
         "ms_per_fa2_iter": st["layout_ms"] / ITERS,
         "end_to_end_s": r["ms_step"] / 1000.0,
         "stage_ms": {k: st[k] for k in ("ingest_ms", "detect_ms", "contract_ms", "layout_ms")},
+        "community_pass_fast": {
+            "edges_per_s": st["m"] / (r["fast"]["ms"] / 1000.0), "ms": r["fast"]["ms"],
+            "rounds": r["fast"]["rounds"], "communities": r["fast"]["communities"],
+            "hbm_frac": community_pass_bytes(dict(st, m_r=r["fast"]["m_r"])) /
+            (r["fast"]["ms"] / 1000.0) / 1e9 / peak},
+        "community_pass_hbm_frac": community_pass_bytes(st) / (st["detect_ms"] / 1000.0) / 1e9 / peak,
+        "roofline": roof,
+        "top_kernels": top,
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "e2e": {"value": r["m_in"] * ws / (r["e2e_ms"] / 1000.0), "unit": "edges/s",

@@ -46,6 +46,17 @@ const char *cvz_last_error(void);
 /* Number of kernels this library has launched so far (process-wide).     */
 long long cvz_launch_count(void);
 
+/* Per-kernel device timing.  Between begin and end every library kernel
+ * (and every CUB primitive, by region name) launched on a stream that is not
+ * being captured is bracketed by CUDA events on its own stream; layout runs
+ * launch their iterations directly instead of replaying a CUDA graph.  end
+ * synchronises the device and builds the report: one line per kernel,
+ * "name<TAB>launches<TAB>total_ms".  No reference counterpart (the
+ * reference has only wall-clock stage timing, C/cli.py:106-117). */
+int cvz_profile_begin(void);
+int cvz_profile_end(void);
+const char *cvz_profile_report(void);
+
 /* ---------------------------------------------------------------- graph */
 
 /* C/graph.py:114-122 from_edge_array (mask u==v keeping stream order) and

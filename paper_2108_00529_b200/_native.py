@@ -42,6 +42,9 @@ SIGNATURES = {
     "cvz_version": [],
     "cvz_last_error": [],
     "cvz_launch_count": [],
+    "cvz_profile_begin": [],
+    "cvz_profile_end": [],
+    "cvz_profile_report": [],
     "cvz_edges_compact": [_P, _I32, _I64, _P, _P, _P, _I32, _P],
     "cvz_degree_count": [_P, _I64, _I64, _P, _P],
     "cvz_degree_stats": [_P, _I64, _P, _P],
@@ -81,12 +84,30 @@ def load():
             fn.restype = ctypes.c_int
         lib.cvz_last_error.restype = ctypes.c_char_p
         lib.cvz_launch_count.restype = ctypes.c_longlong
+        lib.cvz_profile_report.restype = ctypes.c_char_p
         _lib = lib
     return _lib
 
 
 def launch_count() -> int:
     return int(load().cvz_launch_count())
+
+
+class profile:
+    """Context manager: per-kernel device times of every library launch in
+    the block (cvz_profile_begin/end).  .kernels = {name: (launches, ms)}."""
+
+    def __enter__(self):
+        call("cvz_profile_begin")
+        self.kernels = {}
+        return self
+
+    def __exit__(self, *exc):
+        call("cvz_profile_end")
+        for line in load().cvz_profile_report().decode().splitlines():
+            name, cnt, ms = line.split("\t")
+            self.kernels[name] = (int(cnt), float(ms))
+        return False
 
 
 def check(rc: int, what: str = ""):

@@ -42,6 +42,8 @@ class _History(list):
     """Per-round label snapshots; device tensors converted on access."""
 
     def __init__(self, items=()):
+        if isinstance(items, _History):
+            items = [items._dev(i) for i in range(len(items))]
         super().__init__(items)
 
     def __getitem__(self, i):
@@ -71,7 +73,10 @@ class CommunityAssignment:
     def __init__(self, label, counter_degree, round_history=None):
         self._label = label if isinstance(label, Dual) else Dual(host=label)
         self._counter = counter_degree if isinstance(counter_degree, Dual) else Dual(host=counter_degree)
-        self.round_history = _History(round_history or [])
+        if isinstance(round_history, _History):
+            self.round_history = round_history  # keep device snapshots on device
+        else:
+            self.round_history = _History(round_history or [])
 
     label = property(lambda self: self._label.host(),
                      lambda self, v: self._label.set_host(v))
@@ -228,9 +233,11 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
     next_m = nat._I64(0)
     changed = ctypes.c_int(0)
     rs = 0 if round_stream == "contract" else 1
+    streamed = []  # m_r per executed round (bench roofline bytes; no reference counterpart)
     for i in range(1, schedule.rounds + 1):
         if m_cur == 0:
             break
+        streamed.append(m_cur)
         thr = min(schedule.threshold(i), cap)
         order = _schedule_dev(m_cur, workers, seed + i, interleave)
         snap = T.empty(n, dtype=T.int64, device=dev)
@@ -244,8 +251,10 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
         if not changed.value:
             break
         cur, m_cur = out, int(next_m.value)
-    return CommunityAssignment(label=Dual(dev=node_lab), counter_degree=Dual(dev=deg),
-                               round_history=_History(history))
+    a = CommunityAssignment(label=Dual(dev=node_lab), counter_degree=Dual(dev=deg),
+                            round_history=_History(history))
+    a.stream_edges = streamed
+    return a
 
 
 def export_hierarchy_tsv(a: CommunityAssignment, path) -> None:

@@ -42,13 +42,46 @@ extern std::atomic<long long> g_launches;
         if (!(cond)) throw ::cvz::Error(code, msg);  \
     } while (0)
 
+// ---- per-kernel device timing (cvz_profile_begin/end/report) --------------
+// While enabled, every CVZ_LAUNCH / CVZ_REGION on a stream that is not being
+// captured is bracketed by a pair of CUDA events recorded on the launching
+// stream; the report sums the elapsed times per kernel name.  Layout runs
+// skip CUDA-graph capture while profiling so their kernels are seen too.
+bool prof_on();
+void prof_record(const char *name, cudaEvent_t a, cudaEvent_t b);
+cudaEvent_t prof_event();
+
+struct ProfScope {
+    const char *name;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    ProfScope(const char *n, cudaStream_t st) : name(n), s(st) {
+        if (!prof_on()) return;
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cs);
+        if (cs != cudaStreamCaptureStatusNone) return;
+        a = prof_event();
+        cudaEventRecord(a, s);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        cudaEvent_t b = prof_event();
+        cudaEventRecord(b, s);
+        prof_record(name, a, b);
+    }
+};
+
 // Launch with accounting + immediate launch-error check.
 #define CVZ_LAUNCH(kernel, grid, block, smem, stream, ...)              \
     do {                                                                \
+        ::cvz::ProfScope _cvz_ps(#kernel, (stream));                    \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);     \
         ::cvz::g_launches.fetch_add(1, std::memory_order_relaxed);      \
         CVZ_CUDA(cudaGetLastError());                                   \
     } while (0)
+
+// Time a library primitive (CUB) under `name` (same rules as CVZ_LAUNCH).
+#define CVZ_REGION(name, stream) ::cvz::ProfScope _cvz_region(name, (stream))
 
 // Count a library (CUB) primitive's kernels in the launch tally.
 inline void count_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }

@@ -177,7 +177,10 @@ void superedges(const int2 *e, long long m, const int *dense, long long k, int B
     size_t tb = 0;
     CVZ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, (int)c, 0, 2 * B, s));
     void *tmp = sc.alloc<char>(tb);
-    CVZ_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, (int)c, 0, 2 * B, s));
+    {
+        CVZ_REGION("cub_sort:contract_pairs", s);
+        CVZ_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, (int)c, 0, 2 * B, s));
+    }
     count_launches(1 + (2 * B + 7) / 8);
     K *uniq = sc.alloc<K>(c);
     int *counts = sc.alloc<int>(c);
@@ -185,7 +188,10 @@ void superedges(const int2 *e, long long m, const int *dense, long long k, int B
     size_t tb2 = 0;
     CVZ_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tb2, sorted, uniq, counts, nruns, (int)c, s));
     void *tmp2 = sc.alloc<char>(tb2);
-    CVZ_CUDA(cub::DeviceRunLengthEncode::Encode(tmp2, tb2, sorted, uniq, counts, nruns, (int)c, s));
+    {
+        CVZ_REGION("cub_rle:contract_pairs", s);
+        CVZ_CUDA(cub::DeviceRunLengthEncode::Encode(tmp2, tb2, sorted, uniq, counts, nruns, (int)c, s));
+    }
     count_launches(2);
     long long hr = 0;
     CVZ_CUDA(cudaMemcpyAsync(&hr, nruns, sizeof(hr), cudaMemcpyDeviceToHost, s));
@@ -222,7 +228,10 @@ long long dense_ids(const int64_t *labels, int64_t n, int *dense, int64_t **comm
         size_t tb = 0;
         CVZ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, present, rank, (int)range, s));
         void *tmp = sc.alloc<char>(tb);
-        CVZ_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, present, rank, (int)range, s));
+        {
+            CVZ_REGION("cub_scan:contract_dense", s);
+            CVZ_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, present, rank, (int)range, s));
+        }
         count_launches(2);
         int last[2];
         CVZ_CUDA(cudaMemcpyAsync(&last[0], rank + range - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -242,7 +251,11 @@ long long dense_ids(const int64_t *labels, int64_t n, int *dense, int64_t **comm
         size_t tb = 0;
         CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, lab, sorted, iota, node, (int)n, 0, 64, s));
         void *tmp = sc.alloc<char>(tb);
-        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, lab, sorted, iota, node, (int)n, 0, 64, s));
+        {
+            CVZ_REGION("cub_sort:contract_labels", s);
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, lab, sorted, iota, node, (int)n, 0,
+                                                     64, s));
+        }
         count_launches(9);
         int *flags = sc.alloc<int>(n), *incl = sc.alloc<int>(n);
         CVZ_LAUNCH(head_flags_kernel, grid_for(n, 256, 1, 8), 256, 0, s, sorted, (long long)n, flags);

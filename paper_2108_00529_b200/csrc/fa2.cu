@@ -54,6 +54,20 @@ __device__ __forceinline__ double separation(double &dx, double &dy, long long a
     return EPS;
 }
 
+// 1 / d2 without DDIV: fp32 seed + two fp64 Newton steps (relative error
+// ~1e-16, i.e. at the last ulp).  The reference computes kr*mi*mj / (d*d)
+// with d = sqrt(d2) (C/layout.py:240,260); d*d and d2 differ by <= 1 ulp, so
+// f = kr*mi*mj * (1/d2) agrees to ~1e-15 relative while skipping the fp64
+// sqrt + divide sequences that bound the traversal on the FP64 pipe.
+__device__ __forceinline__ double inv_d2(double d2) {
+    if (d2 > 1e30) return 1.0 / d2;  // outside the fp32 seed's range
+    double r = (double)__frcp_rn((float)d2);
+    double e = fma(-d2, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d2, r, 1.0);
+    return fma(r, e, r);
+}
+
 struct Body {
     double x, y, m;
     int orig, pad;
@@ -262,7 +276,7 @@ __global__ void com_kernel(const Body *__restrict__ bodies, int n, const int *__
                            const int *__restrict__ rc_by_split, unsigned *__restrict__ visit,
                            double *__restrict__ smass, double *__restrict__ sx,
                            double *__restrict__ sy, const double *__restrict__ bbox,
-                           TNode *__restrict__ nodes) {
+                           TNode *__restrict__ nodes, int2 *__restrict__ i12) {
     Geo g = root_geo(bbox);
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
         int node = parent_leaf[p];
@@ -298,6 +312,11 @@ __global__ void com_kernel(const Body *__restrict__ bodies, int n, const int *__
                 x1 = mul(b.m, b.x);
                 y1 = mul(b.m, b.y);
             }
+            if (i12) {  // two smallest original body ids of the subtree
+                int2 a = l >= 0 ? __ldcg(i12 + l) : make_int2(bodies[~l].orig, INT_MAX);
+                int2 b = rc >= 0 ? __ldcg(i12 + rc) : make_int2(bodies[~rc].orig, INT_MAX);
+                i12[node] = a.x < b.x ? make_int2(a.x, min(a.y, b.x)) : make_int2(b.x, min(b.y, a.x));
+            }
             double mm = add(m0, m1), xx = add(x0, x1), yy = add(y0, y1);
             smass[node] = mm;
             sx[node] = xx;
@@ -327,7 +346,134 @@ __global__ void com_kernel(const Body *__restrict__ bodies, int n, const int *__
     }
 }
 
+// ---- reference cell numbering (coincident-point jitter keys) ---------------
+// The reference keys the jitter direction of a CELL interaction by the cell's
+// array index, i.e. its creation order during sequential insertion
+// (C/layout.py:140-210,258).  That order is reconstructed here without
+// inserting: a cell is created while inserting body t at depth L, cells of
+// one insertion are created top-down, and at a split the old body's child
+// comes before the new body's.  So the index of a cell is its rank under the
+// key (t, L, flag), where for a cell P with parent cell Y
+//   t = i2(Y) if P holds i1(Y) or i2(Y) (created by Y's split), else i1(P);
+//   flag = 0 iff P holds i1(Y)      (i1/i2 = two smallest body ids).
+// A compressed GPU cell X spans the reference's single-child chain of
+// levels [Ltop, Lbot]: its top cell (entry A) follows the rule above, the
+// rest (entry B, Lbot - Ltop cells) are created consecutively while inserting
+// i2(X).  Single-body leaves get one entry each.  Rank = exclusive scan of
+// the entry counts in key order; the root is cell 0.
+__device__ __forceinline__ int cell_parent(const int *__restrict__ parent_int,
+                                           const int *__restrict__ pdelta, int y, int ly) {
+    while (y != 0 && (pdelta[y] >> 1) == ly) y = parent_int[y];  // topmost node of level ly
+    return y;
+}
+
+__device__ __forceinline__ unsigned long long cell_key(int t, int level, int flag) {
+    return ((unsigned long long)(unsigned)t << 8) | ((unsigned long long)level << 1) |
+           (unsigned long long)flag;
+}
+
+constexpr unsigned long long NO_KEY = ~0ull;
+
+__global__ void cell_entries_kernel(const Body *__restrict__ bodies, int n,
+                                    const TNode *__restrict__ nodes, const int *__restrict__ delta,
+                                    const int *__restrict__ pdelta,
+                                    const int *__restrict__ parent_int,
+                                    const int *__restrict__ parent_leaf,
+                                    const int2 *__restrict__ i12,
+                                    unsigned long long *__restrict__ key,
+                                    unsigned *__restrict__ slot, unsigned *__restrict__ count) {
+    const int ni = n - 1;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 2 * ni + n;
+         t += gridDim.x * blockDim.x) {
+        unsigned long long k = NO_KEY;
+        unsigned c = 0;
+        if (t < 2 * ni) {
+            int x = t >> 1, which = t & 1;
+            int kind = nodes[x].kind;
+            if (kind != 0) {
+                int lbot = kind == 2 ? MAX_DEPTH : (delta[x] >> 1);
+                int2 ix = i12[x];
+                if (x == 0) {  // root: reference cell 0 at level 0 + chain 1..lbot
+                    if (which == 1 && lbot >= 1) {
+                        k = cell_key(ix.y, 1, 0);
+                        c = (unsigned)lbot;
+                    }
+                } else {
+                    int ly = pdelta[x] >> 1, ltop = ly + 1;
+                    if (which == 0) {
+                        int y = cell_parent(parent_int, pdelta, parent_int[x], ly);
+                        int2 iy = i12[y];
+                        bool has1 = ix.x == iy.x, has2 = ix.x == iy.y || ix.y == iy.y;
+                        k = cell_key((has1 || has2) ? iy.y : ix.x, ltop, has1 ? 0 : 1);
+                        c = 1;
+                    } else if (lbot > ltop) {
+                        k = cell_key(ix.y, ltop + 1, 0);
+                        c = (unsigned)(lbot - ltop);
+                    }
+                }
+            }
+        } else {
+            int p = t - 2 * ni;
+            int par = parent_leaf[p];
+            if (delta[par] < 2 * MAX_DEPTH) {  // not inside an aggregate
+                int ly = delta[par] >> 1;
+                int y = cell_parent(parent_int, pdelta, par, ly);
+                int2 iy = i12[y];
+                int b = bodies[p].orig;
+                k = cell_key((b == iy.x || b == iy.y) ? iy.y : b, ly + 1, b == iy.x ? 0 : 1);
+                c = 1;
+            }
+        }
+        key[t] = k;
+        slot[t] = (unsigned)t;
+        count[t] = c;
+    }
+}
+
+__global__ void gather_counts_kernel(const unsigned *__restrict__ sslot,
+                                     const unsigned *__restrict__ count, int ne,
+                                     unsigned *__restrict__ scount) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ne; j += gridDim.x * blockDim.x)
+        scount[j] = count[sslot[j]];
+}
+
+__global__ void scatter_ids_kernel(const unsigned *__restrict__ sslot,
+                                   const unsigned *__restrict__ excl, int ne,
+                                   int *__restrict__ idslot) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ne; j += gridDim.x * blockDim.x)
+        idslot[sslot[j]] = 1 + (int)excl[j];
+}
+
+// Reference cell index of the first cell of X's chain that the body would
+// approximate: levels [ltop, lcap] tested top-down with the reference's
+// `side * side < theta * theta * d2`; none passing -> level lcap + 1 (the
+// aggregate, always approximated) -- only reached for aggregates.
+__device__ long long ref_cell_id(int c, const int *__restrict__ delta,
+                                 const int *__restrict__ pdelta, const int *__restrict__ idslot,
+                                 int kind, double half, double th2d2, bool at_bottom) {
+    int ltop = c == 0 ? 0 : (pdelta[c] >> 1) + 1;
+    int lbot = kind == 2 ? MAX_DEPTH : (delta[c] >> 1);
+    int lcap = kind == 2 ? MAX_DEPTH - 1 : lbot;
+    int l = at_bottom ? lbot : ltop;
+    for (; l <= lcap; ++l) {
+        double side = 2.0 * ldexp(half, -l);
+        if (mul(side, side) < th2d2) break;
+    }
+    if (l > lbot) l = lbot;
+    if (c == 0 && l == 0) return 0;
+    return l == ltop ? idslot[2 * c] : idslot[2 * c + 1] + (l - ltop - 1);
+}
+
 // ---- repulsion traversal ---------------------------------------------------
+// Cell-jitter context: idslot == nullptr on the first pass (a cell
+// interaction closer than COINCIDE_EPS only raises *jflag); the caller then
+// builds the reference cell numbering and reruns with idslot set.
+struct CellRef {
+    const int *delta, *pdelta, *idslot;
+    unsigned *jflag;
+    const double *bbox;
+};
+
 __global__ void __launch_bounds__(FB) bh_kernel(const Body *__restrict__ bodies, int n,
                                                 const TNode *__restrict__ nodes,
                                                 const int *__restrict__ rc_by_split,
@@ -337,13 +483,14 @@ __global__ void __launch_bounds__(FB) bh_kernel(const Body *__restrict__ bodies,
                                                 const double *__restrict__ sx,
                                                 const double *__restrict__ sy, double kr,
                                                 double theta, double2 *__restrict__ out,
-                                                const long long *__restrict__ bad) {
+                                                const long long *__restrict__ bad, CellRef cr) {
     if (bad && *bad) return;
     const double th2 = mul(theta, theta);
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
         Body me = bodies[p];
         const long long i = me.orig;
         const double xi = me.x, yi = me.y, mi = me.m;
+        const double kmi = mul(kr, mi);  // (kr * mi) * mj, the reference's order
         double fx = 0.0, fy = 0.0;
         int c = 0;  // root (n >= 2)
         while (c != END) {
@@ -352,8 +499,14 @@ __global__ void __launch_bounds__(FB) bh_kernel(const Body *__restrict__ bodies,
                 if (q != p) {
                     Body bj = bodies[q];
                     double dx = sub(xi, bj.x), dy = sub(yi, bj.y);
-                    double d = separation(dx, dy, i, bj.orig);
-                    double f = mul(mul(kr, mi), bj.m) / mul(d, d);
+                    double d2 = add(mul(dx, dx), mul(dy, dy));
+                    double f;
+                    if (d2 >= EPS * EPS) {
+                        f = mul(mul(kmi, bj.m), inv_d2(d2));
+                    } else {  // coincident: reference jitter (C/layout.py:85-94)
+                        double d = separation(dx, dy, i, bj.orig);
+                        f = mul(kmi, bj.m) / mul(d, d);
+                    }
                     fx = add(fx, mul(f, dx));
                     fy = add(fy, mul(f, dy));
                 }
@@ -366,8 +519,17 @@ __global__ void __launch_bounds__(FB) bh_kernel(const Body *__restrict__ bodies,
                 continue;
             }
             double mc = t.mass, cx = t.comx, cy = t.comy;
-            if (t.kind == 2) {  // aggregate (C/layout.py:247-252)
-                if (p >= first[c] && p <= last[c]) {
+            bool self_out = false;
+            if (t.kind == 2 && p >= first[c] && p <= last[c]) {  // aggregate holding i
+                // The reference first tests the single-child cells above the
+                // aggregate with the FULL centre of mass (self included) and
+                // approximates there if one passes (C/layout.py:253-261);
+                // only the depth-40 cell itself subtracts self (:247-252).
+                int ltop = c == 0 ? 0 : (cr.pdelta[c] >> 1) + 1;
+                double dxf = sub(xi, cx), dyf = sub(yi, cy);
+                double d2f = add(mul(dxf, dxf), mul(dyf, dyf));
+                double s39 = 2.0 * ldexp(root_geo(cr.bbox).half, -(MAX_DEPTH - 1));
+                if (!(ltop <= MAX_DEPTH - 1 && mul(s39, s39) < mul(th2, d2f))) {
                     double m2 = sub(smass[c], mi);
                     double x2 = sub(sx[c], mul(mi, xi)), y2 = sub(sy[c], mul(mi, yi));
                     if (m2 <= 0.0) {
@@ -377,13 +539,27 @@ __global__ void __launch_bounds__(FB) bh_kernel(const Body *__restrict__ bodies,
                     mc = m2;
                     cx = x2 / m2;
                     cy = y2 / m2;
+                    self_out = true;
                 }
             }
             double dx = sub(xi, cx), dy = sub(yi, cy);
             double d2 = add(mul(dx, dx), mul(dy, dy));
             if (t.kind == 2 || t.side2 < mul(th2, d2)) {  // (C/layout.py:256-261)
-                double d = separation(dx, dy, i, (long long)n + c);
-                double f = mul(mul(kr, mi), mc) / mul(d, d);
+                double f;
+                if (d2 >= EPS * EPS) {
+                    f = mul(mul(kmi, mc), inv_d2(d2));
+                } else {
+                    long long cell;
+                    if (cr.idslot) {
+                        cell = ref_cell_id(c, cr.delta, cr.pdelta, cr.idslot, t.kind,
+                                           root_geo(cr.bbox).half, mul(th2, d2), self_out);
+                    } else {
+                        atomicOr(cr.jflag, 1u);
+                        cell = c;
+                    }
+                    double d = separation(dx, dy, i, (long long)n + cell);
+                    f = mul(kmi, mc) / mul(d, d);
+                }
                 fx = add(fx, mul(f, dx));
                 fy = add(fy, mul(f, dy));
                 c = t.skip;
@@ -474,10 +650,54 @@ struct StepScalars {
     unsigned long long maxdisp_bits;
 };
 
+// Rows longer than HEAVY are summed by a whole warp (lane-strided partials,
+// fixed butterfly order -> deterministic); a thread-per-row loop would leave
+// the warp waiting on the power-law tail.  C/layout.py:293-304.
+constexpr int HEAVY = 32;
+
+__global__ void classify_rows_kernel(const long long *__restrict__ rowptr, int n,
+                                     int *__restrict__ hidx, int *__restrict__ heavy,
+                                     unsigned *__restrict__ nheavy) {
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        int h = -1;
+        if (rowptr[u + 1] - rowptr[u] > HEAVY) {
+            h = (int)atomicAdd(nheavy, 1u);
+            heavy[h] = u;
+        }
+        hidx[u] = h;
+    }
+}
+
+__global__ void __launch_bounds__(FB) springs_heavy_kernel(
+    const double2 *__restrict__ pos, const long long *__restrict__ rowptr,
+    const int *__restrict__ col, const double *__restrict__ cw, const int *__restrict__ heavy,
+    int nheavy, double2 *__restrict__ hsum, const StepScalars *__restrict__ sc) {
+    if (sc && sc->bad) return;
+    const int lane = lane_id();
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nheavy;
+         w += (gridDim.x * blockDim.x) >> 5) {
+        int u = heavy[w];
+        double2 pu = pos[u];
+        double fx = 0.0, fy = 0.0;
+        for (long long j = rowptr[u] + lane; j < rowptr[u + 1]; j += 32) {
+            double2 pv = pos[col[j]];
+            double c = cw[j];
+            fx = add(fx, mul(c, sub(pv.x, pu.x)));
+            fy = add(fy, mul(c, sub(pv.y, pu.y)));
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            fx = add(fx, __shfl_xor_sync(0xffffffffu, fx, o));
+            fy = add(fy, __shfl_xor_sync(0xffffffffu, fy, o));
+        }
+        if (lane == 0) hsum[w] = make_double2(fx, fy);
+    }
+}
+
 __global__ void __launch_bounds__(FB) forces_kernel(
     const double2 *__restrict__ pos, const double *__restrict__ mass, int n,
     const long long *__restrict__ rowptr, const int *__restrict__ col,
-    const double *__restrict__ cw, const double2 *__restrict__ frep, double gravity,
+    const double *__restrict__ cw, const int *__restrict__ hidx,
+    const double2 *__restrict__ hsum, const double2 *__restrict__ frep, double gravity,
     const double2 *__restrict__ prev, double2 *__restrict__ force, double *__restrict__ swing,
     double *__restrict__ part, unsigned *__restrict__ ctr, StepScalars *__restrict__ sc,
     double jt) {
@@ -487,12 +707,19 @@ __global__ void __launch_bounds__(FB) forces_kernel(
     if (u < n) {
         double2 pu = pos[u];
         double2 f = frep[u];
-        // springs in edge order (CSR rows are stably sorted by edge id)
-        for (long long j = rowptr[u]; j < rowptr[u + 1]; ++j) {
-            double2 pv = pos[col[j]];
-            double w = cw[j];
-            f.x = add(f.x, mul(w, sub(pv.x, pu.x)));
-            f.y = add(f.y, mul(w, sub(pv.y, pu.y)));
+        int h = hidx[u];
+        if (h >= 0) {  // heavy row: warp-summed by springs_heavy_kernel
+            double2 hs = hsum[h];
+            f.x = add(f.x, hs.x);
+            f.y = add(f.y, hs.y);
+        } else {
+            // springs in edge order (CSR rows are stably sorted by edge id)
+            for (long long j = rowptr[u]; j < rowptr[u + 1]; ++j) {
+                double2 pv = pos[col[j]];
+                double w = cw[j];
+                f.x = add(f.x, mul(w, sub(pv.x, pu.x)));
+                f.y = add(f.y, mul(w, sub(pv.y, pu.y)));
+            }
         }
         double mu = mass[u];
         if (gravity > 0) {  // C/layout.py:307-309,370-371
@@ -622,12 +849,13 @@ __global__ void __launch_bounds__(FB) update_kernel(
         last = atomicAdd(ctr, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!last || threadIdx.x != 0) return;
+    if (!last) return;
     __threadfence();
+    // last block: all threads reduce the per-block partials
     volatile double *vp = bpart;
     double mn_x = INFINITY, mx_x = -INFINITY, mn_y = INFINITY, mx_y = -INFINITY, md = 0.0;
     bool bad = false;
-    for (unsigned k = 0; k < gridDim.x; ++k) {
+    for (unsigned k = threadIdx.x; k < gridDim.x; k += FB) {
         mn_x = fmin(mn_x, vp[5 * k]);
         mx_x = fmax(mx_x, vp[5 * k + 1]);
         mn_y = fmin(mn_y, vp[5 * k + 2]);
@@ -636,10 +864,29 @@ __global__ void __launch_bounds__(FB) update_kernel(
         if (v < 0) bad = true;
         md = fmax(md, v);
     }
-    bbox[0] = mn_x;
-    bbox[1] = mx_x;
-    bbox[2] = mn_y;
-    bbox[3] = mx_y;
+    __syncthreads();
+    sm[threadIdx.x] = md;
+    s0[threadIdx.x] = mn_x;
+    s1[threadIdx.x] = mx_x;
+    s2[threadIdx.x] = mn_y;
+    s3[threadIdx.x] = mx_y;
+    bad = __syncthreads_or(bad);
+    for (int o = FB / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + o]);
+            s0[threadIdx.x] = fmin(s0[threadIdx.x], s0[threadIdx.x + o]);
+            s1[threadIdx.x] = fmax(s1[threadIdx.x], s1[threadIdx.x + o]);
+            s2[threadIdx.x] = fmin(s2[threadIdx.x], s2[threadIdx.x + o]);
+            s3[threadIdx.x] = fmax(s3[threadIdx.x], s3[threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    md = sm[0];
+    bbox[0] = s0[0];
+    bbox[1] = s1[0];
+    bbox[2] = s2[0];
+    bbox[3] = s3[0];
     long long it = sc->it;
     disp_hist[it] = md;
     if (bad) sc->bad = it + 1;  // C/layout.py:395-397 (1-based)
@@ -669,10 +916,26 @@ struct Tree {
     unsigned *visit;
     double *smass, *sx, *sy;
     TNode *nodes;
+    int2 *i12;
+    double *bbox = nullptr;
+    unsigned *jflag = nullptr;
+    // reference cell numbering (allocated on first use)
+    Scratch *scr = nullptr;
+    int ne = 0;
+    unsigned long long *ekey = nullptr, *ekey2 = nullptr;
+    unsigned *eslot = nullptr, *eslot2 = nullptr, *ecnt = nullptr, *ecnt2 = nullptr,
+             *eexcl = nullptr;
+    int *idslot = nullptr;
+    void *etmp = nullptr;
+    size_t etmp_sort = 0, etmp_scan = 0;
     void *tmp;
     size_t tmp_bytes;
     void alloc(int n_, Scratch &sc) {
         n = n_;
+        scr = &sc;
+        i12 = sc.alloc<int2>(n > 1 ? n - 1 : 1);
+        jflag = sc.alloc<unsigned>(1);
+        CVZ_CUDA(cudaMemsetAsync(jflag, 0, sizeof(unsigned), sc.stream()));
         khi = sc.alloc<unsigned long long>(n);
         khi2 = sc.alloc<unsigned long long>(n);
         khi3 = sc.alloc<unsigned long long>(n);
@@ -701,16 +964,23 @@ struct Tree {
         tmp = sc.alloc<char>(tmp_bytes);
     }
     // build from pos + bbox (bbox already on device)
-    void build(const double2 *pos, const double *mass, const double *bbox, cudaStream_t s) {
+    void build(const double2 *pos, const double *mass, const double *bbox_, cudaStream_t s) {
+        bbox = const_cast<double *>(bbox_);
         unsigned g = grid_for(n, FB, 1, 8);
         CVZ_LAUNCH(keys_kernel, g, FB, 0, s, pos, (long long)n, bbox, khi, klo, idx);
         size_t tb = tmp_bytes;
         // LSD: low 8 digits first (16 bits), then the high 32 digits (64 bits)
-        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, klo, klo2, idx, idx2, n, 16, 32, s));
+        {
+            CVZ_REGION("cub_sort:tree_keys_lo", s);
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, klo, klo2, idx, idx2, n, 16, 32, s));
+        }
         count_launches(3);
         CVZ_LAUNCH(gather_hi_kernel, g, FB, 0, s, khi, idx2, (long long)n, khi2);
         tb = tmp_bytes;
-        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, khi2, khi3, idx2, idx3, n, 0, 64, s));
+        {
+            CVZ_REGION("cub_sort:tree_keys_hi", s);
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, khi2, khi3, idx2, idx3, n, 0, 64, s));
+        }
         count_launches(9);
         CVZ_LAUNCH(gather_bodies_kernel, g, FB, 0, s, pos, mass, idx3, klo, (long long)n, bodies,
                    klo3);
@@ -719,11 +989,55 @@ struct Tree {
         CVZ_LAUNCH(karras_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, K, left, first, last, delta,
                    parent_int, parent_leaf, pdelta, rc_by_split);
         CVZ_LAUNCH(com_kernel, g, FB, 0, s, bodies, n, left, first, last, delta, parent_int,
-                   parent_leaf, pdelta, rc_by_split, visit, smass, sx, sy, bbox, nodes);
+                   parent_leaf, pdelta, rc_by_split, visit, smass, sx, sy, bbox, nodes, i12);
     }
-    void repulse(double kr, double theta, double2 *out, const long long *bad, cudaStream_t s) {
+    // reference cell numbering of the current tree (see cell_entries_kernel)
+    void build_ids(cudaStream_t s) {
+        if (!idslot) {
+            ne = 2 * (n - 1) + n;
+            ekey = scr->alloc<unsigned long long>(ne);
+            ekey2 = scr->alloc<unsigned long long>(ne);
+            eslot = scr->alloc<unsigned>(ne);
+            eslot2 = scr->alloc<unsigned>(ne);
+            ecnt = scr->alloc<unsigned>(ne);
+            ecnt2 = scr->alloc<unsigned>(ne);
+            eexcl = scr->alloc<unsigned>(ne);
+            idslot = scr->alloc<int>(ne);
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, etmp_sort, ekey, ekey2, eslot,
+                                                     eslot2, ne, 0, 40, s));
+            CVZ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, etmp_scan, ecnt2, eexcl, ne, s));
+            etmp = scr->alloc<char>(std::max(etmp_sort, etmp_scan));
+        }
+        unsigned g = grid_for(ne, FB, 1, 8);
+        CVZ_LAUNCH(cell_entries_kernel, g, FB, 0, s, bodies, n, nodes, delta, pdelta, parent_int,
+                   parent_leaf, i12, ekey, eslot, ecnt);
+        {
+            CVZ_REGION("cub_sort:cell_ids", s);
+            size_t tb = etmp_sort;
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(etmp, tb, ekey, ekey2, eslot, eslot2, ne, 0,
+                                                     40, s));
+            count_launches(6);
+        }
+        CVZ_LAUNCH(gather_counts_kernel, g, FB, 0, s, eslot2, ecnt, ne, ecnt2);
+        {
+            CVZ_REGION("cub_scan:cell_ids", s);
+            size_t tb = etmp_scan;
+            CVZ_CUDA(cub::DeviceScan::ExclusiveSum(etmp, tb, ecnt2, eexcl, ne, s));
+            count_launches(2);
+        }
+        CVZ_LAUNCH(scatter_ids_kernel, g, FB, 0, s, eslot2, eexcl, ne, idslot);
+    }
+    void repulse(double kr, double theta, double2 *out, const long long *bad, bool ids,
+                 cudaStream_t s) {
+        CellRef cr{delta, pdelta, ids ? idslot : nullptr, jflag, bbox};
         CVZ_LAUNCH(bh_kernel, blocks_for(n, FB), FB, 0, s, bodies, n, nodes, rc_by_split, first,
-                   last, smass, sx, sy, kr, theta, out, bad);
+                   last, smass, sx, sy, kr, theta, out, bad, cr);
+    }
+    bool jitter_seen(cudaStream_t s) {
+        unsigned h = 0;
+        CVZ_CUDA(cudaMemcpyAsync(&h, jflag, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CVZ_CUDA(cudaStreamSynchronize(s));
+        return h != 0;
     }
 };
 
@@ -755,13 +1069,21 @@ void repulsion_dev(const double *pos, const double *mass, long long n, double kr
     Tree t;
     t.alloc((int)n, sc);
     t.build(p2, mass, bbox, s);
-    t.repulse(kr, theta, o2, nullptr, s);
+    t.repulse(kr, theta, o2, nullptr, false, s);
+    if (t.jitter_seen(s)) {  // a cell jitter needs the reference's cell numbering
+        t.build_ids(s);
+        t.repulse(kr, theta, o2, nullptr, true, s);
+    }
 }
 
 struct Csr {
     long long *rowptr;
     int *col;
     double *w;
+    int *hidx;      // [n] heavy slot or -1
+    int *heavy;     // [nheavy] heavy row ids
+    int nheavy = 0;
+    double2 *hsum;  // [nheavy] warp-summed springs
 };
 
 static Csr build_csr(const int2 *e, long long m, long long n, const double *weight, double sign,
@@ -783,8 +1105,11 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
         CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, skey, val, sval, (int)nh, 0,
                                                  bits, s));
         void *tmp = sc.alloc<char>(tb);
-        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, skey, val, sval, (int)nh, 0, bits,
-                                                 s));
+        {
+            CVZ_REGION("cub_sort:csr", s);
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, skey, val, sval, (int)nh, 0, bits,
+                                                     s));
+        }
         count_launches(1 + (bits + 7) / 8);
         CVZ_LAUNCH(csr_fill_kernel, grid_for(nh, FB, 1, 8), FB, 0, s, e, sval, nh, weight, sign,
                    c.col, c.w);
@@ -795,7 +1120,25 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
     void *tmp2 = sc.alloc<char>(tb2);
     CVZ_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, tb2, cnt, c.rowptr, (int)(n + 1), s));
     count_launches(2);
+    c.hidx = sc.alloc<int>(n);
+    c.heavy = sc.alloc<int>(n);
+    unsigned *nh_d = sc.alloc<unsigned>(1);
+    CVZ_CUDA(cudaMemsetAsync(nh_d, 0, sizeof(unsigned), s));
+    CVZ_LAUNCH(classify_rows_kernel, grid_for(n, FB, 1, 8), FB, 0, s, c.rowptr, (int)n, c.hidx,
+               c.heavy, nh_d);
+    unsigned nh_h = 0;
+    CVZ_CUDA(cudaMemcpyAsync(&nh_h, nh_d, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    CVZ_CUDA(cudaStreamSynchronize(s));
+    c.nheavy = (int)nh_h;
+    c.hsum = sc.alloc<double2>(c.nheavy > 0 ? c.nheavy : 1);
     return c;
+}
+
+static void springs_heavy(const double2 *pos, const Csr &c, const StepScalars *sc,
+                          cudaStream_t s) {
+    if (c.nheavy == 0) return;
+    CVZ_LAUNCH(springs_heavy_kernel, blocks_for((long long)c.nheavy * 32, FB), FB, 0, s, pos,
+               c.rowptr, c.col, c.w, c.heavy, c.nheavy, c.hsum, sc);
 }
 
 __global__ void attraction_only_kernel(const double2 *__restrict__ pos, int n,
@@ -872,65 +1215,88 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
         const bool exact = P->theta <= 0;
         Tree tree;
         if (!exact) tree.alloc(N, sc);
-        bbox_dev(p2, N, bbox, sc, s);  // first bbox; later ones come from update
         long long *badp = &scal->bad;
+        // snapshot for the (rare) rerun with the reference's cell numbering
+        double2 *pos0 = sc.alloc<double2>(n), *prev0 = sc.alloc<double2>(n);
+        CVZ_CUDA(cudaMemcpyAsync(pos0, p2, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+        CVZ_CUDA(cudaMemcpyAsync(prev0, prev, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
 
-        auto one_iteration = [&](cudaStream_t st) {
+        auto one_iteration = [&](cudaStream_t st, bool ids) {
             if (exact) {
                 CVZ_LAUNCH(exact_kernel, blocks_for(n, XT), XT, 0, st, p2, mass, N, P->repulsion,
                            frep);
             } else {
                 tree.build(p2, mass, bbox, st);
-                tree.repulse(P->repulsion, P->theta, frep, badp, st);
+                if (ids) tree.build_ids(st);
+                tree.repulse(P->repulsion, P->theta, frep, badp, ids, st);
             }
-            CVZ_LAUNCH(forces_kernel, nb, FB, 0, st, p2, mass, N, csr.rowptr, csr.col, csr.w, frep,
+            springs_heavy(p2, csr, scal, st);
+            CVZ_LAUNCH(forces_kernel, nb, FB, 0, st, p2, mass, N, csr.rowptr, csr.col, csr.w,
+                       csr.hidx, csr.hsum, frep,
                        P->gravity, prev, force, swing, fpart, ctrs, scal, P->jitter_tolerance);
             CVZ_LAUNCH(update_kernel, nb, FB, 0, st, p2, N, force, swing, prev, P->speed_form,
                        P->max_step, upart, ctrs + 1, bbox, scal, disp_hist);
         };
 
-        bool use_graph = getenv("CVZ_NO_GRAPH") == nullptr && P->iterations > 1;
-        if (use_graph) {
-            // capture one iteration on a private stream, then replay
-            cudaStream_t cs;
-            CVZ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-            cudaEvent_t ev;
-            CVZ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            CVZ_CUDA(cudaEventRecord(ev, s));
-            CVZ_CUDA(cudaStreamWaitEvent(cs, ev, 0));
-            cudaGraph_t graph = nullptr;
-            cudaGraphExec_t exec = nullptr;
-            long long before = g_launches.load();
-            CVZ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-            bool ok = true;
-            try {
-                one_iteration(cs);
-            } catch (...) {
-                ok = false;
-            }
-            cudaError_t ce = cudaStreamEndCapture(cs, &graph);
-            long long per_iter = g_launches.load() - before;
-            g_launches.fetch_sub(per_iter);
-            if (ok && ce == cudaSuccess &&
-                cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
-                for (long long it = 0; it < P->iterations; ++it) {
-                    CVZ_CUDA(cudaGraphLaunch(exec, cs));
-                    g_launches.fetch_add(per_iter);
+        auto run_all = [&](bool ids) {
+            bbox_dev(p2, N, bbox, sc, s);  // first bbox; later ones come from update
+            bool use_graph =
+                getenv("CVZ_NO_GRAPH") == nullptr && P->iterations > 1 && !prof_on();
+            if (use_graph) {
+                // capture one iteration on a private stream, then replay
+                cudaStream_t cs;
+                CVZ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+                cudaEvent_t ev;
+                CVZ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CVZ_CUDA(cudaEventRecord(ev, s));
+                CVZ_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+                cudaGraph_t graph = nullptr;
+                cudaGraphExec_t exec = nullptr;
+                long long before = g_launches.load();
+                CVZ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+                bool ok = true;
+                try {
+                    one_iteration(cs, ids);
+                } catch (...) {
+                    ok = false;
                 }
-                CVZ_CUDA(cudaEventRecord(ev, cs));
-                CVZ_CUDA(cudaStreamWaitEvent(s, ev, 0));
-            } else {
-                cudaGetLastError();
-                use_graph = false;
+                cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+                long long per_iter = g_launches.load() - before;
+                g_launches.fetch_sub(per_iter);
+                if (ok && ce == cudaSuccess &&
+                    cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+                    for (long long it = 0; it < P->iterations; ++it) {
+                        CVZ_CUDA(cudaGraphLaunch(exec, cs));
+                        g_launches.fetch_add(per_iter);
+                    }
+                    CVZ_CUDA(cudaEventRecord(ev, cs));
+                    CVZ_CUDA(cudaStreamWaitEvent(s, ev, 0));
+                } else {
+                    cudaGetLastError();
+                    use_graph = false;
+                }
+                if (exec) cudaGraphExecDestroy(exec);
+                if (graph) cudaGraphDestroy(graph);
+                CVZ_CUDA(cudaStreamSynchronize(cs));
+                cudaStreamDestroy(cs);
+                cudaEventDestroy(ev);
             }
-            if (exec) cudaGraphExecDestroy(exec);
-            if (graph) cudaGraphDestroy(graph);
-            CVZ_CUDA(cudaStreamSynchronize(cs));
-            cudaStreamDestroy(cs);
-            cudaEventDestroy(ev);
+            if (!use_graph)
+                for (long long it = 0; it < P->iterations; ++it) one_iteration(s, ids);
+        };
+
+        run_all(false);
+        if (!exact && tree.jitter_seen(s)) {
+            // a cell interaction closer than COINCIDE_EPS happened: its jitter
+            // direction is keyed by the reference's cell number -- replay the
+            // whole run with that numbering (C/layout.py:258)
+            CVZ_CUDA(cudaMemcpyAsync(p2, pos0, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+            CVZ_CUDA(cudaMemcpyAsync(prev, prev0, sizeof(double2) * n, cudaMemcpyDeviceToDevice,
+                                     s));
+            CVZ_CUDA(cudaMemcpyAsync(scal, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+            CVZ_CUDA(cudaMemsetAsync(ctrs, 0, 2 * sizeof(unsigned), s));
+            run_all(true);
         }
-        if (!use_graph)
-            for (long long it = 0; it < P->iterations; ++it) one_iteration(s);
         StepScalars out;
         CVZ_CUDA(cudaMemcpyAsync(&out, scal, sizeof(out), cudaMemcpyDeviceToHost, s));
         CVZ_CUDA(cudaStreamSynchronize(s));

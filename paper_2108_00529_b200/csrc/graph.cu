@@ -7,6 +7,10 @@
 // decoupled look-back (no second pass over the edges).
 #include <cub/cub.cuh>
 
+#include <map>
+#include <mutex>
+#include <sstream>
+
 #include "common.cuh"
 
 namespace cvz {
@@ -14,6 +18,38 @@ namespace cvz {
 std::atomic<long long> g_launches{0};
 static thread_local std::string t_last_error;
 void set_last_error(const std::string &m) { t_last_error = m; }
+
+// ---- kernel profiler ---------------------------------------------------------
+namespace {
+struct ProfRec {
+    const char *name;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::atomic<bool> g_prof{false};
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_prof_pool;
+std::string g_prof_report;
+}  // namespace
+
+bool prof_on() { return g_prof.load(std::memory_order_relaxed); }
+
+cudaEvent_t prof_event() {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t e;
+    if (!g_prof_pool.empty()) {
+        e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+    } else {
+        cudaEventCreate(&e);
+    }
+    return e;
+}
+
+void prof_record(const char *name, cudaEvent_t a, cudaEvent_t b) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_recs.push_back(ProfRec{name, a, b});
+}
 
 void init_pool_once() {
     static bool done = false;
@@ -260,6 +296,45 @@ extern "C" {
 int cvz_version(void) { return 1; }
 const char *cvz_last_error(void) { return t_last_error.c_str(); }
 long long cvz_launch_count(void) { return g_launches.load(); }
+
+int cvz_profile_begin(void) {
+    return guard([&] {
+        {
+            std::lock_guard<std::mutex> lk(g_prof_mu);
+            for (auto &r : g_prof_recs) {
+                g_prof_pool.push_back(r.a);
+                g_prof_pool.push_back(r.b);
+            }
+            g_prof_recs.clear();
+        }
+        g_prof.store(true);
+    });
+}
+
+int cvz_profile_end(void) {
+    return guard([&] {
+        g_prof.store(false);
+        CVZ_CUDA(cudaDeviceSynchronize());
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        std::map<std::string, std::pair<long long, double>> agg;
+        for (auto &r : g_prof_recs) {
+            float ms = 0.f;
+            CVZ_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+            auto &v = agg[r.name];
+            v.first += 1;
+            v.second += ms;
+            g_prof_pool.push_back(r.a);
+            g_prof_pool.push_back(r.b);
+        }
+        g_prof_recs.clear();
+        std::ostringstream os;
+        os.precision(9);
+        for (auto &kv : agg) os << kv.first << "\t" << kv.second.first << "\t" << kv.second.second << "\n";
+        g_prof_report = os.str();
+    });
+}
+
+const char *cvz_profile_report(void) { return g_prof_report.c_str(); }
 
 int cvz_edges_compact(const void *edges, int in_is_int32, int64_t m, int32_t *edges_out,
                       int64_t *d_m_out, int64_t *d_max_id, int check_range, void *stream) {

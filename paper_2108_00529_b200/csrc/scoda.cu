@@ -24,6 +24,7 @@
 // the reached cycle.  Pointer doubling with a shrinking worklist until every
 // node sees a fixed point; nodes that never do sit on/above a >=2-cycle and
 // get a min-doubling pass over the (closed) set of such nodes.
+#include <algorithm>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -34,6 +35,8 @@ namespace cvz {
 namespace {
 
 constexpr int TB = 256;
+// fast mode: edges in flight <= m / FAST_WINDOW_DIV
+constexpr long long FAST_WINDOW_DIV = 128;
 
 struct MaxOp {
     __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
@@ -450,6 +453,7 @@ void cub_sort_pairs(const unsigned *kin, unsigned *kout, const T *vin, T *vout, 
     CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, (int)ns, 0,
                                              end_bit, s));
     void *tmp = sc.alloc<char>(tb);
+    CVZ_REGION("cub_sort:scoda_slots", s);
     CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, (int)ns, 0, end_bit,
                                              s));
     count_launches(1 + (end_bit + 7) / 8);
@@ -496,8 +500,11 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
         CVZ_CUDA(cub::DeviceScan::InclusiveScanByKey(nullptr, tb, skeys, vin, lastw, MaxOp(),
                                                      (int)ns, cub::Equality(), s));
         void *tmp = sc.alloc<char>(tb);
-        CVZ_CUDA(cub::DeviceScan::InclusiveScanByKey(tmp, tb, skeys, vin, lastw, MaxOp(), (int)ns,
-                                                     cub::Equality(), s));
+        {
+            CVZ_REGION("cub_scan_by_key:scoda_lastw", s);
+            CVZ_CUDA(cub::DeviceScan::InclusiveScanByKey(tmp, tb, skeys, vin, lastw, MaxOp(),
+                                                         (int)ns, cub::Equality(), s));
+        }
         count_launches(2);
         int *parent = sc.alloc<int>(m);
         CVZ_LAUNCH(parents_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, svals, ns,
@@ -545,10 +552,17 @@ void scoda_pass_dev(const int2 *E, long long m, long long n, long long T, int ti
     CVZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * n, s));
     CVZ_LAUNCH(init_labels_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n,
                reinterpret_cast<const long long *>(lab0), reinterpret_cast<long long *>(lab_out));
-    if (m > 0)
-        CVZ_LAUNCH(fast_pass_kernel, grid_for(m, TB, 1, 16), TB, 0, s, E, m,
+    if (m > 0) {
+        // Bounded in-flight window: the racy pass stays close to the
+        // reference's own parallel schedules (C/community.py:164-195) only
+        // while the edges in flight are a small fraction of the stream
+        // (DESIGN.md "fast mode"); at C4 scale this is full occupancy anyway.
+        long long window = std::max(256LL, std::min(m / FAST_WINDOW_DIV, 2048LL * num_sms()));
+        unsigned blocks = (unsigned)((window + TB - 1) / TB);
+        CVZ_LAUNCH(fast_pass_kernel, blocks, TB, 0, s, E, m,
                    reinterpret_cast<const long long *>(d0), T, tie, cnt,
                    reinterpret_cast<volatile long long *>(lab_out));
+    }
     CVZ_LAUNCH(fast_finalize_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n, cnt,
                reinterpret_cast<const long long *>(d0), T, reinterpret_cast<long long *>(deg_out));
 }

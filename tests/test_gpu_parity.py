@@ -9,8 +9,9 @@ Gates (stated here):
     the same order); Barnes-Hut repulsion: max |dF| <= 1e-9 * max |F|;
   * layout trajectories: max |dpos| <= 1e-7 * layout diameter over the
     golden runs (1..30 iterations);
-  * fast (racy) community mode: |Q_fast - Q_det| <= 0.02, community count
-    within 5 %, top-10 size share within 0.02.
+  * fast (racy) community mode: inside the envelope of the reference's own
+    parallel schedules (workers 1/4/64) widened by Q +- 0.02, k +- 5 %,
+    top-10 size share +- 0.02.
 """
 
 import numpy as np
@@ -189,24 +190,38 @@ def test_reference_community_kats(cv):
                               cv.ThresholdSchedule(base=2))
 
 
+def _top10(lab):
+    c = np.sort(np.unique(lab, return_counts=True)[1])[::-1]
+    return c[:10].sum() / len(lab)
+
+
 @pytest.mark.parametrize("name", ["C1", "C2"])
 def test_fast_mode_within_tolerance(cv, orc, name):
+    """Fast (racy) mode must land inside the envelope of the reference's own
+    parallel schedules (SPEC: "result is order-dependent under parallelism
+    (accepted, tested statistically)"; C/community.py:164-195): the oracle
+    run with workers in {1, 4, 64} x 3 seeds gives [Q_min, Q_max],
+    [k_min, k_max] and the top-10 share range; fast mode must lie within
+    Q +- 0.02, k within [0.95 k_min, 1.05 k_max], top-10 share +- 0.02."""
     from paper_2108_00529_b200 import synth
     e = synth.config_graph(name)
     g = cv.from_edge_array(e)
     base = cv.degree_stats(g).mode_degree
-    det = cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1)
+    n, ee, deg = orc.from_edge_array(e)
+    qs, ks, ts = [], [], []
+    for workers, seeds in ((1, [0]), (4, [0, 1, 2]), (64, [0, 1, 2])):
+        for seed in seeds:
+            lab, _, _ = orc.detect_communities(n, ee, deg, base, 10, seed, workers=workers)
+            qs.append(orc.modularity(ee, deg, lab))
+            ks.append(len(np.unique(lab)))
+            ts.append(_top10(lab))
     fast = cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1, mode="fast")
-    q_det = orc.modularity(g.edges, g.degree, det.label)
     q_fast = orc.modularity(g.edges, g.degree, fast.label)
-    assert abs(q_fast - q_det) <= 0.02, (q_fast, q_det)
-    cd, cf = det.community_count, fast.community_count
-    assert abs(cf - cd) <= 0.05 * cd, (cf, cd)
-
-    def top10(lab):
-        c = np.sort(np.unique(lab, return_counts=True)[1])[::-1]
-        return c[:10].sum() / len(lab)
-    assert abs(top10(fast.label) - top10(det.label)) <= 0.02
+    assert min(qs) - 0.02 <= q_fast <= max(qs) + 0.02, (q_fast, min(qs), max(qs))
+    kf = fast.community_count
+    assert 0.95 * min(ks) <= kf <= 1.05 * max(ks), (kf, min(ks), max(ks))
+    t = _top10(fast.label)
+    assert min(ts) - 0.02 <= t <= max(ts) + 0.02, (t, min(ts), max(ts))
     # every label is one of its own members (C/community.py:123-161 invariant)
     lab = fast.label
     assert np.all(lab[lab] == lab)
@@ -311,19 +326,45 @@ def test_contract_at_scale(cv, orc):
 
 # ----------------------------------------------------------------- layout
 def test_repulsion_golden(cv):
+    """BH / exact repulsion vs the reference (C/layout.py:215-290) on the
+    golden cases, including all-coincident, half-coincident and 1e-3-cloud
+    inputs whose coincident-point jitter is keyed by the reference's
+    sequential cell numbering (C/layout.py:258) -- rebuilt on the GPU.
+    Exact mode without coincident points: bit-identical; otherwise
+    max |dF| <= 1e-9 * max |F|."""
     d = golden("layout")
     for i in cases(d, "f"):
         pos, mass = d[f"f{i}_pos"], d[f"f{i}_mass"]
         theta = float(d[f"f{i}_theta"][0])
         out = cv.repulsion_forces(pos, mass, 80.0, theta)
         ref = d[f"f{i}_out"]
+        assert np.all(np.isfinite(out)), i
         coincident = len(np.unique(pos, axis=0)) < len(pos)
         if theta == 0 and not coincident:
             assert np.array_equal(out, ref), i
-        else:
-            scale = np.abs(ref).max()
-            tol = 1e-9 if not coincident else 1e-3  # jitter keys differ for cells
-            assert np.max(np.abs(out - ref)) <= tol * scale, (i, np.max(np.abs(out - ref)) / scale)
+            continue
+        scale = np.abs(ref).max()
+        err = np.max(np.abs(out - ref))
+        assert err <= 1e-9 * scale, (i, err / scale)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_repulsion_clusters_vs_oracle(cv, orc, seed):
+    """Clustered / duplicated bodies stress the coincident-point paths: leaf
+    jitter (pair ids), cell jitter (reference cell numbering), depth-40
+    aggregates minus self, and the chain cells above an aggregate."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(50, 3000))
+    centers = rng.uniform(-20, 20, (int(rng.integers(1, 12)), 2))
+    pos = centers[rng.integers(0, len(centers), n)]
+    scale = [0.0, 1e-9, 1e-6, 3e-5, 1e-3, 0.1][seed]
+    pos = pos + rng.normal(0, scale, (n, 2)) * (rng.random((n, 1)) < 0.7)
+    mass = rng.uniform(1, 10, n)
+    for theta in (0.3, 0.5, 0.9):
+        ref = orc.repulsion_forces(pos, mass, 80.0, theta)
+        out = cv.repulsion_forces(pos, mass, 80.0, theta)
+        err = np.max(np.abs(out - ref))
+        assert err <= 1e-9 * np.abs(ref).max(), (theta, err / np.abs(ref).max())
 
 
 def test_bh_vs_exact_properties(cv):
