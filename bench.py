@@ -355,6 +355,11 @@ def main():
     peak, _src = peak_hbm()
     roof, top = roofline(r["prof"], st, peak)
     roof["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs ({_src})"
+    try:  # DRAM bytes per launch from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            roof["traffic"] = json.load(fh).get(roof["kernel"])
+    except (OSError, ValueError):
+        pass
     value = r["m_in"] * ws / (r["ms_step"] / 1000.0)
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws,

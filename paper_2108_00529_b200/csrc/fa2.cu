@@ -571,6 +571,144 @@ __global__ void __launch_bounds__(FB) bh_kernel(const Body *__restrict__ bodies,
     }
 }
 
+// ---- flattened traversal --------------------------------------------------
+// The binary radix tree has "transparent" nodes (the inner halves of a quad
+// cell) that the reference tree does not have and that are always opened.
+// After the COM pass every non-transparent node and every body leaf is
+// written into one flat array whose open/skip links already step over the
+// transparent nodes, so the walk visits exactly the reference's cells and
+// leaves, and a leaf is just a node that always passes the opening test
+// (side2 = -1) -- one uniform loop body, no leaf/cell divergence.
+struct __align__(16) FNode {
+    double x, y, m, side2;  // COM (body position for a leaf), mass, cell side^2
+    int open, skip;         // flat links: first child / DFS successor (-1 = end)
+    int kind;               // 1 cell, 2 depth-40 aggregate, 3 body leaf
+    int aux;                // cell: binary node id; leaf: sorted body index
+};
+
+__device__ __forceinline__ int flat_resolve(int raw, int n, const TNode *__restrict__ nodes,
+                                            const int *__restrict__ left) {
+    while (true) {
+        if (raw == END) return -1;
+        if (raw < 0) return n - 1 + ~raw;
+        if (nodes[raw].kind != 0) return raw;
+        raw = left[raw];
+    }
+}
+
+__global__ void flatten_kernel(int n, const TNode *__restrict__ nodes,
+                               const int *__restrict__ left, const int *__restrict__ rc_by_split,
+                               const Body *__restrict__ bodies, FNode *__restrict__ fn) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 2 * n - 1;
+         t += gridDim.x * blockDim.x) {
+        FNode f;
+        if (t < n - 1) {
+            TNode c = nodes[t];
+            if (c.kind == 0) continue;
+            f.x = c.comx;
+            f.y = c.comy;
+            f.m = c.mass;
+            f.side2 = c.kind == 2 ? -1.0 : c.side2;
+            f.open = flat_resolve(c.left, n, nodes, left);
+            f.skip = flat_resolve(c.skip, n, nodes, left);
+            f.kind = c.kind;
+            f.aux = t;
+        } else {
+            int q = t - (n - 1);
+            Body b = bodies[q];
+            f.x = b.x;
+            f.y = b.y;
+            f.m = b.m;
+            f.side2 = -1.0;
+            f.open = -1;
+            f.skip = flat_resolve(q == n - 1 ? END : rc_by_split[q], n, nodes, left);
+            f.kind = 3;
+            f.aux = q;
+        }
+        fn[t] = f;
+    }
+}
+
+__global__ void __launch_bounds__(FB) bh_flat_kernel(const Body *__restrict__ bodies, int n,
+                                                     const FNode *__restrict__ fn,
+                                                     const int *__restrict__ first,
+                                                     const int *__restrict__ last,
+                                                     const double *__restrict__ smass,
+                                                     const double *__restrict__ sx,
+                                                     const double *__restrict__ sy, double kr,
+                                                     double theta, double2 *__restrict__ out,
+                                                     const long long *__restrict__ bad,
+                                                     CellRef cr) {
+    if (bad && *bad) return;
+    const double th2 = mul(theta, theta);
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        Body me = bodies[p];
+        const long long i = me.orig;
+        const double xi = me.x, yi = me.y, mi = me.m;
+        const double kmi = mul(kr, mi);  // (kr * mi) * mj, the reference's order
+        double fx = 0.0, fy = 0.0;
+        int c = 0;  // root cell (n >= 2)
+        while (c >= 0) {
+            const FNode t = fn[c];
+            double mc = t.m, dx = sub(xi, t.x), dy = sub(yi, t.y);
+            double d2 = add(mul(dx, dx), mul(dy, dy));
+            bool self_out = false;
+            if (t.kind == 2 && p >= first[t.aux] && p <= last[t.aux]) {
+                // aggregate holding i: the reference tests the single-child
+                // cells above it with the FULL COM (self included) and
+                // approximates there if one passes (C/layout.py:253-261); only
+                // the depth-40 cell itself subtracts self (:247-252)
+                int a = t.aux;
+                int ltop = a == 0 ? 0 : (cr.pdelta[a] >> 1) + 1;
+                double s39 = 2.0 * ldexp(root_geo(cr.bbox).half, -(MAX_DEPTH - 1));
+                if (!(ltop <= MAX_DEPTH - 1 && mul(s39, s39) < mul(th2, d2))) {
+                    double m2 = sub(smass[a], mi);
+                    if (m2 <= 0.0) {
+                        c = t.skip;
+                        continue;
+                    }
+                    double x2 = sub(sx[a], mul(mi, xi)), y2 = sub(sy[a], mul(mi, yi));
+                    mc = m2;
+                    dx = sub(xi, x2 / m2);
+                    dy = sub(yi, y2 / m2);
+                    d2 = add(mul(dx, dx), mul(dy, dy));
+                    self_out = true;
+                }
+            }
+            // leaves and aggregates carry side2 = -1: always approximated
+            if (t.side2 < mul(th2, d2)) {  // C/layout.py:256-261
+                if (!(t.kind == 3 && t.aux == p)) {  // j == i skipped (:237-238)
+                    double f;
+                    if (d2 >= EPS * EPS) {
+                        f = mul(mul(kmi, mc), inv_d2(d2));
+                    } else {  // coincident: reference jitter (C/layout.py:85-94)
+                        long long key;
+                        if (t.kind == 3) {
+                            key = bodies[t.aux].orig;
+                        } else if (cr.idslot) {
+                            key = (long long)n + ref_cell_id(t.aux, cr.delta, cr.pdelta,
+                                                             cr.idslot, t.kind,
+                                                             root_geo(cr.bbox).half,
+                                                             mul(th2, d2), self_out);
+                        } else {
+                            atomicOr(cr.jflag, 1u);
+                            key = (long long)n + t.aux;
+                        }
+                        double d = separation(dx, dy, i, key);
+                        f = mul(kmi, mc) / mul(d, d);
+                    }
+                    fx = add(fx, mul(f, dx));
+                    fy = add(fy, mul(f, dy));
+                }
+                c = t.skip;
+            } else {
+                c = t.open;
+            }
+        }
+        out[i] = make_double2(fx, fy);
+    }
+}
+
 // exact O(n^2) (C/layout.py:273-290): j ascending, same op order as the CPU
 constexpr int XT = 256;
 __global__ void __launch_bounds__(XT) exact_kernel(const double2 *__restrict__ pos,
@@ -917,6 +1055,7 @@ struct Tree {
     double *smass, *sx, *sy;
     TNode *nodes;
     int2 *i12;
+    FNode *fn;
     double *bbox = nullptr;
     unsigned *jflag = nullptr;
     // reference cell numbering (allocated on first use)
@@ -934,6 +1073,7 @@ struct Tree {
         n = n_;
         scr = &sc;
         i12 = sc.alloc<int2>(n > 1 ? n - 1 : 1);
+        fn = sc.alloc<FNode>(2 * n - 1);
         jflag = sc.alloc<unsigned>(1);
         CVZ_CUDA(cudaMemsetAsync(jflag, 0, sizeof(unsigned), sc.stream()));
         khi = sc.alloc<unsigned long long>(n);
@@ -990,7 +1130,11 @@ struct Tree {
                    parent_int, parent_leaf, pdelta, rc_by_split);
         CVZ_LAUNCH(com_kernel, g, FB, 0, s, bodies, n, left, first, last, delta, parent_int,
                    parent_leaf, pdelta, rc_by_split, visit, smass, sx, sy, bbox, nodes, i12);
+        if (flat())
+            CVZ_LAUNCH(flatten_kernel, grid_for(2LL * n, FB, 1, 8), FB, 0, s, n, nodes, left,
+                       rc_by_split, bodies, fn);
     }
+    bool flat() const { return getenv("CVZ_BH_BINARY") == nullptr; }
     // reference cell numbering of the current tree (see cell_entries_kernel)
     void build_ids(cudaStream_t s) {
         if (!idslot) {
@@ -1030,8 +1174,12 @@ struct Tree {
     void repulse(double kr, double theta, double2 *out, const long long *bad, bool ids,
                  cudaStream_t s) {
         CellRef cr{delta, pdelta, ids ? idslot : nullptr, jflag, bbox};
-        CVZ_LAUNCH(bh_kernel, blocks_for(n, FB), FB, 0, s, bodies, n, nodes, rc_by_split, first,
-                   last, smass, sx, sy, kr, theta, out, bad, cr);
+        if (flat())
+            CVZ_LAUNCH(bh_flat_kernel, blocks_for(n, FB), FB, 0, s, bodies, n, fn, first, last,
+                       smass, sx, sy, kr, theta, out, bad, cr);
+        else
+            CVZ_LAUNCH(bh_kernel, blocks_for(n, FB), FB, 0, s, bodies, n, nodes, rc_by_split,
+                       first, last, smass, sx, sy, kr, theta, out, bad, cr);
     }
     bool jitter_seen(cudaStream_t s) {
         unsigned h = 0;
