@@ -12,6 +12,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <tuple>
+#include <type_traits>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -79,6 +81,32 @@ struct ProfScope {
         ::cvz::g_launches.fetch_add(1, std::memory_order_relaxed);      \
         CVZ_CUDA(cudaGetLastError());                                   \
     } while (0)
+
+// Cooperative launch (grid-wide barriers inside the kernel): the grid is the
+// number of CTAs that can be co-resident on all SMs.
+template <class... KArgs, class... Args>
+void coop_launch(const char *name, void (*kernel)(KArgs...), int block, cudaStream_t s,
+                 Args... args) {
+    int per_sm = 0;
+    CVZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0));
+    int dev = 0, sms = 0;
+    CVZ_CUDA(cudaGetDevice(&dev));
+    CVZ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    dim3 grid((unsigned)(per_sm > 0 ? per_sm : 1) * (unsigned)sms);
+    // arguments converted to the kernel's exact parameter types first
+    std::tuple<typename std::decay<KArgs>::type...> typed(args...);
+    void *argv[sizeof...(KArgs) > 0 ? sizeof...(KArgs) : 1];
+    std::apply([&](auto &...a) {
+        int i = 0;
+        ((argv[i++] = static_cast<void *>(&a)), ...);
+    }, typed);
+    ProfScope ps(name, s);
+    CVZ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kernel), grid, dim3(block),
+                                         argv, 0, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+#define CVZ_COOP(kernel, block, stream, ...) \
+    ::cvz::coop_launch(#kernel, kernel, (block), (stream), __VA_ARGS__)
 
 // Time a library primitive (CUB) under `name` (same rules as CVZ_LAUNCH).
 #define CVZ_REGION(name, stream) ::cvz::ProfScope _cvz_region(name, (stream))

@@ -25,6 +25,10 @@
 // node sees a fixed point; nodes that never do sit on/above a >=2-cycle and
 // get a min-doubling pass over the (closed) set of such nodes.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -32,11 +36,12 @@
 #include "common.cuh"
 
 namespace cvz {
+namespace cg = cooperative_groups;
 namespace {
 
 constexpr int TB = 256;
 // fast mode: edges in flight <= m / FAST_WINDOW_DIV
-constexpr long long FAST_WINDOW_DIV = 128;
+constexpr long long FAST_WINDOW_DIV = 64;
 
 struct MaxOp {
     __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
@@ -51,21 +56,88 @@ __global__ void gather_edges_kernel(const int2 *__restrict__ e, const long long 
 
 // ---- deterministic pass --------------------------------------------------
 
-__global__ void slot_keys_kernel(const int2 *__restrict__ E, long long m,
-                                 const long long *__restrict__ d0, long long T, unsigned n,
-                                 uint2 *__restrict__ keys, uint2 *__restrict__ vals) {
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
-         k += (long long)gridDim.x * blockDim.x) {
-        int2 p = __ldg(E + k);
-        unsigned ku = (unsigned)p.x, kv = (unsigned)p.y;
-        if (p.x == p.y) kv = n;  // a self-loop bumps its counter once
-        if (d0) {
-            if (__ldg(d0 + p.x) > T) ku = n;
-            if (__ldg(d0 + p.y) > T) kv = n;
+// Slot keys in stream order, with the slots that can never matter dropped
+// on the fly (stable, single pass, decoupled look-back): the second slot of a
+// self-loop (its counter is bumped once) and slots of nodes whose seeded
+// counter already exceeds T (they can neither change nor merge).  Every
+// dropped slot keeps counter T+1 (inactive).
+constexpr int SITEMS = 4;
+constexpr int STILE = TB * SITEMS;
+
+__global__ void __launch_bounds__(TB) slot_keys_kernel(
+    const int2 *__restrict__ E, long long m, const long long *__restrict__ d0, long long T,
+    unsigned *__restrict__ keys, unsigned *__restrict__ vals, LookbackState st,
+    unsigned long long *__restrict__ d_count, unsigned num_tiles) {
+    __shared__ unsigned s_tile;
+    __shared__ unsigned long long s_prefix;
+    const unsigned tile = acquire_tile(st, &s_tile);
+    const long long base = (long long)tile * STILE;
+    int2 e[SITEMS];
+    bool ku[SITEMS], kv[SITEMS];
+#pragma unroll
+    for (int j = 0; j < SITEMS; ++j) {
+        long long k = base + (long long)j * TB + threadIdx.x;
+        ku[j] = kv[j] = false;
+        if (k < m) {
+            int2 p = __ldg(E + k);
+            e[j] = p;
+            ku[j] = !d0 || __ldg(d0 + p.x) <= T;
+            kv[j] = p.x != p.y && (!d0 || __ldg(d0 + p.y) <= T);
         }
-        keys[k] = make_uint2(ku, kv);
-        vals[k] = make_uint2((unsigned)(2 * k), (unsigned)(2 * k + 1));
     }
+    constexpr int NW = TB / 32;
+    __shared__ unsigned s_cnt[SITEMS * NW];
+    __shared__ unsigned s_total;
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    unsigned woff[SITEMS];
+#pragma unroll
+    for (int j = 0; j < SITEMS; ++j) {  // warp-inclusive scan of the 0..2 live slots
+        unsigned c = ku[j] + kv[j], x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        woff[j] = x - c;
+        if (lane == 31) s_cnt[j * NW + wid] = x;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        static_assert(SITEMS * NW == 32, "scan below covers 32 entries");
+        unsigned v = s_cnt[lane], x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        s_cnt[lane] = x - v;
+        if (lane == 31) s_total = x;
+    }
+    __syncthreads();
+    const unsigned total = s_total;
+    unsigned long long prefix = tile_prefix(st, tile, (unsigned long long)total, &s_prefix);
+#pragma unroll
+    for (int j = 0; j < SITEMS; ++j) {
+        long long k = base + (long long)j * TB + threadIdx.x;
+        long long w = (long long)prefix + s_cnt[j * NW + wid] + woff[j];
+        if (ku[j]) {
+            keys[w] = (unsigned)e[j].x;
+            vals[w] = (unsigned)(2 * k);
+            ++w;
+        }
+        if (kv[j]) {
+            keys[w] = (unsigned)e[j].y;
+            vals[w] = (unsigned)(2 * k + 1);
+        }
+    }
+    if (threadIdx.x == 0 && tile == num_tiles - 1) *d_count = prefix + total;
+}
+
+template <class CT>
+__global__ void fill_kernel(CT *__restrict__ a, long long len, CT v) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+         i += (long long)gridDim.x * blockDim.x)
+        a[i] = v;
 }
 
 __global__ void seg_bounds_kernel(const unsigned *__restrict__ key, long long ns, unsigned n,
@@ -95,7 +167,7 @@ __global__ void slot_counter_kernel(const unsigned *__restrict__ key,
         }
         long long r = i - seg_start[x] + 1;
         long long d = d0 ? d0[x] : 0;
-        long long c = d > T ? d : min(d + r, T + 1);
+        long long c = min(d + r, T + 1);  // d <= T here (larger seeds were dropped)
         cval[s] = (CT)c;
     }
 }
@@ -184,31 +256,198 @@ __global__ void events_init_kernel(const int2 *__restrict__ E, long long m,
     }
 }
 
-// one pointer-jumping sweep; racy reads of origin/ptr are safe (monotone)
-__global__ void events_jump_kernel(const int *__restrict__ work, const unsigned *__restrict__ nin,
-                                   volatile int *origin, volatile int *ptr,
-                                   int *__restrict__ work_out, unsigned *__restrict__ nout) {
-    unsigned cnt = *nin;
-    unsigned cc = (cnt + 31) / 32 * 32;
-    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < cc; t += gridDim.x * blockDim.x) {
-        bool keep = false;
-        int k = -1;
-        if (t < cnt) {
-            k = work[t];
-            int p = ptr[k];
-            int op = origin[p];
-            if (op >= 0) {
-                origin[k] = op;
-            } else {
-                ptr[k] = ptr[p];
-                keep = true;
-            }
+// Pointer jumping runs as ONE cooperative launch instead of a launch + host
+// round trip per sweep: grid-wide sweeps separated by grid barriers while
+// the worklist is large, then block 0 alone (block barriers, ~100x cheaper
+// than a grid barrier) once it is at most SMALL_LIST long.  counts[r] =
+// worklist length before sweep r (counts[0] set by the init step, the rest
+// zeroed by the caller; R + 1 entries).
+constexpr unsigned SMALL_LIST = 2048;
+constexpr int CB = 512;  // cooperative-kernel block size
+
+// Worklist length after a barrier: one plain L2 load per warp (an atomic
+// read here would serialise every thread of the grid on one address).
+__device__ __forceinline__ unsigned ld_count(const unsigned *c) {
+    return *reinterpret_cast<const volatile unsigned *>(c);
+}
+
+__device__ __forceinline__ void push_compact(bool keep, int v, unsigned *counter, int *out) {
+    unsigned mask = __ballot_sync(0xffffffffu, keep);
+    unsigned b = 0;
+    if (lane_id() == 0 && mask) b = atomicAdd(counter, (unsigned)__popc(mask));
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (keep) out[b + __popc(mask & ((1u << lane_id()) - 1))] = v;
+}
+
+// event values: origin[k] = node whose initial label event k carries; a
+// pending event follows its parent chain (parents are earlier events, so
+// chains end and there are no cycles).
+__global__ void events_coop_kernel(int *__restrict__ wa, int *__restrict__ wb,
+                                   unsigned *__restrict__ counts, int R, int *origin, int *ptr) {
+    cg::grid_group grid = cg::this_grid();
+    int *cur = wa, *nxt = wb;
+    bool single = false;
+    for (int r = 0; r < R; ++r) {
+        const unsigned cnt = ld_count(counts + r);
+        if (cnt == 0) return;
+        if (!single && cnt <= SMALL_LIST) {
+            single = true;
+            if (blockIdx.x != 0) return;
         }
-        unsigned mask = __ballot_sync(0xffffffffu, keep);
-        unsigned base = 0;
-        if (lane_id() == 0 && mask) base = atomicAdd(nout, (unsigned)__popc(mask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (keep) work_out[base + __popc(mask & ((1u << lane_id()) - 1))] = k;
+        const unsigned start = single ? threadIdx.x : blockIdx.x * blockDim.x + threadIdx.x;
+        const unsigned stride = single ? blockDim.x : gridDim.x * blockDim.x;
+        const unsigned cc = (cnt + 31) / 32 * 32;
+        for (unsigned t = start; t < cc; t += stride) {
+            bool keep = false;
+            int k = -1;
+            if (t < cnt) {
+                k = cur[t];
+                int p = __ldcg(ptr + k);
+                int op = __ldcg(origin + p);
+                if (op >= 0) {
+                    origin[k] = op;
+                } else {
+                    ptr[k] = __ldcg(ptr + p);
+                    keep = true;
+                }
+            }
+            push_compact(keep, k, counts + r + 1, nxt);
+        }
+        if (single)
+            __syncthreads();
+        else
+            grid.sync();
+        int *tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+    }
+}
+
+// _resolve_labels (C/community.py:123-161): rep[x] = min id on the cycle
+// reached from x.  Terminals -- fixed points (rep = x) and 2-cycle members
+// (rep = min(x, f[x]); mutual adoptions make these common) -- are resolved
+// at init.  Every other node pointer-doubles (p[x] = p[p[x]]) until p[x]
+// lands on a node whose rep is already known (a terminal, or a node that
+// retired earlier: retiring publishes rep[x]).  While tree nodes remain,
+// every sweep retires at least one (the last remaining node on each path
+// points at a published node), so a sweep that retires nobody, once 2^r >=
+// remaining (every tail is shorter than that), leaves exactly the nodes that
+// lead into >= 3-cycles with p[x] on their cycle; min-doubling over that
+// f-closed set gives each cycle's minimum.  rep must start at -1.
+__global__ void resolve_coop_kernel(const long long *__restrict__ lab, long long n,
+                                    int *__restrict__ f, int *p, long long *rep,
+                                    int *__restrict__ wa, int *__restrict__ wb,
+                                    unsigned *__restrict__ counts, int R, int *__restrict__ mn_a,
+                                    int *__restrict__ q_a, int *__restrict__ mn_b,
+                                    int *__restrict__ q_b, int *__restrict__ bad) {
+    cg::grid_group grid = cg::this_grid();
+    const long long nn = (n + 31) / 32 * 32;
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < nn;
+         x += (long long)gridDim.x * blockDim.x) {
+        if (x < n) {
+            long long y = lab[x];
+            if (y < 0 || y >= n) {
+                atomicExch(bad, 1);
+                y = x;
+            }
+            f[x] = (int)y;
+            p[x] = (int)y;
+        }
+    }
+    grid.sync();
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < nn;
+         x += (long long)gridDim.x * blockDim.x) {
+        bool pend = false;
+        if (x < n) {
+            int y = f[x];
+            if (y == x)
+                rep[x] = x;
+            else if (f[y] == x)
+                rep[x] = min((long long)y, x);  // 2-cycle
+            else
+                pend = true;
+        }
+        push_compact(pend, (int)x, counts, wa);
+    }
+    grid.sync();
+    int *cur = wa, *nxt = wb;
+    bool single = false;
+    unsigned cnt = 0, prev = 0xffffffffu;
+    for (int r = 0;; ++r) {
+        cnt = ld_count(counts + r);
+        if (cnt == 0) return;
+        if (r == R || (cnt == prev && (r >= 31 || (1u << r) >= cnt))) break;
+        if (!single && cnt <= SMALL_LIST) {
+            single = true;
+            if (blockIdx.x != 0) return;
+        }
+        const unsigned start = single ? threadIdx.x : blockIdx.x * blockDim.x + threadIdx.x;
+        const unsigned stride = single ? blockDim.x : gridDim.x * blockDim.x;
+        const unsigned cc = (cnt + 31) / 32 * 32;
+        for (unsigned t = start; t < cc; t += stride) {
+            bool keep = false;
+            int x = -1;
+            if (t < cnt) {
+                x = cur[t];
+                int y = __ldcg(p + x);
+                long long ry = __ldcg(rep + y);
+                if (ry >= 0) {
+                    __stcg(rep + x, ry);  // retire + publish
+                } else {
+                    p[x] = __ldcg(p + y);
+                    keep = true;
+                }
+            }
+            push_compact(keep, x, counts + r + 1, nxt);
+        }
+        if (single)
+            __syncthreads();
+        else
+            grid.sync();
+        int *tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        prev = cnt;
+    }
+    // >= 3-cycles: min-doubling over cur[0..cnt)
+    if (!single && cnt <= SMALL_LIST) {
+        single = true;
+        if (blockIdx.x != 0) return;
+    }
+    const unsigned start = single ? threadIdx.x : blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned stride = single ? blockDim.x : gridDim.x * blockDim.x;
+    int K = 1;
+    while (K < 31 && (1u << (K + 1)) < cnt) ++K;  // window 2^(K+1) >= cnt >= cycle length
+    for (unsigned t = start; t < cnt; t += stride) {
+        int x = cur[t];
+        mn_a[x] = min(x, f[x]);
+        q_a[x] = f[f[x]];
+    }
+    if (single)
+        __syncthreads();
+    else
+        grid.sync();
+    for (int k = 0; k < K; ++k) {
+        for (unsigned t = start; t < cnt; t += stride) {
+            int x = cur[t];
+            int y = q_a[x];
+            mn_b[x] = min(mn_a[x], mn_a[y]);
+            q_b[x] = q_a[y];
+        }
+        if (single)
+            __syncthreads();
+        else
+            grid.sync();
+        int *t1 = mn_a;
+        mn_a = mn_b;
+        mn_b = t1;
+        int *t2 = q_a;
+        q_a = q_b;
+        q_b = t2;
+    }
+    for (unsigned t = start; t < cnt; t += stride) {
+        int x = cur[t];
+        rep[x] = mn_a[p[x]];
     }
 }
 
@@ -233,33 +472,84 @@ __global__ void det_finalize_kernel(long long n, const int *__restrict__ seg_sta
 
 // ---- fast (racy) pass ------------------------------------------------------
 
-__device__ __forceinline__ long long bump(unsigned *cnt, int x, long long d, long long T) {
-    if (d > T) return d;
-    long long room = T + 1 - d;  // increments that still matter
-    unsigned cur = *(volatile unsigned *)(cnt + x);
-    if ((long long)cur >= room) return T + 1;  // saturated: skip the atomic
-    unsigned old = atomicAdd(cnt + x, 1u);
-    return min(d + (long long)old + 1, T + 1);
-}
+// FU edges per thread in flight (grid-stride over the stream, W threads
+// => FU * W edges in flight): the next edges are prefetched, and for all FU
+// edges the counter checks, then the atomics, then the label loads are
+// issued back to back so their L2 round trips overlap.  A counter that
+// already reached T + 1 is not touched again (no atomic on saturated hubs).
+// Labels: racy last-writer-wins (SPEC "benign races").
+constexpr int FU = 2;
 
-__global__ void fast_pass_kernel(const int2 *__restrict__ E, long long m,
-                                 const long long *__restrict__ d0, long long T, int tie,
-                                 unsigned *__restrict__ cnt, volatile long long *lab) {
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
-         k += (long long)gridDim.x * blockDim.x) {
-        int2 p = __ldg(E + k);
-        long long du0 = d0 ? d0[p.x] : 0, dv0 = d0 ? d0[p.y] : 0;
-        if (p.x == p.y) {
-            bump(cnt, p.x, du0, T);
-            continue;
+__global__ void __launch_bounds__(TB) fast_pass_kernel(const int2 *__restrict__ E, long long m,
+                                                       const long long *__restrict__ d0,
+                                                       long long T, int tie,
+                                                       unsigned *__restrict__ cnt,
+                                                       long long *lab) {
+    const long long W = (long long)gridDim.x * blockDim.x;
+    const long long k0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    int2 nxt[FU];
+#pragma unroll
+    for (int u = 0; u < FU; ++u) {
+        long long k = k0 + u * W;
+        nxt[u] = k < m ? __ldcs(E + k) : make_int2(-1, -1);
+    }
+    for (long long kb = k0; kb < m; kb += FU * W) {
+        int2 p[FU];
+        long long du0[FU], dv0[FU];
+#pragma unroll
+        for (int u = 0; u < FU; ++u) {
+            p[u] = nxt[u];
+            long long kn = kb + (FU + u) * W;
+            nxt[u] = kn < m ? __ldcs(E + kn) : make_int2(-1, -1);
         }
-        long long du = bump(cnt, p.x, du0, T);
-        long long dv = bump(cnt, p.y, dv0, T);
-        if (du > T || dv > T) continue;
-        if (du < dv || (du == dv && tie == 0))
-            lab[p.x] = lab[p.y];
-        else if (dv < du || (du == dv && tie == 1))
-            lab[p.y] = lab[p.x];
+#pragma unroll
+        for (int u = 0; u < FU; ++u) {
+            const bool ok = p[u].x >= 0;
+            du0[u] = (d0 && ok) ? __ldg(d0 + p[u].x) : 0;
+            dv0[u] = (d0 && ok) ? __ldg(d0 + p[u].y) : 0;
+        }
+        bool nu[FU], nv[FU], au[FU], av[FU];
+        unsigned cu[FU], cv[FU], ou[FU], ov[FU];
+#pragma unroll
+        for (int u = 0; u < FU; ++u) {
+            const bool ok = p[u].x >= 0;
+            nu[u] = ok && du0[u] <= T;
+            nv[u] = ok && p[u].x != p[u].y && dv0[u] <= T;
+            cu[u] = nu[u] ? __ldcg(cnt + p[u].x) : 0u;
+            cv[u] = nv[u] ? __ldcg(cnt + p[u].y) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < FU; ++u) {
+            au[u] = nu[u] && (long long)cu[u] < T + 1 - du0[u];
+            av[u] = nv[u] && (long long)cv[u] < T + 1 - dv0[u];
+            ou[u] = au[u] ? atomicAdd(cnt + p[u].x, 1u) : 0u;
+            ov[u] = av[u] ? atomicAdd(cnt + p[u].y, 1u) : 0u;
+        }
+        int tgt[FU], src[FU];
+#pragma unroll
+        for (int u = 0; u < FU; ++u) {
+            tgt[u] = -1;
+            if (p[u].x < 0 || p[u].x == p[u].y) continue;
+            const long long du =
+                !nu[u] ? du0[u] : (au[u] ? min(du0[u] + (long long)ou[u] + 1, T + 1) : T + 1);
+            const long long dv =
+                !nv[u] ? dv0[u] : (av[u] ? min(dv0[u] + (long long)ov[u] + 1, T + 1) : T + 1);
+            if (du > T || dv > T) continue;  // C/community.py:110-111
+            if (du < dv || (du == dv && tie == 0)) {  // :112-113, :116-117
+                tgt[u] = p[u].x;
+                src[u] = p[u].y;
+            } else if (dv < du || (du == dv && tie == 1)) {  // :114-115, :118-119
+                tgt[u] = p[u].y;
+                src[u] = p[u].x;
+            }
+        }
+        long long val[FU];
+#pragma unroll
+        for (int u = 0; u < FU; ++u)
+            if (tgt[u] >= 0) val[u] = __ldcg(lab + src[u]);
+#pragma unroll
+        for (int u = 0; u < FU; ++u)
+            if (tgt[u] >= 0) __stcg(lab + tgt[u], val[u]);
     }
 }
 
@@ -281,92 +571,6 @@ __global__ void init_labels_kernel(long long n, const long long *__restrict__ la
 }
 
 // ---- resolve ---------------------------------------------------------------
-
-__global__ void resolve_init_kernel(const long long *__restrict__ lab, long long n,
-                                    int *__restrict__ f, int *__restrict__ p,
-                                    long long *__restrict__ rep, int *__restrict__ work,
-                                    unsigned *__restrict__ nwork, int *__restrict__ bad) {
-    long long nn = (n + 31) / 32 * 32;
-    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < nn;
-         x += (long long)gridDim.x * blockDim.x) {
-        bool pend = false;
-        if (x < n) {
-            long long y = lab[x];
-            if (y < 0 || y >= n) {
-                atomicExch(bad, 1);
-                y = x;
-            }
-            f[x] = (int)y;
-            p[x] = (int)y;
-            if (y == x)
-                rep[x] = x;
-            else
-                pend = true;
-        }
-        unsigned mask = __ballot_sync(0xffffffffu, pend);
-        unsigned base = 0;
-        if (lane_id() == 0 && mask) base = atomicAdd(nwork, (unsigned)__popc(mask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (pend) work[base + __popc(mask & ((1u << lane_id()) - 1))] = (int)x;
-    }
-}
-
-__global__ void resolve_jump_kernel(const int *__restrict__ work, const unsigned *__restrict__ nin,
-                                    const int *__restrict__ f, volatile int *p,
-                                    long long *__restrict__ rep, int *__restrict__ work_out,
-                                    unsigned *__restrict__ nout) {
-    unsigned cnt = *nin;
-    unsigned cc = (cnt + 31) / 32 * 32;
-    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < cc; t += gridDim.x * blockDim.x) {
-        bool keep = false;
-        int x = -1;
-        if (t < cnt) {
-            x = work[t];
-            int y = p[x];
-            if (f[y] == y) {
-                rep[x] = y;  // reached a fixed point
-            } else {
-                p[x] = p[y];
-                keep = true;
-            }
-        }
-        unsigned mask = __ballot_sync(0xffffffffu, keep);
-        unsigned base = 0;
-        if (lane_id() == 0 && mask) base = atomicAdd(nout, (unsigned)__popc(mask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (keep) work_out[base + __popc(mask & ((1u << lane_id()) - 1))] = x;
-    }
-}
-
-__global__ void cycle_min_init_kernel(const int *__restrict__ work, unsigned cnt,
-                                      const int *__restrict__ f, int *__restrict__ mn,
-                                      int *__restrict__ q) {
-    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
-        int x = work[t];
-        mn[x] = min(x, f[x]);
-        q[x] = f[f[x]];
-    }
-}
-
-__global__ void cycle_min_step_kernel(const int *__restrict__ work, unsigned cnt,
-                                      const int *__restrict__ mn_in, const int *__restrict__ q_in,
-                                      int *__restrict__ mn_out, int *__restrict__ q_out) {
-    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
-        int x = work[t];
-        int y = q_in[x];
-        mn_out[x] = min(mn_in[x], mn_in[y]);
-        q_out[x] = q_in[y];
-    }
-}
-
-__global__ void cycle_rep_kernel(const int *__restrict__ work, unsigned cnt,
-                                 const int *__restrict__ p, const int *__restrict__ mn,
-                                 long long *__restrict__ rep) {
-    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
-        int x = work[t];
-        rep[x] = mn[p[x]];
-    }
-}
 
 // ---- round driver helpers --------------------------------------------------
 
@@ -405,7 +609,7 @@ __global__ void compose_kernel(long long n, const long long *__restrict__ rep,
 }
 
 // stable relabel + drop-intra compaction (single pass, decoupled look-back)
-constexpr int RITEMS = 8;
+constexpr int RITEMS = 16;
 constexpr int RTILE = TB * RITEMS;
 
 __global__ void __launch_bounds__(TB) relabel_compact_kernel(
@@ -414,12 +618,10 @@ __global__ void __launch_bounds__(TB) relabel_compact_kernel(
     unsigned num_tiles) {
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_prefix;
-    __shared__ int s_warp[TB / 32];
     const unsigned tile = acquire_tile(st, &s_tile);
     const long long base = (long long)tile * RTILE;
     int2 e[RITEMS];
     bool keep[RITEMS];
-    int cnt = 0;
 #pragma unroll
     for (int j = 0; j < RITEMS; ++j) {
         long long i = base + (long long)j * TB + threadIdx.x;
@@ -429,19 +631,51 @@ __global__ void __launch_bounds__(TB) relabel_compact_kernel(
             int a = (int)__ldg(map + p.x), b = (int)__ldg(map + p.y);
             e[j] = make_int2(a, b);
             keep[j] = a != b;
-            cnt += keep[j];
         }
     }
-    int total;
-    block_exclusive_scan<TB>(cnt, s_warp, total);
-    unsigned long long prefix = tile_prefix(st, tile, (unsigned long long)total, &s_prefix);
-    long long run = 0;
+    // warp ballots -> per (item, warp) counts -> one 64-entry scan by warp 0:
+    // two block barriers per tile instead of one block scan per item
+    constexpr int NW = TB / 32;
+    __shared__ unsigned s_cnt[RITEMS * NW];
+    __shared__ unsigned s_total;
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    unsigned bal[RITEMS];
 #pragma unroll
     for (int j = 0; j < RITEMS; ++j) {
-        int tot_j;
-        int o = block_exclusive_scan<TB>(keep[j] ? 1 : 0, s_warp, tot_j);
-        if (keep[j]) out[prefix + run + o] = e[j];
-        run += tot_j;
+        bal[j] = __ballot_sync(0xffffffffu, keep[j]);
+        if (lane == 0) s_cnt[j * NW + wid] = __popc(bal[j]);
+    }
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan of the RITEMS * NW counts, PER consecutive per lane
+        constexpr int PER = RITEMS * NW / 32;
+        static_assert(PER * 32 == RITEMS * NW, "scan layout");
+        unsigned a[PER], v = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            a[q] = s_cnt[PER * lane + q];
+            v += a[q];
+        }
+        unsigned x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        unsigned run = x - v;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            s_cnt[PER * lane + q] = run;
+            run += a[q];
+        }
+        if (lane == 31) s_total = x;
+    }
+    __syncthreads();
+    const unsigned total = s_total;
+    unsigned long long prefix = tile_prefix(st, tile, (unsigned long long)total, &s_prefix);
+    const unsigned lt = (1u << lane) - 1;
+#pragma unroll
+    for (int j = 0; j < RITEMS; ++j) {
+        if (keep[j]) out[prefix + s_cnt[j * NW + wid] + __popc(bal[j] & lt)] = e[j];
     }
     if (threadIdx.x == 0 && tile == num_tiles - 1) *d_count = prefix + total;
 }
@@ -468,66 +702,87 @@ int bits_for_value(unsigned long long v) {  // bits to hold 0..v
 }  // namespace
 
 // Deterministic pass.  E: stream-ordered edges.  lab0/d0 nullable.
+// CT = per-slot counter type: u8 whenever T + 1 < 256 (the 2m-slot counter
+// array then stays L2-resident for the scattered writes), else int/int64.
 template <class CT>
 static void det_pass_t(const int2 *E, long long m, long long n, long long T, int tie,
                        const int64_t *d0, const int64_t *lab0, int64_t *deg_out,
                        int64_t *lab_out, Scratch &sc, cudaStream_t s) {
-    const long long ns = 2 * m;
+    const long long ns_all = 2 * m;
     auto *d0p = reinterpret_cast<const long long *>(d0);
-    auto *keys = sc.alloc<unsigned>(ns), *vals = sc.alloc<unsigned>(ns);
-    auto *skeys = sc.alloc<unsigned>(ns), *svals = sc.alloc<unsigned>(ns);
     int *seg_start = sc.alloc<int>(n), *seg_end = sc.alloc<int>(n), *finalw = sc.alloc<int>(n);
     CVZ_CUDA(cudaMemsetAsync(seg_start, 0xff, sizeof(int) * n, s));
     CVZ_CUDA(cudaMemsetAsync(finalw, 0xff, sizeof(int) * n, s));
     int *origin = nullptr;
     if (m > 0) {
-        CVZ_LAUNCH(slot_keys_kernel, grid_for(m, TB, 1, 16), TB, 0, s, E, m, d0p, T, (unsigned)n,
-                   reinterpret_cast<uint2 *>(keys), reinterpret_cast<uint2 *>(vals));
-        cub_sort_pairs(keys, skeys, vals, svals, ns, bits_for_value((unsigned long long)n), sc, s);
+        // 1. live slots in stream order (dead ones dropped, see slot_keys_kernel)
+        auto *keys = sc.alloc<unsigned>(ns_all), *vals = sc.alloc<unsigned>(ns_all);
+        unsigned tiles = (unsigned)((m + STILE - 1) / STILE);
+        auto *status = sc.alloc<unsigned long long>(tiles);
+        auto *ctr = sc.alloc<unsigned>(1);
+        auto *dcount = sc.alloc<unsigned long long>(1);
+        CVZ_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * tiles, s));
+        CVZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+        CVZ_LAUNCH(slot_keys_kernel, tiles, TB, 0, s, E, m, d0p, T, keys, vals,
+                   LookbackState{status, ctr}, dcount, tiles);
+        unsigned long long hns = 0;
+        CVZ_CUDA(cudaMemcpyAsync(&hns, dcount, sizeof(hns), cudaMemcpyDeviceToHost, s));
+        CVZ_CUDA(cudaStreamSynchronize(s));
+        const long long ns = (long long)hns;
+        // 2. stable sort by node: each node's slots in stream order
+        auto *skeys = sc.alloc<unsigned>(ns), *svals = sc.alloc<unsigned>(ns);
+        if (ns > 0)
+            cub_sort_pairs(keys, skeys, vals, svals, ns, bits_for_value((unsigned long long)n), sc,
+                           s);
         CVZ_LAUNCH(seg_bounds_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, ns, (unsigned)n,
                    seg_start, seg_end);
-        CT *cval = sc.alloc<CT>(ns);
+        // 3. post-increment counters (dead slots: T + 1)
+        CT *cval = sc.alloc<CT>(ns_all);
+        if (sizeof(CT) == 1)
+            CVZ_CUDA(cudaMemsetAsync(cval, (int)(T + 1), ns_all, s));
+        else
+            CVZ_LAUNCH(fill_kernel<CT>, grid_for(ns_all, TB, 1, 8), TB, 0, s, cval, ns_all,
+                       (CT)(T + 1));
         CVZ_LAUNCH(slot_counter_kernel<CT>, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, svals, ns,
                    (unsigned)n, seg_start, d0p, T, cval);
         auto *role = sc.alloc<signed char>(m);
         CVZ_LAUNCH(edge_role_kernel<CT>, grid_for(m, TB, 1, 16), TB, 0, s, E, m, cval, T, tie,
                    role);
-        // segmented "last write so far" over the node-sorted slots
+        // 4. segmented "last write so far" over the node-sorted slots
         int *lastw = sc.alloc<int>(ns);
-        WriteVal wv{skeys, svals, role, (unsigned)n};
-        auto vin = thrust::make_transform_iterator(thrust::counting_iterator<int>(0), wv);
-        size_t tb = 0;
-        CVZ_CUDA(cub::DeviceScan::InclusiveScanByKey(nullptr, tb, skeys, vin, lastw, MaxOp(),
-                                                     (int)ns, cub::Equality(), s));
-        void *tmp = sc.alloc<char>(tb);
-        {
+        if (ns > 0) {
+            WriteVal wv{skeys, svals, role, (unsigned)n};
+            auto vin = thrust::make_transform_iterator(thrust::counting_iterator<int>(0), wv);
+            size_t tb = 0;
+            CVZ_CUDA(cub::DeviceScan::InclusiveScanByKey(nullptr, tb, skeys, vin, lastw, MaxOp(),
+                                                         (int)ns, cub::Equality(), s));
+            void *tmp = sc.alloc<char>(tb);
             CVZ_REGION("cub_scan_by_key:scoda_lastw", s);
             CVZ_CUDA(cub::DeviceScan::InclusiveScanByKey(tmp, tb, skeys, vin, lastw, MaxOp(),
                                                          (int)ns, cub::Equality(), s));
+            count_launches(2);
         }
-        count_launches(2);
         int *parent = sc.alloc<int>(m);
         CVZ_LAUNCH(parents_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, svals, ns,
                    (unsigned)n, role, lastw, parent, finalw);
+        // 5. event values by pointer jumping (one cooperative launch)
         origin = sc.alloc<int>(m);
         int *ptr = sc.alloc<int>(m);
         int *wa = sc.alloc<int>(m), *wb = sc.alloc<int>(m);
-        unsigned *cnt = sc.alloc<unsigned>(2);
-        CVZ_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned), s));
+        const int R = bits_for_value((unsigned long long)m) + 2;
+        unsigned *cnt = sc.alloc<unsigned>(R + 1);
+        CVZ_CUDA(cudaMemsetAsync(cnt, 0, (R + 1) * sizeof(unsigned), s));
         CVZ_LAUNCH(events_init_kernel, grid_for(m, TB, 1, 16), TB, 0, s, E, m, role, parent,
                    origin, ptr, wa, cnt);
-        unsigned hc = 0;
-        CVZ_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
-        int cur = 0;
-        while (hc > 0) {
-            unsigned *cin = cnt + cur, *cout = cnt + (1 - cur);
-            CVZ_CUDA(cudaMemsetAsync(cout, 0, sizeof(unsigned), s));
-            CVZ_LAUNCH(events_jump_kernel, grid_for(hc, TB, 1, 16), TB, 0, s, cur ? wb : wa, cin,
-                       origin, ptr, cur ? wa : wb, cout);
-            CVZ_CUDA(cudaMemcpyAsync(&hc, cout, sizeof(hc), cudaMemcpyDeviceToHost, s));
+        CVZ_COOP(events_coop_kernel, CB, s, wa, wb, cnt, R, origin, ptr);
+        if (getenv("CVZ_DEBUG_RESOLVE")) {  // development aid: event worklist per sweep
+            std::vector<unsigned> h(R + 1);
+            CVZ_CUDA(cudaMemcpyAsync(h.data(), cnt, (R + 1) * sizeof(unsigned),
+                                     cudaMemcpyDeviceToHost, s));
             CVZ_CUDA(cudaStreamSynchronize(s));
-            cur = 1 - cur;
+            fprintf(stderr, "events m=%lld live slots=%lld counts:", m, ns);
+            for (unsigned v : h) fprintf(stderr, " %u", v);
+            fprintf(stderr, "\n");
         }
     }
     if (!origin) origin = sc.alloc<int>(1);
@@ -542,7 +797,9 @@ void scoda_pass_dev(const int2 *E, long long m, long long n, long long T, int ti
     CVZ_REQUIRE(2 * m < (1LL << 31) - 1, CVZ_ERR_VALUE,
                 "edge stream too long for one pass (2m must be < 2^31)");
     if (mode == CVZ_SCODA_DETERMINISTIC) {
-        if (T < (1LL << 30))
+        if (T < 255)
+            det_pass_t<unsigned char>(E, m, n, T, tie, d0, lab0, deg_out, lab_out, sc, s);
+        else if (T < (1LL << 30))
             det_pass_t<int>(E, m, n, T, tie, d0, lab0, deg_out, lab_out, sc, s);
         else
             det_pass_t<long long>(E, m, n, T, tie, d0, lab0, deg_out, lab_out, sc, s);
@@ -557,65 +814,49 @@ void scoda_pass_dev(const int2 *E, long long m, long long n, long long T, int ti
         // reference's own parallel schedules (C/community.py:164-195) only
         // while the edges in flight are a small fraction of the stream
         // (DESIGN.md "fast mode"); at C4 scale this is full occupancy anyway.
-        long long window = std::max(256LL, std::min(m / FAST_WINDOW_DIV, 2048LL * num_sms()));
-        unsigned blocks = (unsigned)((window + TB - 1) / TB);
+        long long window = std::max(256LL, std::min(m / FAST_WINDOW_DIV, 2048LL * num_sms() * FU));
+        unsigned blocks = (unsigned)((window / FU + TB - 1) / TB);
         CVZ_LAUNCH(fast_pass_kernel, blocks, TB, 0, s, E, m,
                    reinterpret_cast<const long long *>(d0), T, tie, cnt,
-                   reinterpret_cast<volatile long long *>(lab_out));
+                   reinterpret_cast<long long *>(lab_out));
     }
     CVZ_LAUNCH(fast_finalize_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n, cnt,
                reinterpret_cast<const long long *>(d0), T, reinterpret_cast<long long *>(deg_out));
 }
 
-// rep[x] = min id on the cycle reached from lab[x].  Returns false on range error
-// (only checked when check != 0; that synchronises).
+// rep[x] = min id on the cycle reached from lab[x] (C/community.py:123-161),
+// one cooperative launch.  The range check (labels in [0, n)) synchronises
+// only when check != 0.
 void resolve_dev(const int64_t *lab, long long n, int64_t *rep_out, bool check, Scratch &sc,
                  cudaStream_t s) {
     if (n <= 0) return;
     int *f = sc.alloc<int>(n), *p = sc.alloc<int>(n);
     int *wa = sc.alloc<int>(n), *wb = sc.alloc<int>(n);
-    unsigned *cnt = sc.alloc<unsigned>(2);
+    int *mn_a = sc.alloc<int>(n), *q_a = sc.alloc<int>(n);
+    int *mn_b = sc.alloc<int>(n), *q_b = sc.alloc<int>(n);
+    const int R = bits_for_value((unsigned long long)n) + 2;  // 2^R >= 2n
+    unsigned *cnt = sc.alloc<unsigned>(R + 1);
     int *bad = sc.alloc<int>(1);
-    CVZ_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned), s));
+    CVZ_CUDA(cudaMemsetAsync(cnt, 0, (R + 1) * sizeof(unsigned), s));
     CVZ_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
-    auto *rep = reinterpret_cast<long long *>(rep_out);
-    CVZ_LAUNCH(resolve_init_kernel, grid_for(n, TB, 1, 8), TB, 0, s,
-               reinterpret_cast<const long long *>(lab), n, f, p, rep, wa, cnt, bad);
-    unsigned hc[2] = {0, 0};
-    int hbad = 0;
-    CVZ_CUDA(cudaMemcpyAsync(&hc[0], cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-    if (check) CVZ_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CVZ_CUDA(cudaStreamSynchronize(s));
-    CVZ_REQUIRE(!hbad, CVZ_ERR_RANGE, "labels must lie in [0, n)");
-    unsigned c = hc[0];
-    int cur = 0;
-    int rounds = 0;
-    const int max_rounds = bits_for_value((unsigned long long)n) + 2;  // 2^rounds >= n
-    while (c > 0 && rounds < max_rounds) {
-        unsigned *cin = cnt + cur, *cout = cnt + (1 - cur);
-        CVZ_CUDA(cudaMemsetAsync(cout, 0, sizeof(unsigned), s));
-        CVZ_LAUNCH(resolve_jump_kernel, grid_for(c, TB, 1, 16), TB, 0, s, cur ? wb : wa, cin, f,
-                   p, rep, cur ? wa : wb, cout);
-        CVZ_CUDA(cudaMemcpyAsync(&c, cout, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    CVZ_CUDA(cudaMemsetAsync(rep_out, 0xff, sizeof(int64_t) * n, s));
+    CVZ_COOP(resolve_coop_kernel, CB, s, reinterpret_cast<const long long *>(lab), (long long)n,
+             f, p, reinterpret_cast<long long *>(rep_out), wa, wb, cnt, R, mn_a, q_a, mn_b, q_b,
+             bad);
+    if (getenv("CVZ_DEBUG_RESOLVE")) {  // development aid: worklist length per sweep
+        std::vector<unsigned> h(R + 1);
+        CVZ_CUDA(cudaMemcpyAsync(h.data(), cnt, (R + 1) * sizeof(unsigned),
+                                 cudaMemcpyDeviceToHost, s));
         CVZ_CUDA(cudaStreamSynchronize(s));
-        cur = 1 - cur;
-        ++rounds;
+        fprintf(stderr, "resolve n=%lld counts:", n);
+        for (unsigned v : h) fprintf(stderr, " %u", v);
+        fprintf(stderr, "\n");
     }
-    if (c > 0) {
-        // remaining nodes never reach a fixed point: p[x] is on a >=2 cycle and
-        // the remaining set is closed under f.  Min over each cycle by doubling.
-        int *work = cur ? wb : wa;
-        int *mn_a = sc.alloc<int>(n), *q_a = sc.alloc<int>(n);
-        int *mn_b = sc.alloc<int>(n), *q_b = sc.alloc<int>(n);
-        unsigned g = grid_for(c, TB, 1, 16);
-        CVZ_LAUNCH(cycle_min_init_kernel, g, TB, 0, s, work, c, f, mn_a, q_a);
-        // after init the window covers 2 nodes; double until >= n
-        for (int r = 1; r < max_rounds; ++r) {
-            CVZ_LAUNCH(cycle_min_step_kernel, g, TB, 0, s, work, c, mn_a, q_a, mn_b, q_b);
-            std::swap(mn_a, mn_b);
-            std::swap(q_a, q_b);
-        }
-        CVZ_LAUNCH(cycle_rep_kernel, g, TB, 0, s, work, c, p, mn_a, rep);
+    if (check) {
+        int hbad = 0;
+        CVZ_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CVZ_CUDA(cudaStreamSynchronize(s));
+        CVZ_REQUIRE(!hbad, CVZ_ERR_RANGE, "labels must lie in [0, n)");
     }
 }
 
@@ -696,7 +937,7 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
         // 4. compose + history + early-stop test (:266-269)
         int *dchg = sc.alloc<int>(1);
         CVZ_CUDA(cudaMemsetAsync(dchg, 0, sizeof(int), s));
-        CVZ_LAUNCH(compose_kernel, grid_for(n, TB, 1, 8), TB, 0, s, (long long)n,
+        CVZ_LAUNCH(compose_kernel, blocks_for(n, TB), TB, 0, s, (long long)n,
                    reinterpret_cast<const long long *>(rep), reinterpret_cast<long long *>(node_lab),
                    reinterpret_cast<long long *>(prev_lab),
                    reinterpret_cast<long long *>(history_out), round_index > 1 ? 1 : 0, dchg);
