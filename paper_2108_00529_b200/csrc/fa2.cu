@@ -26,6 +26,8 @@
 // block -> next bbox].  The whole iteration is captured once into a CUDA
 // graph and replayed `iterations` times; all scalars live on the device.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "common.cuh"
 
@@ -268,16 +270,100 @@ __global__ void karras_kernel(Keys K, int *__restrict__ left, int *__restrict__ 
     if (blockIdx.x == 0 && threadIdx.x == 0) pdelta[0] = -2;  // root
 }
 
-// bottom-up sums + cell classification + skip pointers
-__global__ void com_kernel(const Body *__restrict__ bodies, int n, const int *__restrict__ left,
-                           const int *__restrict__ first, const int *__restrict__ last,
-                           const int *__restrict__ delta, const int *__restrict__ parent_int,
-                           const int *__restrict__ parent_leaf, const int *__restrict__ pdelta,
-                           const int *__restrict__ rc_by_split, unsigned *__restrict__ visit,
-                           double *__restrict__ smass, double *__restrict__ sx,
-                           double *__restrict__ sy, const double *__restrict__ bbox,
-                           TNode *__restrict__ nodes, int2 *__restrict__ i12) {
+// ---- cell sums from double-double prefix sums ----------------------------------
+// Every radix-tree node covers a contiguous range [first, last] of the
+// key-sorted bodies, so its mass and moments are differences of prefix sums.
+// The prefixes are double-double (error-free TwoSum), so a difference is
+// exact to ~n * 2^-106 of the prefix magnitude -- as accurate as summing the
+// cell directly -- and every node is computed independently: no bottom-up
+// pass, no atomics, no depth-serial chain.
+struct DD {
+    double h, l;
+};
+struct DD3 {
+    DD m, x, y;
+};
+
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+    double s = __dadd_rn(a.h, b.h);
+    double bb = __dsub_rn(s, a.h);
+    double e = __dadd_rn(__dsub_rn(a.h, __dsub_rn(s, bb)), __dsub_rn(b.h, bb));
+    e = __dadd_rn(e, __dadd_rn(a.l, b.l));
+    double h = __dadd_rn(s, e);
+    return DD{h, __dsub_rn(e, __dsub_rn(h, s))};
+}
+
+__device__ __forceinline__ DD dd_neg(DD a) { return DD{-a.h, -a.l}; }
+
+struct DD3Add {
+    __device__ __forceinline__ DD3 operator()(const DD3 &a, const DD3 &b) const {
+        return DD3{dd_add(a.m, b.m), dd_add(a.x, b.x), dd_add(a.y, b.y)};
+    }
+};
+
+struct BodyMoments {  // body -> (m, m*x, m*y) as the reference forms them
+    const Body *b;
+    __device__ __forceinline__ DD3 operator()(int i) const {
+        Body q = b[i];
+        return DD3{DD{q.m, 0.0}, DD{mul(q.m, q.x), 0.0}, DD{mul(q.m, q.y), 0.0}};
+    }
+};
+
+__global__ void node_sums_kernel(int n, const DD3 *__restrict__ incl,
+                                 const int *__restrict__ left, const int *__restrict__ first,
+                                 const int *__restrict__ last, const int *__restrict__ delta,
+                                 const int *__restrict__ pdelta,
+                                 const int *__restrict__ rc_by_split,
+                                 const double *__restrict__ bbox, double *__restrict__ smass,
+                                 double *__restrict__ sx, double *__restrict__ sy,
+                                 TNode *__restrict__ nodes) {
     Geo g = root_geo(bbox);
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < n - 1;
+         node += gridDim.x * blockDim.x) {
+        const int f0 = first[node], l0 = last[node];
+        DD3 hi = incl[l0];
+        double mm, xx, yy;
+        if (f0 == 0) {
+            mm = hi.m.h;
+            xx = hi.x.h;
+            yy = hi.y.h;
+        } else {
+            DD3 lo = incl[f0 - 1];
+            DD a = dd_add(hi.m, dd_neg(lo.m)), b = dd_add(hi.x, dd_neg(lo.x)),
+               c = dd_add(hi.y, dd_neg(lo.y));
+            mm = __dadd_rn(a.h, a.l);
+            xx = __dadd_rn(b.h, b.l);
+            yy = __dadd_rn(c.h, c.l);
+        }
+        smass[node] = mm;
+        sx[node] = xx;
+        sy[node] = yy;
+        int dl = delta[node], pd = pdelta[node];
+        int kind;
+        if (dl >= 80)
+            kind = (pd < 80) ? 2 : 0;  // depth-40 aggregate top (identical keys)
+        else
+            kind = (node == 0 || (pd >> 1) < (dl >> 1)) ? 1 : 0;  // topmost of its level
+        double side = 2.0 * ldexp(g.half, -(dl >> 1));  // exact halvings
+        TNode t;
+        t.comx = xx / mm;
+        t.comy = yy / mm;
+        t.mass = mm;
+        t.side2 = mul(side, side);
+        t.left = left[node];
+        t.skip = (l0 == n - 1) ? END : rc_by_split[l0];
+        t.kind = kind;
+        t.pad = 0;
+        nodes[node] = t;
+    }
+}
+
+// two smallest original body ids per node (reference cell numbering only)
+__global__ void i12_kernel(const Body *__restrict__ bodies, int n, const int *__restrict__ left,
+                           const int *__restrict__ last, const int *__restrict__ parent_int,
+                           const int *__restrict__ parent_leaf,
+                           const int *__restrict__ rc_by_split, unsigned *__restrict__ visit,
+                           int2 *__restrict__ i12) {
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
         int node = parent_leaf[p];
         while (node >= 0) {
@@ -285,62 +371,11 @@ __global__ void com_kernel(const Body *__restrict__ bodies, int n, const int *__
             if (atomicAdd(visit + node, 1u) == 0) break;  // first arrival stops
             __threadfence();
             int l = left[node];
-            int r = (l >= 0) ? -1 : 0;  // placeholder, computed below
-            (void)r;
-            // children: left = l; right = rc_by_split[split] -- recover split:
-            // left child covers [first, gamma]: gamma = (l >= 0 ? last[l] : ~l)
             int gamma = l >= 0 ? last[l] : ~l;
             int rc = rc_by_split[gamma];
-            double m0, x0, y0, m1, x1, y1;
-            if (l >= 0) {
-                m0 = ((volatile double *)smass)[l];
-                x0 = ((volatile double *)sx)[l];
-                y0 = ((volatile double *)sy)[l];
-            } else {
-                Body b = bodies[~l];
-                m0 = b.m;
-                x0 = mul(b.m, b.x);
-                y0 = mul(b.m, b.y);
-            }
-            if (rc >= 0) {
-                m1 = ((volatile double *)smass)[rc];
-                x1 = ((volatile double *)sx)[rc];
-                y1 = ((volatile double *)sy)[rc];
-            } else {
-                Body b = bodies[~rc];
-                m1 = b.m;
-                x1 = mul(b.m, b.x);
-                y1 = mul(b.m, b.y);
-            }
-            if (i12) {  // two smallest original body ids of the subtree
-                int2 a = l >= 0 ? __ldcg(i12 + l) : make_int2(bodies[~l].orig, INT_MAX);
-                int2 b = rc >= 0 ? __ldcg(i12 + rc) : make_int2(bodies[~rc].orig, INT_MAX);
-                i12[node] = a.x < b.x ? make_int2(a.x, min(a.y, b.x)) : make_int2(b.x, min(b.y, a.x));
-            }
-            double mm = add(m0, m1), xx = add(x0, x1), yy = add(y0, y1);
-            smass[node] = mm;
-            sx[node] = xx;
-            sy[node] = yy;
-            int dl = delta[node], pd = pdelta[node];
-            int kind;
-            if (dl >= 80)
-                kind = (pd < 80) ? 2 : 0;  // aggregate top (or never visited)
-            else
-                kind = (node == 0 || (pd >> 1) < (dl >> 1)) ? 1 : 0;
-            int lvl = dl >> 1;
-            double chalf = ldexp(g.half, -lvl);  // exact halvings
-            double side = 2.0 * chalf;
-            TNode t;
-            t.comx = xx / mm;
-            t.comy = yy / mm;
-            t.mass = mm;
-            t.side2 = mul(side, side);
-            t.left = l;
-            int lst = last[node];
-            t.skip = (lst == n - 1) ? END : rc_by_split[lst];
-            t.kind = kind;
-            t.pad = 0;
-            nodes[node] = t;
+            int2 a = l >= 0 ? __ldcg(i12 + l) : make_int2(bodies[~l].orig, INT_MAX);
+            int2 b = rc >= 0 ? __ldcg(i12 + rc) : make_int2(bodies[~rc].orig, INT_MAX);
+            i12[node] = a.x < b.x ? make_int2(a.x, min(a.y, b.x)) : make_int2(b.x, min(b.y, a.x));
             node = (node == 0) ? -1 : parent_int[node];
         }
     }
@@ -1054,6 +1089,9 @@ struct Tree {
     unsigned *visit;
     double *smass, *sx, *sy;
     TNode *nodes;
+    DD3 *prefix;
+    void *ptmp = nullptr;
+    size_t ptmp_bytes = 0;
     int2 *i12;
     FNode *fn;
     double *bbox = nullptr;
@@ -1073,6 +1111,14 @@ struct Tree {
         n = n_;
         scr = &sc;
         i12 = sc.alloc<int2>(n > 1 ? n - 1 : 1);
+        prefix = sc.alloc<DD3>(n);
+        {
+            auto it = thrust::make_transform_iterator(thrust::counting_iterator<int>(0),
+                                                      BodyMoments{nullptr});
+            CVZ_CUDA(cub::DeviceScan::InclusiveScan(nullptr, ptmp_bytes, it, prefix, DD3Add(), n,
+                                                    sc.stream()));
+            ptmp = sc.alloc<char>(ptmp_bytes);
+        }
         fn = sc.alloc<FNode>(2 * n - 1);
         jflag = sc.alloc<unsigned>(1);
         CVZ_CUDA(cudaMemsetAsync(jflag, 0, sizeof(unsigned), sc.stream()));
@@ -1124,12 +1170,19 @@ struct Tree {
         count_launches(9);
         CVZ_LAUNCH(gather_bodies_kernel, g, FB, 0, s, pos, mass, idx3, klo, (long long)n, bodies,
                    klo3);
-        CVZ_CUDA(cudaMemsetAsync(visit, 0, sizeof(unsigned) * (n - 1), s));
         Keys K{khi3, klo3, n};
         CVZ_LAUNCH(karras_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, K, left, first, last, delta,
                    parent_int, parent_leaf, pdelta, rc_by_split);
-        CVZ_LAUNCH(com_kernel, g, FB, 0, s, bodies, n, left, first, last, delta, parent_int,
-                   parent_leaf, pdelta, rc_by_split, visit, smass, sx, sy, bbox, nodes, i12);
+        {
+            CVZ_REGION("cub_scan:dd_moments", s);
+            auto it = thrust::make_transform_iterator(thrust::counting_iterator<int>(0),
+                                                      BodyMoments{bodies});
+            size_t tb = ptmp_bytes;
+            CVZ_CUDA(cub::DeviceScan::InclusiveScan(ptmp, tb, it, prefix, DD3Add(), n, s));
+            count_launches(2);
+        }
+        CVZ_LAUNCH(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix, left, first,
+                   last, delta, pdelta, rc_by_split, bbox, smass, sx, sy, nodes);
         if (flat())
             CVZ_LAUNCH(flatten_kernel, grid_for(2LL * n, FB, 1, 8), FB, 0, s, n, nodes, left,
                        rc_by_split, bodies, fn);
@@ -1152,6 +1205,9 @@ struct Tree {
             CVZ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, etmp_scan, ecnt2, eexcl, ne, s));
             etmp = scr->alloc<char>(std::max(etmp_sort, etmp_scan));
         }
+        CVZ_CUDA(cudaMemsetAsync(visit, 0, sizeof(unsigned) * (n - 1), s));
+        CVZ_LAUNCH(i12_kernel, grid_for(n, FB, 1, 8), FB, 0, s, bodies, n, left, last, parent_int,
+                   parent_leaf, rc_by_split, visit, i12);
         unsigned g = grid_for(ne, FB, 1, 8);
         CVZ_LAUNCH(cell_entries_kernel, g, FB, 0, s, bodies, n, nodes, delta, pdelta, parent_int,
                    parent_leaf, i12, ekey, eslot, ecnt);

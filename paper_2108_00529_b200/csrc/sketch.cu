@@ -97,7 +97,7 @@ __global__ void add_direct_kernel(unsigned long long *__restrict__ table,
     }
 }
 
-__global__ void add_staged_kernel(unsigned long long *__restrict__ table,
+__global__ void add_staged_kernel(unsigned long long *__restrict__ partial,
                                   const long long *__restrict__ ha,
                                   const long long *__restrict__ hb, int rows, unsigned cols,
                                   const long long *__restrict__ keys,
@@ -125,8 +125,21 @@ __global__ void add_staged_kernel(unsigned long long *__restrict__ table,
         }
     }
     __syncthreads();
-    for (unsigned i = threadIdx.x; i < cells; i += blockDim.x)
-        if (sh[i]) atomicAdd(table + i, sh[i]);
+    // plain coalesced store of this CTA's partial table; reduce_partials sums
+    // them (no global atomics on a 26K-cell table from every CTA)
+    unsigned long long *mine = partial + (size_t)blockIdx.x * cells;
+    for (unsigned i = threadIdx.x; i < cells; i += blockDim.x) mine[i] = sh[i];
+}
+
+__global__ void reduce_partials_kernel(unsigned long long *__restrict__ table,
+                                       const unsigned long long *__restrict__ partial,
+                                       unsigned nparts, unsigned cells) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cells;
+         i += gridDim.x * blockDim.x) {
+        unsigned long long acc = table[i];  // u64 wrap-around == numpy int64 add.at
+        for (unsigned p = 0; p < nparts; ++p) acc += partial[(size_t)p * cells + i];
+        table[i] = acc;
+    }
 }
 
 __global__ void saturate_kernel(long long *__restrict__ table, long long cells,
@@ -180,11 +193,16 @@ void sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *ha, const
                                               (int)STAGED_MAX_BYTES));
                 attr = true;
             }
-            // enough CTAs to fill the chip once; each flushes <= rows*cols cells
-            long long want = k / (8LL * rows * cols) + 1;
+            // one CTA per SM (the table fills its shared memory); each writes
+            // a partial table, one pass sums them into the sketch
+            long long want = k / (2LL * rows * cols) + 1;
             unsigned grid = (unsigned)std::min<long long>(want, num_sms());
-            CVZ_LAUNCH(add_staged_kernel, grid, 1024, bytes, s, t, pa, pb, rows, (unsigned)cols,
-                       kk, aa, (long long)k);
+            Scratch sc(s);
+            auto *partial = sc.alloc<unsigned long long>((size_t)grid * rows * cols);
+            CVZ_LAUNCH(add_staged_kernel, grid, 1024, bytes, s, partial, pa, pb, rows,
+                       (unsigned)cols, kk, aa, (long long)k);
+            CVZ_LAUNCH(reduce_partials_kernel, grid_for((long long)rows * cols, 256, 1, 4), 256,
+                       0, s, t, partial, grid, (unsigned)(rows * cols));
         } else {
             CVZ_LAUNCH(add_direct_kernel, grid_for(k, 256, 1, 8), 256, 0, s, t, pa, pb, rows,
                        (unsigned)cols, kk, aa, (long long)k);
