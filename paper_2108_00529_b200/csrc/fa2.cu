@@ -664,7 +664,8 @@ __global__ void flatten_kernel(int n, const TNode *__restrict__ nodes,
     }
 }
 
-__global__ void __launch_bounds__(FB) bh_flat_kernel(const Body *__restrict__ bodies, int n,
+template <int MINB>
+__global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(const Body *__restrict__ bodies, int n,
                                                      const FNode *__restrict__ fn,
                                                      const int *__restrict__ first,
                                                      const int *__restrict__ last,
@@ -1230,9 +1231,19 @@ struct Tree {
     void repulse(double kr, double theta, double2 *out, const long long *bad, bool ids,
                  cudaStream_t s) {
         CellRef cr{delta, pdelta, ids ? idslot : nullptr, jflag, bbox};
-        if (flat())
-            CVZ_LAUNCH(bh_flat_kernel, blocks_for(n, FB), FB, 0, s, bodies, n, fn, first, last,
-                       smass, sx, sy, kr, theta, out, bad, cr);
+        if (flat()) {
+            static const int minb = getenv("CVZ_BH_MINB") ? atoi(getenv("CVZ_BH_MINB")) : 5;
+#define CVZ_BH_FLAT(B)                                                                     \
+    CVZ_LAUNCH(bh_flat_kernel<B>, blocks_for(n, FB), FB, 0, s, bodies, n, fn, first, last, \
+               smass, sx, sy, kr, theta, out, bad, cr)
+            if (minb >= 6)
+                CVZ_BH_FLAT(6);
+            else if (minb == 5)
+                CVZ_BH_FLAT(5);
+            else
+                CVZ_BH_FLAT(4);
+#undef CVZ_BH_FLAT
+        }
         else
             CVZ_LAUNCH(bh_kernel, blocks_for(n, FB), FB, 0, s, bodies, n, nodes, rc_by_split,
                        first, last, smass, sx, sy, kr, theta, out, bad, cr);
