@@ -195,6 +195,16 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                    double *prev_force, double *speed, double *disp_hist,
                    int64_t *bad_iteration, void *stream);
 
+/* ------------------------------------------------------------------ rng */
+
+/* numpy Generator(PCG64).uniform(low, low + range, count) on the device,
+ * bit-exact: out[i] = low + range * ((next_u64 >> 11) * 2^-53), the i-th
+ * draw of the generator whose 128-bit state/increment are given (take them
+ * from numpy: default_rng(seed).bit_generator.state).  Replaces the host
+ * draw of C/layout.py:78-82 init_positions.  out [dev] f64[count]. */
+int cvz_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                      double low, double range, int64_t count, double *out, void *stream);
+
 /* -------------------------------------------------------------- metrics */
 
 /* C/metrics.py:34-46 modularity ingredients: intra[c] and degsum[c] over

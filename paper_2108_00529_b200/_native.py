@@ -63,6 +63,8 @@ SIGNATURES = {
     "cvz_attraction": [_P, _I64, _P, _I64, _P, _D, _P, _P],
     "cvz_layout_run": [_P, _P, _I64, _P, _I64, _P, ctypes.POINTER(_LayoutParams),
                        _P, _P, _P, ctypes.POINTER(_I64), _P],
+    "cvz_pcg64_uniform": [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                          _D, _D, _I64, _P, _P],
     "cvz_modularity_parts": [_P, _I64, _P, _P, _I64, _I64, _P, _P, _P],
 }
 

@@ -70,6 +70,22 @@ def init_positions(n: int, seed: int = 0) -> np.ndarray:
     return np.random.default_rng(seed).uniform(-side / 2, side / 2, size=(n, 2))
 
 
+def _init_positions_dev(n: int, seed: int = 0):
+    """init_positions drawn on the GPU (cvz_pcg64_uniform): numpy's PCG64
+    stream seeded by numpy on the host, bit-identical values, no host loop
+    or (n, 2) upload."""
+    T = nat.torch()
+    side = max(np.sqrt(n), 1.0)
+    low, high = -side / 2, side / 2
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m64 = (1 << 64) - 1
+    out = T.empty((n, 2), dtype=T.float64, device=nat.device())
+    nat.call("cvz_pcg64_uniform", s >> 64, s & m64, inc >> 64, inc & m64, low, high - low,
+             2 * n, nat.ptr(out), nat.stream())
+    return out
+
+
 def _f64(x):
     T = nat.torch()
     if isinstance(x, T.Tensor):
@@ -142,19 +158,18 @@ def layout(obj, params: LayoutParams | None = None, positions=None) -> LayoutRes
         params = LayoutParams()
     T = nat.torch()
     n = obj.node_count
-    if positions is None:
-        pos = init_positions(n, params.seed)
-    else:
+    if positions is not None:
         pos = np.array(positions, dtype=np.float64)
         if pos.shape != (n, 2):
             raise ValueError("positions must be an (n, 2) array")
     if n == 1:
+        pos = init_positions(n, params.seed) if positions is None else pos
         return LayoutResult(positions=pos, displacement=np.zeros(params.iterations),
                             iterations=params.iterations)
     if n == 0:
         raise ValueError("layout needs at least one node")
     mass, e, ew = _device_model(obj)
-    pos_d = nat.to_dev(pos, T.float64)
+    pos_d = _init_positions_dev(n, params.seed) if positions is None else nat.to_dev(pos, T.float64)
     prev = T.zeros_like(pos_d)
     speed = T.ones(1, dtype=T.float64, device=nat.device())
     hist = T.zeros(params.iterations, dtype=T.float64, device=nat.device())

@@ -512,3 +512,12 @@ def test_full_graph_layout_matches_oracle(cv, orc):
     pos, disp = orc.layout(g.node_count, mass, g.edges, ew, iterations=10, seed=2)
     diam = np.hypot(*(pos.max(0) - pos.min(0)))
     assert np.max(np.abs(res.positions - pos)) <= 1e-7 * diam
+
+
+# ------------------------------------------------------------------- rng
+@pytest.mark.parametrize("n,seed", [(1, 0), (7, 3), (1000, 0), (318813, 0), (100003, 12345)])
+def test_device_init_positions_bit_exact(cv, orc, n, seed):
+    """numpy PCG64 uniform stream reproduced on the GPU (C/layout.py:78-82)."""
+    from paper_2108_00529_b200.layout import _init_positions_dev
+    dev = _init_positions_dev(n, seed).cpu().numpy()
+    assert np.array_equal(dev, orc.init_positions(n, seed))
