@@ -295,21 +295,112 @@ __device__ __forceinline__ DD dd_add(DD a, DD b) {
 
 __device__ __forceinline__ DD dd_neg(DD a) { return DD{-a.h, -a.l}; }
 
-struct DD3Add {
-    __device__ __forceinline__ DD3 operator()(const DD3 &a, const DD3 &b) const {
-        return DD3{dd_add(a.m, b.m), dd_add(a.x, b.x), dd_add(a.y, b.y)};
-    }
-};
+// Two-level double-double prefix: tile-local inclusive prefixes (TILE_DD
+// bodies per CTA, 8 per thread) + one small scan of the tile totals.
+constexpr int DD_ITEMS = 2;
+constexpr int TILE_DD = FB * DD_ITEMS;
 
-struct BodyMoments {  // body -> (m, m*x, m*y) as the reference forms them
-    const Body *b;
-    __device__ __forceinline__ DD3 operator()(int i) const {
-        Body q = b[i];
-        return DD3{DD{q.m, 0.0}, DD{mul(q.m, q.x), 0.0}, DD{mul(q.m, q.y), 0.0}};
-    }
-};
+__device__ __forceinline__ DD dd_shfl_up(DD v, int o) {
+    return DD{__shfl_up_sync(0xffffffffu, v.h, o), __shfl_up_sync(0xffffffffu, v.l, o)};
+}
 
-__global__ void node_sums_kernel(int n, const DD3 *__restrict__ incl,
+__device__ __forceinline__ DD3 dd3_add(const DD3 &a, const DD3 &b) {
+    return DD3{dd_add(a.m, b.m), dd_add(a.x, b.x), dd_add(a.y, b.y)};
+}
+
+// block-wide inclusive scan of one DD3 per thread
+__device__ DD3 block_scan_dd3(DD3 v, DD3 *warp_tot, DD3 &block_total) {
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    DD3 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        DD3 y{dd_shfl_up(x.m, o), dd_shfl_up(x.x, o), dd_shfl_up(x.y, o)};
+        if (lane >= o) x = dd3_add(y, x);
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    DD3 before{{0, 0}, {0, 0}, {0, 0}};
+    DD3 tot{{0, 0}, {0, 0}, {0, 0}};
+    for (int w = 0; w < FB / 32; ++w) {
+        if (w < wid) before = dd3_add(before, warp_tot[w]);
+        tot = dd3_add(tot, warp_tot[w]);
+    }
+    block_total = tot;
+    return wid ? dd3_add(before, x) : x;
+}
+
+__global__ void __launch_bounds__(FB) dd_tile_scan_kernel(const Body *__restrict__ bodies, int n,
+                                                          DD3 *__restrict__ local,
+                                                          DD3 *__restrict__ tile_tot) {
+    __shared__ DD3 warp_tot[FB / 32];
+    const long long base = (long long)blockIdx.x * TILE_DD + (long long)threadIdx.x * DD_ITEMS;
+    DD3 acc{{0, 0}, {0, 0}, {0, 0}};
+    DD3 item[DD_ITEMS];
+#pragma unroll
+    for (int j = 0; j < DD_ITEMS; ++j) {
+        long long i = base + j;
+        DD3 v{{0, 0}, {0, 0}, {0, 0}};
+        if (i < n) {
+            Body q = bodies[i];
+            v = DD3{DD{q.m, 0.0}, DD{mul(q.m, q.x), 0.0}, DD{mul(q.m, q.y), 0.0}};
+        }
+        acc = dd3_add(acc, v);
+        item[j] = acc;
+    }
+    DD3 total;
+    DD3 incl = block_scan_dd3(acc, warp_tot, total);
+    DD3 excl{{0, 0}, {0, 0}, {0, 0}};
+    // exclusive prefix of this thread = incl - acc, formed as a sum to stay exact
+    {
+        const int lane = lane_id(), wid = threadIdx.x >> 5;
+        DD3 up{dd_shfl_up(incl.m, 1), dd_shfl_up(incl.x, 1), dd_shfl_up(incl.y, 1)};
+        if (lane > 0) {
+            excl = up;
+        } else if (wid > 0) {
+            for (int w = 0; w < wid; ++w) excl = dd3_add(excl, warp_tot[w]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < DD_ITEMS; ++j) {
+        long long i = base + j;
+        if (i < n) local[i] = dd3_add(excl, item[j]);
+    }
+    if (threadIdx.x == 0) tile_tot[blockIdx.x] = total;
+}
+
+// exclusive scan of the tile totals, one CTA
+__global__ void __launch_bounds__(FB) dd_tiles_kernel(DD3 *__restrict__ tile_tot, int tiles) {
+    __shared__ DD3 warp_tot[FB / 32];
+    DD3 carry{{0, 0}, {0, 0}, {0, 0}};
+    for (int t0 = 0; t0 < tiles; t0 += FB) {
+        int t = t0 + threadIdx.x;
+        DD3 v = t < tiles ? tile_tot[t] : DD3{{0, 0}, {0, 0}, {0, 0}};
+        DD3 total;
+        DD3 incl = block_scan_dd3(v, warp_tot, total);
+        __syncthreads();
+        // exclusive = carry + (incl - v): recompute as carry + exclusive sum
+        DD3 excl{{0, 0}, {0, 0}, {0, 0}};
+        const int lane = lane_id(), wid = threadIdx.x >> 5;
+        DD3 up{dd_shfl_up(incl.m, 1), dd_shfl_up(incl.x, 1), dd_shfl_up(incl.y, 1)};
+        if (lane > 0) {
+            excl = up;
+        } else if (wid > 0) {
+            for (int w = 0; w < wid; ++w) excl = dd3_add(excl, warp_tot[w]);
+        }
+        __syncthreads();
+        if (t < tiles) tile_tot[t] = dd3_add(carry, excl);
+        carry = dd3_add(carry, total);
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ DD3 dd_prefix_at(const DD3 *__restrict__ local,
+                                            const DD3 *__restrict__ tile_off, int i) {
+    return dd3_add(tile_off[i / TILE_DD], local[i]);
+}
+
+__global__ void node_sums_kernel(int n, const DD3 *__restrict__ local,
+                                 const DD3 *__restrict__ tile_off,
                                  const int *__restrict__ left, const int *__restrict__ first,
                                  const int *__restrict__ last, const int *__restrict__ delta,
                                  const int *__restrict__ pdelta,
@@ -321,14 +412,14 @@ __global__ void node_sums_kernel(int n, const DD3 *__restrict__ incl,
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < n - 1;
          node += gridDim.x * blockDim.x) {
         const int f0 = first[node], l0 = last[node];
-        DD3 hi = incl[l0];
+        DD3 hi = dd_prefix_at(local, tile_off, l0);
         double mm, xx, yy;
         if (f0 == 0) {
             mm = hi.m.h;
             xx = hi.x.h;
             yy = hi.y.h;
         } else {
-            DD3 lo = incl[f0 - 1];
+            DD3 lo = dd_prefix_at(local, tile_off, f0 - 1);
             DD a = dd_add(hi.m, dd_neg(lo.m)), b = dd_add(hi.x, dd_neg(lo.x)),
                c = dd_add(hi.y, dd_neg(lo.y));
             mm = __dadd_rn(a.h, a.l);
@@ -1090,9 +1181,7 @@ struct Tree {
     unsigned *visit;
     double *smass, *sx, *sy;
     TNode *nodes;
-    DD3 *prefix;
-    void *ptmp = nullptr;
-    size_t ptmp_bytes = 0;
+    DD3 *prefix, *tile_tot;
     int2 *i12;
     FNode *fn;
     double *bbox = nullptr;
@@ -1113,13 +1202,7 @@ struct Tree {
         scr = &sc;
         i12 = sc.alloc<int2>(n > 1 ? n - 1 : 1);
         prefix = sc.alloc<DD3>(n);
-        {
-            auto it = thrust::make_transform_iterator(thrust::counting_iterator<int>(0),
-                                                      BodyMoments{nullptr});
-            CVZ_CUDA(cub::DeviceScan::InclusiveScan(nullptr, ptmp_bytes, it, prefix, DD3Add(), n,
-                                                    sc.stream()));
-            ptmp = sc.alloc<char>(ptmp_bytes);
-        }
+        tile_tot = sc.alloc<DD3>((n + TILE_DD - 1) / TILE_DD);
         fn = sc.alloc<FNode>(2 * n - 1);
         jflag = sc.alloc<unsigned>(1);
         CVZ_CUDA(cudaMemsetAsync(jflag, 0, sizeof(unsigned), sc.stream()));
@@ -1174,15 +1257,11 @@ struct Tree {
         Keys K{khi3, klo3, n};
         CVZ_LAUNCH(karras_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, K, left, first, last, delta,
                    parent_int, parent_leaf, pdelta, rc_by_split);
-        {
-            CVZ_REGION("cub_scan:dd_moments", s);
-            auto it = thrust::make_transform_iterator(thrust::counting_iterator<int>(0),
-                                                      BodyMoments{bodies});
-            size_t tb = ptmp_bytes;
-            CVZ_CUDA(cub::DeviceScan::InclusiveScan(ptmp, tb, it, prefix, DD3Add(), n, s));
-            count_launches(2);
-        }
-        CVZ_LAUNCH(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix, left, first,
+        const int tiles = (n + TILE_DD - 1) / TILE_DD;
+        CVZ_LAUNCH(dd_tile_scan_kernel, tiles, FB, 0, s, bodies, n, prefix, tile_tot);
+        CVZ_LAUNCH(dd_tiles_kernel, 1, FB, 0, s, tile_tot, tiles);
+        CVZ_LAUNCH(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix, tile_tot,
+                   left, first,
                    last, delta, pdelta, rc_by_split, bbox, smass, sx, sy, nodes);
         if (flat())
             CVZ_LAUNCH(flatten_kernel, grid_for(2LL * n, FB, 1, 8), FB, 0, s, n, nodes, left,
