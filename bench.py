@@ -179,6 +179,11 @@ def kernel_bytes(name, st):
         # per body: Body (x, y, m, id) 32 B read + force 16 B write;
         # per tree node: TNode 48 B read once
         "bh_kernel": k * (32 + 16) + (k - 1) * 48,
+        # flat walk: per body 32 B read + 16 B force write; flat node array of
+        # k leaves + <= k-1 cells, FNode 48 B each, read once
+        "bh_flat_kernel<4>": k * (32 + 16) + (2 * k - 1) * 48,
+        "bh_flat_kernel<5>": k * (32 + 16) + (2 * k - 1) * 48,
+        "bh_flat_kernel<6>": k * (32 + 16) + (2 * k - 1) * 48,
         # pos 16 + repulsion 16 + mass 8 + prev 16 + rowptr 8 + force 16 + swing 8
         # per node; col 4 + weight 8 per half-edge
         "forces_kernel": k * 88 + 2 * se * 12,

@@ -135,6 +135,24 @@ int cvz_sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *hash_a
                    const int64_t *hash_b, const int64_t *keys, const int64_t *amounts,
                    int64_t k, int validate, int32_t *d_saturated, void *stream);
 
+/* Sharded sketch building.  accumulate: delta[r, idx_r(key_j)]
+ * += amount_j with u64 wrap-around and NO saturation (a rank-local delta
+ * table, to be summed across ranks).  accumulate_edges: the edge-based form
+ * of C/supergraph.py:42-46 -- +1 under labels[u] and +1 under labels[v] for
+ * every edge (u, v) of edges [dev] int32[m*2]; labels [dev] int64[n].
+ * merge: table += delta (wrap), then the C/sketch.py:80-86 saturation;
+ * *d_saturated [dev] int32 set to 1 if a cell wrapped.  Since the adds are
+ * integer additions mod 2^64, shard + all-reduce(SUM) + merge gives exactly
+ * the single-process table. */
+int cvz_sketch_accumulate(int64_t *delta, int rows, int64_t cols, const int64_t *hash_a,
+                          const int64_t *hash_b, const int64_t *keys, const int64_t *amounts,
+                          int64_t k, void *stream);
+int cvz_sketch_accumulate_edges(int64_t *delta, int rows, int64_t cols, const int64_t *hash_a,
+                                const int64_t *hash_b, const int32_t *edges, int64_t m,
+                                const int64_t *labels, void *stream);
+int cvz_sketch_merge(int64_t *table, const int64_t *delta, int rows, int64_t cols,
+                     int32_t *d_saturated, void *stream);
+
 /* C/sketch.py:93-98 sketch_estimate_many: out[j] = min_r table[r, idx_r]. */
 int cvz_sketch_estimate(const int64_t *table, int rows, int64_t cols,
                         const int64_t *hash_a, const int64_t *hash_b,
@@ -194,6 +212,35 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                    int64_t m, const double *weight, const cvz_layout_params *params,
                    double *prev_force, double *speed, double *disp_hist,
                    int64_t *bad_iteration, void *stream);
+
+/* Node-sharded layout (one rank per GPU).  The single-process
+ * loop C/layout.py:363-398 split at its two reductions.  Every rank keeps
+ * ALL positions (pos [dev] f64[n*2], identical on every rank at the start of
+ * an iteration), builds the full tree, and owns original node ids [lo, hi):
+ * it computes their repulsion / springs / gravity / swing and moves only
+ * them.  Per iteration the caller runs
+ *     cvz_fa2_shard_forces(h, pos, sums)     sums [dev] f64[2] rank-local
+ *     all-reduce(sums, SUM)                   -> Σswing, Σtraction
+ *     cvz_fa2_shard_update(h, pos, sums, red) red [dev] f64[6] rank-local
+ *     all-reduce(red, MAX)                    {-minx,maxx,-miny,maxy,maxdisp,bad}
+ *     all-gather(pos rows [lo,hi))
+ *     cvz_fa2_shard_absorb(h, red, disp_hist) next bbox, disp_hist[it], bad
+ * then cvz_fa2_shard_finish (SYNCHRONISES).  Nothing synchronises inside the
+ * loop.  ref_cell_ids = 1 numbers cells like the reference for coincident-
+ * cell jitter (C/layout.py:258); run with 0 first and rerun with 1 when any
+ * rank's finish reports *jitter_seen.  create SYNCHRONISES (CSR build). */
+typedef struct cvz_fa2_shard cvz_fa2_shard;
+int cvz_fa2_shard_create(const double *pos, const double *mass, int64_t n, const int32_t *edges,
+                         int64_t m, const double *weight, const cvz_layout_params *params,
+                         int64_t lo, int64_t hi, int ref_cell_ids, cvz_fa2_shard **out,
+                         void *stream);
+int cvz_fa2_shard_forces(cvz_fa2_shard *h, const double *pos, double *sums_out, void *stream);
+int cvz_fa2_shard_update(cvz_fa2_shard *h, double *pos, const double *sums, double *red_out,
+                         void *stream);
+int cvz_fa2_shard_absorb(cvz_fa2_shard *h, const double *red, double *disp_hist, void *stream);
+int cvz_fa2_shard_finish(cvz_fa2_shard *h, double *speed_out, int64_t *bad_iteration,
+                         int *jitter_seen, void *stream);
+int cvz_fa2_shard_destroy(cvz_fa2_shard *h, void *stream);
 
 /* ------------------------------------------------------------------ rng */
 

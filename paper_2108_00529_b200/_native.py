@@ -66,6 +66,17 @@ SIGNATURES = {
     "cvz_pcg64_uniform": [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                           _D, _D, _I64, _P, _P],
     "cvz_modularity_parts": [_P, _I64, _P, _P, _I64, _I64, _P, _P, _P],
+    "cvz_sketch_accumulate": [_P, _I32, _I64, _P, _P, _P, _P, _I64, _P],
+    "cvz_sketch_accumulate_edges": [_P, _I32, _I64, _P, _P, _P, _I64, _P, _P],
+    "cvz_sketch_merge": [_P, _P, _I32, _I64, _P, _P],
+    "cvz_fa2_shard_create": [_P, _P, _I64, _P, _I64, _P, ctypes.POINTER(_LayoutParams),
+                             _I64, _I64, _I32, ctypes.POINTER(ctypes.c_void_p), _P],
+    "cvz_fa2_shard_forces": [_P, _P, _P, _P],
+    "cvz_fa2_shard_update": [_P, _P, _P, _P, _P],
+    "cvz_fa2_shard_absorb": [_P, _P, _P, _P],
+    "cvz_fa2_shard_finish": [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64),
+                             ctypes.POINTER(ctypes.c_int), _P],
+    "cvz_fa2_shard_destroy": [_P, _P],
 }
 
 _lib = None

@@ -765,10 +765,16 @@ __global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(const Body *__restric
                                                      const double *__restrict__ sy, double kr,
                                                      double theta, double2 *__restrict__ out,
                                                      const long long *__restrict__ bad,
-                                                     CellRef cr) {
+                                                     CellRef cr, const int *__restrict__ work,
+                                                     const int *__restrict__ nwork) {
     if (bad && *bad) return;
     const double th2 = mul(theta, theta);
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    // work == nullptr: every body; else the sorted bodies this rank owns
+    // (node-sharded layout), still in key order
+    const int count = work ? *nwork : n;
+    for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < count;
+         t0 += gridDim.x * blockDim.x) {
+        const int p = work ? work[t0] : t0;
         Body me = bodies[p];
         const long long i = me.orig;
         const double xi = me.x, yi = me.y, mi = me.m;
@@ -840,11 +846,12 @@ __global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(const Body *__restric
 constexpr int XT = 256;
 __global__ void __launch_bounds__(XT) exact_kernel(const double2 *__restrict__ pos,
                                                    const double *__restrict__ mass, int n,
-                                                   double kr, double2 *__restrict__ out) {
+                                                   double kr, double2 *__restrict__ out,
+                                                   int lo, int hi) {
     __shared__ double3 tile[XT];
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int i = lo + blockIdx.x * blockDim.x + threadIdx.x;  // rows [lo, hi), columns all n
     double xi = 0, yi = 0, mi = 0;
-    if (i < n) {
+    if (i < hi) {
         double2 p = pos[i];
         xi = p.x;
         yi = p.y;
@@ -859,7 +866,7 @@ __global__ void __launch_bounds__(XT) exact_kernel(const double2 *__restrict__ p
         }
         __syncthreads();
         int lim = min(XT, n - j0);
-        if (i < n) {
+        if (i < hi) {
             for (int t = 0; t < lim; ++t) {
                 int jj = j0 + t;
                 if (jj == i) continue;
@@ -873,7 +880,7 @@ __global__ void __launch_bounds__(XT) exact_kernel(const double2 *__restrict__ p
         }
         __syncthreads();
     }
-    if (i < n) out[i] = make_double2(fx, fy);
+    if (i < hi) out[i] = make_double2(fx, fy);
 }
 
 // ---- CSR for attraction ------------------------------------------------------
@@ -920,10 +927,11 @@ struct StepScalars {
 // the warp waiting on the power-law tail.  C/layout.py:293-304.
 constexpr int HEAVY = 32;
 
-__global__ void classify_rows_kernel(const long long *__restrict__ rowptr, int n,
+__global__ void classify_rows_kernel(const long long *__restrict__ rowptr, int lo, int n,
                                      int *__restrict__ hidx, int *__restrict__ heavy,
                                      unsigned *__restrict__ nheavy) {
-    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    for (int u = lo + blockIdx.x * blockDim.x + threadIdx.x; u < n;
+         u += gridDim.x * blockDim.x) {
         int h = -1;
         if (rowptr[u + 1] - rowptr[u] > HEAVY) {
             h = (int)atomicAdd(nheavy, 1u);
@@ -965,10 +973,10 @@ __global__ void __launch_bounds__(FB) forces_kernel(
     const double2 *__restrict__ hsum, const double2 *__restrict__ frep, double gravity,
     const double2 *__restrict__ prev, double2 *__restrict__ force, double *__restrict__ swing,
     double *__restrict__ part, unsigned *__restrict__ ctr, StepScalars *__restrict__ sc,
-    double jt) {
+    double jt, int lo, double *__restrict__ sums_out) {
     if (sc->bad) return;
     double s_sw = 0.0, s_tr = 0.0;
-    int u = blockIdx.x * blockDim.x + threadIdx.x;
+    int u = lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (u < n) {
         double2 pu = pos[u];
         double2 f = frep[u];
@@ -1038,6 +1046,12 @@ __global__ void __launch_bounds__(FB) forces_kernel(
         }
         __syncthreads();
     }
+    if (threadIdx.x == 0 && sums_out) {  // node-sharded: rank-local sums
+        sums_out[0] = a[0];
+        sums_out[1] = b[0];
+        *ctr = 0;
+        return;
+    }
     if (threadIdx.x == 0) {
         double tsw = a[0], ttr = b[0];
         sc->sum_swing = tsw;
@@ -1054,10 +1068,11 @@ __global__ void __launch_bounds__(FB) update_kernel(
     double2 *__restrict__ pos, int n, const double2 *__restrict__ force,
     const double *__restrict__ swing, double2 *__restrict__ prev, int speed_form,
     double max_step, double *__restrict__ bpart, unsigned *__restrict__ ctr,
-    double *__restrict__ bbox, StepScalars *__restrict__ sc, double *__restrict__ disp_hist) {
+    double *__restrict__ bbox, StepScalars *__restrict__ sc, double *__restrict__ disp_hist,
+    int lo, double *__restrict__ red_out) {
     if (sc->bad) return;
     const double speed = sc->speed;
-    int u = blockIdx.x * blockDim.x + threadIdx.x;
+    int u = lo + blockIdx.x * blockDim.x + threadIdx.x;
     double nrm = 0.0;
     bool fin = true;
     double a = INFINITY, b = -INFINITY, c = INFINITY, d = -INFINITY;
@@ -1148,6 +1163,16 @@ __global__ void __launch_bounds__(FB) update_kernel(
     }
     if (threadIdx.x != 0) return;
     md = sm[0];
+    if (red_out) {  // node-sharded: the all-reduce (MAX) finishes the reduction
+        red_out[0] = -s0[0];
+        red_out[1] = s1[0];
+        red_out[2] = -s2[0];
+        red_out[3] = s3[0];
+        red_out[4] = md;
+        red_out[5] = bad ? 1.0 : 0.0;
+        *ctr = 0;
+        return;
+    }
     bbox[0] = s0[0];
     bbox[1] = s1[0];
     bbox[2] = s2[0];
@@ -1267,7 +1292,8 @@ struct Tree {
             CVZ_LAUNCH(flatten_kernel, grid_for(2LL * n, FB, 1, 8), FB, 0, s, n, nodes, left,
                        rc_by_split, bodies, fn);
     }
-    bool flat() const { return getenv("CVZ_BH_BINARY") == nullptr; }
+    bool force_flat = false;  // node-sharded runs always walk the flat tree
+    bool flat() const { return force_flat || getenv("CVZ_BH_BINARY") == nullptr; }
     // reference cell numbering of the current tree (see cell_entries_kernel)
     void build_ids(cudaStream_t s) {
         if (!idslot) {
@@ -1307,14 +1333,15 @@ struct Tree {
         }
         CVZ_LAUNCH(scatter_ids_kernel, g, FB, 0, s, eslot2, eexcl, ne, idslot);
     }
+    // work/nwork: optional list of owned sorted bodies (node-sharded layout)
     void repulse(double kr, double theta, double2 *out, const long long *bad, bool ids,
-                 cudaStream_t s) {
+                 cudaStream_t s, const int *work = nullptr, const int *nwork = nullptr) {
         CellRef cr{delta, pdelta, ids ? idslot : nullptr, jflag, bbox};
         if (flat()) {
             static const int minb = getenv("CVZ_BH_MINB") ? atoi(getenv("CVZ_BH_MINB")) : 5;
 #define CVZ_BH_FLAT(B)                                                                     \
     CVZ_LAUNCH(bh_flat_kernel<B>, blocks_for(n, FB), FB, 0, s, bodies, n, fn, first, last, \
-               smass, sx, sy, kr, theta, out, bad, cr)
+               smass, sx, sy, kr, theta, out, bad, cr, work, nwork)
             if (minb >= 6)
                 CVZ_BH_FLAT(6);
             else if (minb == 5)
@@ -1355,7 +1382,8 @@ void repulsion_dev(const double *pos, const double *mass, long long n, double kr
         return;
     }
     if (theta <= 0) {
-        CVZ_LAUNCH(exact_kernel, blocks_for(n, XT), XT, 0, s, p2, mass, (int)n, kr, o2);
+        CVZ_LAUNCH(exact_kernel, blocks_for(n, XT), XT, 0, s, p2, mass, (int)n, kr, o2, 0,
+                   (int)n);
         return;
     }
     double *bbox = sc.alloc<double>(4);
@@ -1380,8 +1408,11 @@ struct Csr {
     double2 *hsum;  // [nheavy] warp-summed springs
 };
 
+// Heavy rows are classified over [row_lo, row_hi) only (a node-sharded rank
+// sums the springs of the rows it owns); row_hi < 0 means all n.
 static Csr build_csr(const int2 *e, long long m, long long n, const double *weight, double sign,
-                     Scratch &sc, cudaStream_t s) {
+                     Scratch &sc, cudaStream_t s, long long row_lo = 0, long long row_hi = -1) {
+    if (row_hi < 0) row_hi = n;
     Csr c;
     long long nh = 2 * m;
     c.rowptr = sc.alloc<long long>(n + 1);
@@ -1418,8 +1449,8 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
     c.heavy = sc.alloc<int>(n);
     unsigned *nh_d = sc.alloc<unsigned>(1);
     CVZ_CUDA(cudaMemsetAsync(nh_d, 0, sizeof(unsigned), s));
-    CVZ_LAUNCH(classify_rows_kernel, grid_for(n, FB, 1, 8), FB, 0, s, c.rowptr, (int)n, c.hidx,
-               c.heavy, nh_d);
+    CVZ_LAUNCH(classify_rows_kernel, grid_for(row_hi - row_lo, FB, 1, 8), FB, 0, s, c.rowptr,
+               (int)row_lo, (int)row_hi, c.hidx, c.heavy, nh_d);
     unsigned nh_h = 0;
     CVZ_CUDA(cudaMemcpyAsync(&nh_h, nh_d, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     CVZ_CUDA(cudaStreamSynchronize(s));
@@ -1452,11 +1483,205 @@ __global__ void attraction_only_kernel(const double2 *__restrict__ pos, int n,
     }
 }
 
+// ---- node-sharded layout -----------------------------------
+// Every rank holds all positions (all-gathered each iteration) and builds the
+// full tree; it computes repulsion, springs, gravity and swing for the nodes
+// [lo, hi) it owns and updates only those.  The cross-rank steps are two
+// small all-reduces the caller runs between the calls below: Σswing/Σtraction
+// (SUM, 2 doubles) before the speed update, and {-minx, maxx, -miny, maxy,
+// maxdisp, bad} (MAX, 6 doubles) after it -- then an all-gather of the owned
+// position rows.  C/layout.py:363-398 is the single-process loop this splits.
+struct OwnedBody {
+    const Body *bodies;
+    int lo, hi;
+    __device__ __forceinline__ bool operator()(int p) const {
+        int o = bodies[p].orig;
+        return o >= lo && o < hi;
+    }
+};
+
+__global__ void shard_speed_kernel(const double *__restrict__ sums, StepScalars *__restrict__ sc,
+                                   double jt) {
+    if (sc->bad) return;
+    double tsw = sums[0], ttr = sums[1];
+    sc->sum_swing = tsw;
+    sc->sum_traction = ttr;
+    if (tsw > 0) {  // C/layout.py:379-382
+        double target = mul(jt, ttr) / tsw;
+        sc->speed = fmin(target, 1.5 * sc->speed);
+    }
+}
+
+__global__ void shard_absorb_kernel(const double *__restrict__ red, double *__restrict__ bbox,
+                                    StepScalars *__restrict__ sc, double *__restrict__ disp_hist) {
+    if (sc->bad) return;
+    long long it = sc->it;
+    if (disp_hist) disp_hist[it] = red[4];
+    if (red[5] > 0) sc->bad = it + 1;  // C/layout.py:395-397 (1-based)
+    sc->it = it + 1;
+    bbox[0] = -red[0];
+    bbox[1] = red[1];
+    bbox[2] = -red[2];
+    bbox[3] = red[3];
+}
+
 }  // namespace cvz
+
+struct cvz_fa2_shard {
+    cvz::Scratch *sc = nullptr;
+    int n = 0, lo = 0, hi = 0;
+    cvz_layout_params P{};
+    bool exact = false, ids = false;
+    const double *mass = nullptr;
+    cvz::Csr csr;
+    cvz::Tree tree;
+    double2 *frep = nullptr, *force = nullptr, *prev = nullptr;
+    double *swing = nullptr, *fpart = nullptr, *upart = nullptr, *bbox = nullptr;
+    unsigned *ctrs = nullptr;
+    cvz::StepScalars *scal = nullptr;
+    int *work = nullptr, *nwork = nullptr;
+    void *sel_tmp = nullptr;
+    size_t sel_bytes = 0;
+    unsigned nb = 1;
+};
 
 using namespace cvz;
 
 extern "C" {
+
+int cvz_fa2_shard_create(const double *pos, const double *mass, int64_t n, const int32_t *edges,
+                         int64_t m, const double *weight, const cvz_layout_params *P, int64_t lo,
+                         int64_t hi, int ref_cell_ids, cvz_fa2_shard **out, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(n >= 2 && n < (1LL << 30), CVZ_ERR_VALUE, "layout needs 2 <= n < 2^30");
+        CVZ_REQUIRE(0 <= lo && lo <= hi && hi <= n, CVZ_ERR_VALUE, "bad owned node range");
+        cudaStream_t s = as_stream(stream);
+        auto *h = new cvz_fa2_shard();
+        try {
+            h->sc = new Scratch(s);
+            Scratch &sc = *h->sc;
+            h->n = (int)n;
+            h->lo = (int)lo;
+            h->hi = (int)hi;
+            h->P = *P;
+            h->mass = mass;
+            h->exact = P->theta <= 0;
+            h->ids = ref_cell_ids != 0;
+            double sign = P->attraction_form == 0 ? 1.0 : -1.0;
+            h->csr = build_csr(reinterpret_cast<const int2 *>(edges), m, n, weight, sign, sc, s,
+                               lo, hi);
+            h->frep = sc.alloc<double2>(n);
+            h->force = sc.alloc<double2>(n);
+            h->prev = sc.alloc<double2>(n);
+            CVZ_CUDA(cudaMemsetAsync(h->prev, 0, sizeof(double2) * n, s));  // C/layout.py:363
+            h->swing = sc.alloc<double>(n);
+            h->nb = blocks_for(hi - lo, FB);
+            h->fpart = sc.alloc<double>(2 * h->nb);
+            h->upart = sc.alloc<double>(5 * h->nb);
+            h->ctrs = sc.alloc<unsigned>(2);
+            CVZ_CUDA(cudaMemsetAsync(h->ctrs, 0, 2 * sizeof(unsigned), s));
+            h->bbox = sc.alloc<double>(4);
+            h->scal = sc.alloc<StepScalars>(1);
+            StepScalars init{};
+            init.speed = 1.0;  // C/layout.py:364
+            CVZ_CUDA(cudaMemcpyAsync(h->scal, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+            bbox_dev(reinterpret_cast<const double2 *>(pos), (int)n, h->bbox, sc, s);
+            if (!h->exact) {
+                h->tree.alloc((int)n, sc);
+                h->tree.force_flat = true;
+                h->work = sc.alloc<int>(hi > lo ? hi - lo : 1);
+                h->nwork = sc.alloc<int>(1);
+                CVZ_CUDA(cub::DeviceSelect::If(nullptr, h->sel_bytes,
+                                               thrust::counting_iterator<int>(0), h->work,
+                                               h->nwork, (int)n, OwnedBody{nullptr, 0, 0}, s));
+                h->sel_tmp = sc.alloc<char>(h->sel_bytes);
+            }
+            CVZ_CUDA(cudaStreamSynchronize(s));  // init copy source is a host local
+        } catch (...) {
+            delete h->sc;
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int cvz_fa2_shard_forces(cvz_fa2_shard *h, const double *pos, double *sums_out, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(h != nullptr, CVZ_ERR_VALUE, "null shard handle");
+        cudaStream_t s = as_stream(stream);
+        auto *p2 = reinterpret_cast<const double2 *>(pos);
+        const cvz_layout_params &P = h->P;
+        long long *badp = &h->scal->bad;
+        if (h->exact) {
+            CVZ_LAUNCH(exact_kernel, blocks_for(h->hi - h->lo, XT), XT, 0, s, p2, h->mass, h->n,
+                       P.repulsion, h->frep, h->lo, h->hi);
+        } else {
+            h->tree.build(p2, h->mass, h->bbox, s);
+            if (h->ids) h->tree.build_ids(s);
+            {
+                CVZ_REGION("cub_select:owned_bodies", s);
+                size_t tb = h->sel_bytes;
+                CVZ_CUDA(cub::DeviceSelect::If(h->sel_tmp, tb, thrust::counting_iterator<int>(0),
+                                               h->work, h->nwork, h->n,
+                                               OwnedBody{h->tree.bodies, h->lo, h->hi}, s));
+                count_launches(2);
+            }
+            h->tree.repulse(P.repulsion, P.theta, h->frep, badp, h->ids, s, h->work, h->nwork);
+        }
+        springs_heavy(p2, h->csr, h->scal, s);
+        CVZ_LAUNCH(forces_kernel, h->nb, FB, 0, s, p2, h->mass, h->hi, h->csr.rowptr, h->csr.col,
+                   h->csr.w, h->csr.hidx, h->csr.hsum, h->frep, P.gravity, h->prev, h->force,
+                   h->swing, h->fpart, h->ctrs, h->scal, P.jitter_tolerance, h->lo, sums_out);
+    });
+}
+
+int cvz_fa2_shard_update(cvz_fa2_shard *h, double *pos, const double *sums, double *red_out,
+                         void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(h != nullptr, CVZ_ERR_VALUE, "null shard handle");
+        cudaStream_t s = as_stream(stream);
+        CVZ_LAUNCH(shard_speed_kernel, 1, 1, 0, s, sums, h->scal, h->P.jitter_tolerance);
+        CVZ_LAUNCH(update_kernel, h->nb, FB, 0, s, reinterpret_cast<double2 *>(pos), h->hi,
+                   h->force, h->swing, h->prev, h->P.speed_form, h->P.max_step, h->upart,
+                   h->ctrs + 1, h->bbox, h->scal, nullptr, h->lo, red_out);
+    });
+}
+
+int cvz_fa2_shard_absorb(cvz_fa2_shard *h, const double *red, double *disp_hist, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(h != nullptr, CVZ_ERR_VALUE, "null shard handle");
+        CVZ_LAUNCH(shard_absorb_kernel, 1, 1, 0, as_stream(stream), red, h->bbox, h->scal,
+                   disp_hist);
+    });
+}
+
+int cvz_fa2_shard_finish(cvz_fa2_shard *h, double *speed_out, int64_t *bad_iteration,
+                         int *jitter_seen, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(h != nullptr, CVZ_ERR_VALUE, "null shard handle");
+        cudaStream_t s = as_stream(stream);
+        StepScalars out;
+        unsigned jf = 0;
+        CVZ_CUDA(cudaMemcpyAsync(&out, h->scal, sizeof(out), cudaMemcpyDeviceToHost, s));
+        if (!h->exact)
+            CVZ_CUDA(cudaMemcpyAsync(&jf, h->tree.jflag, sizeof(jf), cudaMemcpyDeviceToHost, s));
+        CVZ_CUDA(cudaStreamSynchronize(s));
+        if (speed_out) *speed_out = out.speed;
+        *bad_iteration = out.bad;
+        *jitter_seen = jf != 0;
+    });
+}
+
+int cvz_fa2_shard_destroy(cvz_fa2_shard *h, void *stream) {
+    return guard([&] {
+        if (!h) return;
+        (void)stream;
+        delete h->sc;  // stream-ordered frees on the creation stream
+        delete h;
+    });
+}
+
 
 int cvz_repulsion(const double *pos, const double *mass, int64_t n, double repulsion,
                   double theta, double *out, void *stream) {
@@ -1518,7 +1743,7 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
         auto one_iteration = [&](cudaStream_t st, bool ids) {
             if (exact) {
                 CVZ_LAUNCH(exact_kernel, blocks_for(n, XT), XT, 0, st, p2, mass, N, P->repulsion,
-                           frep);
+                           frep, 0, N);
             } else {
                 tree.build(p2, mass, bbox, st);
                 if (ids) tree.build_ids(st);
@@ -1527,9 +1752,10 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
             springs_heavy(p2, csr, scal, st);
             CVZ_LAUNCH(forces_kernel, nb, FB, 0, st, p2, mass, N, csr.rowptr, csr.col, csr.w,
                        csr.hidx, csr.hsum, frep,
-                       P->gravity, prev, force, swing, fpart, ctrs, scal, P->jitter_tolerance);
+                       P->gravity, prev, force, swing, fpart, ctrs, scal, P->jitter_tolerance, 0,
+                       nullptr);
             CVZ_LAUNCH(update_kernel, nb, FB, 0, st, p2, N, force, swing, prev, P->speed_form,
-                       P->max_step, upart, ctrs + 1, bbox, scal, disp_hist);
+                       P->max_step, upart, ctrs + 1, bbox, scal, disp_hist, 0, nullptr);
         };
 
         auto run_all = [&](bool ids) {

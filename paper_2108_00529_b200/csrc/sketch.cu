@@ -79,17 +79,19 @@ __device__ __forceinline__ void agg_add(unsigned long long *base, unsigned cell,
     if (lane_id() == leader) atomicAdd(base + cell, sum);
 }
 
+template <class Src>
 __global__ void add_direct_kernel(unsigned long long *__restrict__ table,
                                   const long long *__restrict__ ha,
                                   const long long *__restrict__ hb, int rows, unsigned cols,
-                                  const long long *__restrict__ keys,
-                                  const long long *__restrict__ amounts, long long k) {
+                                  Src src, long long k) {
     long long stride = (long long)gridDim.x * blockDim.x;
     long long kk = (k + 31) / 32 * 32;  // whole warps iterate together
     for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < kk; j += stride) {
         bool valid = j < k;
-        unsigned long long xm = valid ? key_mod_p(keys[j]) : 0;
-        unsigned long long amt = valid ? (unsigned long long)amounts[j] : 0;
+        long long key = 0;
+        unsigned long long amt = 0;
+        if (valid) src.get(j, key, amt);
+        unsigned long long xm = valid ? key_mod_p(key) : 0;
         for (int r = 0; r < rows; ++r) {
             unsigned c = valid ? hash_col(ha[r], hb[r], xm, cols) : 0;
             agg_add<false>(table + (size_t)r * cols, c, amt, valid && amt != 0);
@@ -97,11 +99,33 @@ __global__ void add_direct_kernel(unsigned long long *__restrict__ table,
     }
 }
 
+// Key sources for the staged add: explicit (key, amount) arrays
+// (sketch_add_many) or the endpoint slots of an edge list, key = label of the
+// endpoint, amount 1 (the edge-based form of accumulate_sizes, SURVEY.md a17:
+// identical counters to the node-based form because it is integer addition).
+struct KeyAmounts {
+    const long long *keys, *amounts;
+    __device__ __forceinline__ void get(long long j, long long &key,
+                                        unsigned long long &amt) const {
+        key = keys[j];
+        amt = (unsigned long long)amounts[j];
+    }
+};
+struct EdgeLabels {
+    const int *ep;  // int32 endpoints, 2 per edge
+    const long long *labels;
+    __device__ __forceinline__ void get(long long j, long long &key,
+                                        unsigned long long &amt) const {
+        key = labels[ep[j]];
+        amt = 1;
+    }
+};
+
+template <class Src>
 __global__ void add_staged_kernel(unsigned long long *__restrict__ partial,
                                   const long long *__restrict__ ha,
                                   const long long *__restrict__ hb, int rows, unsigned cols,
-                                  const long long *__restrict__ keys,
-                                  const long long *__restrict__ amounts, long long k) {
+                                  Src src, long long k) {
     extern __shared__ unsigned long long sh[];
     const unsigned cells = rows * cols;
     for (unsigned i = threadIdx.x; i < cells; i += blockDim.x) sh[i] = 0;
@@ -117,8 +141,10 @@ __global__ void add_staged_kernel(unsigned long long *__restrict__ partial,
     for (long long j0 = lo; j0 < hi; j0 += blockDim.x) {
         long long j = j0 + threadIdx.x;
         bool valid = j < hi;
-        unsigned long long xm = valid ? key_mod_p(keys[j]) : 0;
-        unsigned long long amt = valid ? (unsigned long long)amounts[j] : 0;
+        long long key = 0;
+        unsigned long long amt = 0;
+        if (valid) src.get(j, key, amt);
+        unsigned long long xm = valid ? key_mod_p(key) : 0;
         for (int r = 0; r < rows; ++r) {
             unsigned c = valid ? hash_col(s_a[r], s_b[r], xm, cols) : 0;
             agg_add<true>(sh + (size_t)r * cols, c, amt, valid && amt != 0);
@@ -140,6 +166,13 @@ __global__ void reduce_partials_kernel(unsigned long long *__restrict__ table,
         for (unsigned p = 0; p < nparts; ++p) acc += partial[(size_t)p * cells + i];
         table[i] = acc;
     }
+}
+
+__global__ void merge_kernel(unsigned long long *__restrict__ table,
+                             const unsigned long long *__restrict__ delta, long long cells) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cells;
+         i += (long long)gridDim.x * blockDim.x)
+        table[i] += delta[i];  // u64 wrap-around == numpy int64 add.at
 }
 
 __global__ void saturate_kernel(long long *__restrict__ table, long long cells,
@@ -174,43 +207,53 @@ constexpr size_t STAGED_MAX_BYTES = 220 * 1024;
 
 }  // namespace
 
-void sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *ha, const int64_t *hb,
-                const int64_t *keys, const int64_t *amounts, int64_t k, int32_t *d_sat,
-                cudaStream_t s) {
-    if (k > 0) {
-        size_t bytes = (size_t)rows * cols * sizeof(unsigned long long);
-        bool staged = rows <= 8 && bytes <= STAGED_MAX_BYTES && k >= 4 * (long long)rows * cols;
-        auto *t = reinterpret_cast<unsigned long long *>(table);
-        auto *kk = reinterpret_cast<const long long *>(keys);
-        auto *aa = reinterpret_cast<const long long *>(amounts);
-        auto *pa = reinterpret_cast<const long long *>(ha);
-        auto *pb = reinterpret_cast<const long long *>(hb);
-        if (staged) {
-            static bool attr = false;
-            if (!attr) {
-                CVZ_CUDA(cudaFuncSetAttribute(add_staged_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)STAGED_MAX_BYTES));
-                attr = true;
-            }
-            // one CTA per SM (the table fills its shared memory); each writes
-            // a partial table, one pass sums them into the sketch
-            long long want = k / (2LL * rows * cols) + 1;
-            unsigned grid = (unsigned)std::min<long long>(want, num_sms());
-            Scratch sc(s);
-            auto *partial = sc.alloc<unsigned long long>((size_t)grid * rows * cols);
-            CVZ_LAUNCH(add_staged_kernel, grid, 1024, bytes, s, partial, pa, pb, rows,
-                       (unsigned)cols, kk, aa, (long long)k);
-            CVZ_LAUNCH(reduce_partials_kernel, grid_for((long long)rows * cols, 256, 1, 4), 256,
-                       0, s, t, partial, grid, (unsigned)(rows * cols));
-        } else {
-            CVZ_LAUNCH(add_direct_kernel, grid_for(k, 256, 1, 8), 256, 0, s, t, pa, pb, rows,
-                       (unsigned)cols, kk, aa, (long long)k);
+template <class Src>
+void sketch_accumulate(int64_t *table, int rows, int64_t cols, const int64_t *ha,
+                       const int64_t *hb, Src src, int64_t k, cudaStream_t s) {
+    if (k <= 0) return;
+    size_t bytes = (size_t)rows * cols * sizeof(unsigned long long);
+    bool staged = rows <= 8 && bytes <= STAGED_MAX_BYTES && k >= 4 * (long long)rows * cols;
+    auto *t = reinterpret_cast<unsigned long long *>(table);
+    auto *pa = reinterpret_cast<const long long *>(ha);
+    auto *pb = reinterpret_cast<const long long *>(hb);
+    if (staged) {
+        static bool attr = false;
+        if (!attr) {
+            CVZ_CUDA(cudaFuncSetAttribute(add_staged_kernel<Src>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)STAGED_MAX_BYTES));
+            attr = true;
         }
+        // one CTA per SM (the table fills its shared memory); each writes
+        // a partial table, one pass sums them into the sketch
+        long long want = k / (2LL * rows * cols) + 1;
+        unsigned grid = (unsigned)std::min<long long>(want, num_sms());
+        Scratch sc(s);
+        auto *partial = sc.alloc<unsigned long long>((size_t)grid * rows * cols);
+        CVZ_LAUNCH(add_staged_kernel<Src>, grid, 1024, bytes, s, partial, pa, pb, rows,
+                   (unsigned)cols, src, (long long)k);
+        CVZ_LAUNCH(reduce_partials_kernel, grid_for((long long)rows * cols, 256, 1, 4), 256, 0,
+                   s, t, partial, grid, (unsigned)(rows * cols));
+    } else {
+        CVZ_LAUNCH(add_direct_kernel<Src>, grid_for(k, 256, 1, 8), 256, 0, s, t, pa, pb, rows,
+                   (unsigned)cols, src, (long long)k);
     }
+}
+
+void sketch_saturate(int64_t *table, int rows, int64_t cols, int32_t *d_sat, cudaStream_t s) {
     long long cells = (long long)rows * cols;
     CVZ_LAUNCH(saturate_kernel, grid_for(cells, 256, 4, 2), 256, 0, s,
                reinterpret_cast<long long *>(table), cells, d_sat);
+}
+
+void sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *ha, const int64_t *hb,
+                const int64_t *keys, const int64_t *amounts, int64_t k, int32_t *d_sat,
+                cudaStream_t s) {
+    sketch_accumulate(table, rows, cols, ha, hb,
+                      KeyAmounts{reinterpret_cast<const long long *>(keys),
+                                 reinterpret_cast<const long long *>(amounts)},
+                      k, s);
+    sketch_saturate(table, rows, cols, d_sat, s);
 }
 
 void sketch_estimate(const int64_t *table, int rows, int64_t cols, const int64_t *ha,
@@ -263,6 +306,46 @@ int cvz_sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *hash_a
             CVZ_REQUIRE(!h, CVZ_ERR_VALUE, "amounts must be non-negative");
         }
         sketch_add(table, rows, cols, hash_a, hash_b, keys, amounts, k, d_saturated, s);
+    });
+}
+
+int cvz_sketch_accumulate(int64_t *delta, int rows, int64_t cols, const int64_t *hash_a,
+                          const int64_t *hash_b, const int64_t *keys, const int64_t *amounts,
+                          int64_t k, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(rows >= 1 && cols >= 1 && cols < (1LL << 31), CVZ_ERR_VALUE,
+                    "sketch needs 1 <= cols < 2^31 and rows >= 1");
+        sketch_accumulate(delta, rows, cols, hash_a, hash_b,
+                          KeyAmounts{reinterpret_cast<const long long *>(keys),
+                                     reinterpret_cast<const long long *>(amounts)},
+                          k, as_stream(stream));
+    });
+}
+
+int cvz_sketch_accumulate_edges(int64_t *delta, int rows, int64_t cols, const int64_t *hash_a,
+                                const int64_t *hash_b, const int32_t *edges, int64_t m,
+                                const int64_t *labels, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(rows >= 1 && cols >= 1 && cols < (1LL << 31), CVZ_ERR_VALUE,
+                    "sketch needs 1 <= cols < 2^31 and rows >= 1");
+        CVZ_REQUIRE(m >= 0, CVZ_ERR_VALUE, "negative edge count");
+        sketch_accumulate(delta, rows, cols, hash_a, hash_b,
+                          EdgeLabels{reinterpret_cast<const int *>(edges),
+                                     reinterpret_cast<const long long *>(labels)},
+                          2 * m, as_stream(stream));
+    });
+}
+
+int cvz_sketch_merge(int64_t *table, const int64_t *delta, int rows, int64_t cols,
+                     int32_t *d_saturated, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(rows >= 1 && cols >= 1, CVZ_ERR_VALUE, "bad sketch shape");
+        cudaStream_t s = as_stream(stream);
+        long long cells = (long long)rows * cols;
+        CVZ_LAUNCH(merge_kernel, grid_for(cells, 256, 4, 2), 256, 0, s,
+                   reinterpret_cast<unsigned long long *>(table),
+                   reinterpret_cast<const unsigned long long *>(delta), cells);
+        sketch_saturate(table, rows, cols, d_saturated, s);
     });
 }
 

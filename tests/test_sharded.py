@@ -1,0 +1,198 @@
+"""Multi-process (world_size 2, gloo on 127.0.0.1) tests of the sharded stages
+(paper_2108_00529_b200/sharded.py).
+
+CPU (no GPU): the shard plan, the Comm collectives, and that the
+decomposition the sharded stages use -- per-shard compaction + degrees +
+edge-based sketch deltas, summed across ranks -- reproduces the oracle's
+single-process degrees and sketch table bit-for-bit.
+
+GPU: two ranks sharing cuda:0 over gloo run the real kernels through
+from_edge_array_sharded / accumulate_sizes_sharded / layout_sharded and are
+compared with the single-GPU path (integers bit-exact, layout within the
+stated fp tolerance).
+"""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, has_gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawn(fn, world, *args):
+    import torch.multiprocessing as mp
+    port = _free_port()
+    mp.spawn(fn, args=(world, port) + args, nprocs=world, join=True)
+
+
+def _init(rank, world, port):
+    import sys
+    if ROOT not in sys.path:
+        sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    return dist
+
+
+# ----------------------------------------------------------------- plan
+def test_shard_plan():
+    from paper_2108_00529_b200.sharded import owned_nodes, padded_rows, shard_range
+    for total in (0, 1, 7, 100, 1001):
+        for world in (1, 2, 3, 8):
+            sl = [shard_range(total, r, world) for r in range(world)]
+            assert sl[0][0] == 0 and sl[-1][1] == total
+            assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
+            assert max(h - l for l, h in sl) - min(h - l for l, h in sl) <= 1
+            own = [owned_nodes(total, r, world) for r in range(world)]
+            assert sum(h - l for l, h in own) == total
+            assert all(h - l <= padded_rows(total, world) for l, h in own)
+            assert all(a[1] == b[0] for a, b in zip(own, own[1:]))
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
+
+
+# ------------------------------------------------------- CPU collectives
+def _cpu_worker(rank, world, port, out_dir):
+    dist = _init(rank, world, port)
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2108_00529_b200 import synth
+    from paper_2108_00529_b200.sharded import Comm, shard_range
+    comm = Comm()
+    assert (comm.rank, comm.world, comm.staged) == (rank, world, True)
+    # all_reduce: int64 sum wraps mod 2^64 like np.add.at; max
+    t = torch.tensor([2**62, rank, -5 * rank], dtype=torch.int64)
+    comm.all_reduce(t, "sum")
+    ref = np.array([2**62, 0, 0], dtype=np.int64)
+    for r in range(world):
+        ref = ref + np.array([0 if r == 0 else 2**62, r, -5 * r], dtype=np.int64)
+    assert t.tolist() == ref.tolist()
+    m = torch.tensor([float(rank), -float(rank)], dtype=torch.float64)
+    assert comm.all_reduce(m, "max").tolist() == [world - 1.0, 0.0]
+    # all_gather_rows / varlen / broadcast
+    rows = 3
+    full = torch.full((world * rows, 2), -1.0, dtype=torch.float64)
+    full[rank * rows:(rank + 1) * rows] = rank
+    comm.all_gather_rows(full, rows)
+    assert full[:, 0].tolist() == [float(r) for r in range(world) for _ in range(rows)]
+    v = torch.arange(rank + 1, dtype=torch.int32).reshape(-1, 1) + 10 * rank
+    cat = comm.all_gather_varlen(v)
+    assert cat.ravel().tolist() == [10 * r + i for r in range(world) for i in range(r + 1)]
+    b = torch.tensor([rank + 7])
+    assert comm.broadcast(b, 0).item() == 7
+
+    # the sharded stages' decomposition, restated with the oracle per shard
+    e = synth.planted_partition(3000, 30000, 30, seed=3).copy()
+    e[::97, 1] = e[::97, 0]                       # self-loops to drop
+    lo, hi = shard_range(len(e), rank, world)
+    n_full, ee, deg = orc.from_edge_array(e)
+    _, ee_loc, _ = orc.from_edge_array(e[lo:hi], node_count=n_full)
+    deg_loc = torch.from_numpy(np.bincount(ee_loc.ravel(), minlength=n_full).astype(np.int64))
+    comm.all_reduce(deg_loc, "sum")
+    assert np.array_equal(deg_loc.numpy(), deg)
+    kept = comm.all_gather_varlen(torch.from_numpy(np.ascontiguousarray(ee_loc)))
+    assert np.array_equal(kept.numpy(), ee)
+    lab = orc.detect_communities(n_full, ee, deg, orc.degree_stats(deg)[0], 10, 0)[0]
+    A, B = orc.sketch_params(4, 0)
+    cols = orc.default_cols(len(ee))
+    delta = np.zeros((4, cols), np.int64)
+    orc.sketch_add_many(delta, A, B, lab[ee_loc.ravel()], np.ones(2 * len(ee_loc), np.int64))
+    dt = torch.from_numpy(delta)
+    comm.all_reduce(dt, "sum")
+    table = np.zeros((4, cols), np.int64)
+    orc.sketch_add_many(table, A, B, lab, deg)    # node-based, single process
+    assert np.array_equal(dt.numpy(), table)
+    dist.barrier()
+    dist.destroy_process_group()
+    open(os.path.join(out_dir, f"ok{rank}"), "w").close()
+
+
+def test_sharded_decomposition_cpu_gloo():
+    with tempfile.TemporaryDirectory() as d:
+        _spawn(_cpu_worker, 2, d)
+        assert sorted(os.listdir(d)) == ["ok0", "ok1"]
+
+
+# ------------------------------------------------------------- GPU (gloo)
+def _gpu_worker(rank, world, port, out_dir, iters):
+    dist = _init(rank, world, port)
+    import torch
+    torch.cuda.set_device(0)                      # both ranks share one B200
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import synth
+    from paper_2108_00529_b200.sharded import (Comm, accumulate_sizes_sharded,
+                                               broadcast_labels, edge_slice,
+                                               from_edge_array_sharded, layout_sharded)
+    comm = Comm()
+    e = synth.planted_partition(4000, 40000, 40, seed=5).copy()
+    e[::53, 1] = e[::53, 0]
+    sg = from_edge_array_sharded(edge_slice(e, comm), comm)
+    g = sg.gather()
+    lab = None
+    if rank == 0:
+        base = cv.degree_stats(g).mode_degree
+        lab = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+    labels = broadcast_labels(lab, g.node_count, comm)
+    s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    accumulate_sizes_sharded(s, labels, sg)
+    sup = cv.contract(g, labels, s)
+    p = cv.LayoutParams(iterations=iters)
+    r_sup = layout_sharded(sup, p, comm)
+    r_full = layout_sharded(g, cv.LayoutParams(iterations=max(2, iters // 4)), comm)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), degree=sg.degree, edges=g.edges,
+             m=sg.edge_count, table=s.table, labels=labels.cpu().numpy(),
+             sup_pos=r_sup.positions, sup_disp=r_sup.displacement,
+             full_pos=r_full.positions, full_disp=r_full.displacement)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_sharded_matches_single_gpu():
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import synth
+    iters = 20
+    with tempfile.TemporaryDirectory() as d:
+        _spawn(_gpu_worker, 2, d, iters)
+        r0, r1 = (np.load(os.path.join(d, f"r{i}.npz")) for i in (0, 1))
+    # single GPU, same inputs
+    e = synth.planted_partition(4000, 40000, 40, seed=5).copy()
+    e[::53, 1] = e[::53, 0]
+    g = cv.from_edge_array(e)
+    base = cv.degree_stats(g).mode_degree
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+    s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    cv.accumulate_sizes(s, a, g)
+    sup = cv.contract(g, a, s)
+    ref_sup = cv.layout(sup, cv.LayoutParams(iterations=iters))
+    ref_full = cv.layout(g, cv.LayoutParams(iterations=max(2, iters // 4)))
+    for r in (r0, r1):
+        # integers: bit-exact
+        assert int(r["m"]) == g.edge_count
+        assert np.array_equal(r["degree"], g.degree)
+        assert np.array_equal(r["edges"], g.edges)
+        assert np.array_equal(r["labels"], a.label)
+        assert np.array_equal(r["table"], s.table)
+        # layout: every rank holds the same positions ...
+        for key, ref in (("sup_pos", ref_sup), ("full_pos", ref_full)):
+            pos = r[key]
+            diam = np.hypot(*(ref.positions.max(0) - ref.positions.min(0)))
+            # ... within 1e-7 x diameter of the single-GPU run (regrouped fp64
+            # sums of swing/traction only; same tolerance as the CPU parity)
+            assert np.max(np.abs(pos - ref.positions)) <= 1e-7 * diam, key
+        np.testing.assert_allclose(r["sup_disp"], ref_sup.displacement, rtol=1e-6, atol=1e-9)
+    assert np.array_equal(r0["sup_pos"], r1["sup_pos"])
+    assert np.array_equal(r0["full_pos"], r1["full_pos"])
