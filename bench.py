@@ -33,6 +33,15 @@ sys.path.insert(0, ROOT)
 
 METRIC = "edges/s community pass; ms per ForceAtlas2 iter; end-to-end s at 3M/34M graph"
 WORKLOAD = "C4: DC-SBM power-law 3M nodes / 34M edge draws (gamma 2.3, k=30000, mu 0.1)"
+
+
+def workload(config):
+    if config == "C4":
+        return WORKLOAD
+    from paper_2108_00529_b200.synth import CONFIGS
+    c = CONFIGS[config]
+    return (f"{config}: DC-SBM {c['n']} nodes / {c['m']} edge draws (gamma {c['gamma']}, "
+            f"k={c['k']}, mu 0.1) -- a parity config, not the headline")
 ITERS = 100
 
 
@@ -44,6 +53,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C4")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-sharded", action="store_true")
     return p.parse_args()
 
 
@@ -106,8 +116,14 @@ def dist_init(n_gpus):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # CVZ_DIST_BACKEND=gloo lets several ranks share one GPU (test only)
+        backend = os.environ.get("CVZ_DIST_BACKEND", "nccl")
+        dev = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, ws, local
@@ -245,7 +261,7 @@ def run_ours(args, rank, ws):
     stats = []
     barrier(ws)
     launches0 = _native.launch_count()
-    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+    with Clocks(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -291,6 +307,73 @@ def run_ours(args, rank, ws):
     d2h = pos.nbytes + lab.nbytes
     return dict(ms_step=ms_step, m_in=m_in, stage=st, launches=launches, clocks=clk.summary(),
                 e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, prof=prof.kernels, fast=fast)
+
+
+# ------------------------------------------------------------ sharded stages
+FULL_ITERS = 10
+
+
+def run_sharded(args, rank, ws, reps=3):
+    """SURVEY.md 8e sharded stages on the SAME graph split across the N ranks
+    (strong scaling): edge-sharded ingest + degrees + edge-based sketch
+    (NCCL all-reduce of degrees and counters), and node-sharded full-graph
+    ForceAtlas2 (per-iteration all-reduces + position all-gather).  Device
+    time, max over ranks."""
+    import torch
+
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import sharded as sh
+    from paper_2108_00529_b200 import synth
+    comm = sh.Comm()
+    e = synth.config_graph(args.config, seed=0)
+    mine = torch.from_numpy(np.ascontiguousarray(sh.edge_slice(e, comm))).to("cuda")
+    g_sh = sh.from_edge_array_sharded(mine, comm)
+    g = g_sh.gather()
+    lab = None
+    if rank == 0:
+        base = cv.degree_stats(g).mode_degree
+        lab = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+    labels = sh.broadcast_labels(lab, g.node_count, comm)
+    cols = cv.default_cols(g.edge_count)
+
+    def ingest_sketch():
+        gs = sh.from_edge_array_sharded(mine, comm)
+        s = cv.sketch_new(4, cols, seed=0)
+        sh.accumulate_sizes_sharded(s, labels, gs)
+        return s
+
+    for _ in range(2):
+        ingest_sketch()
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(reps):
+        ingest_sketch()
+    t1.record()
+    torch.cuda.synchronize()
+    ing_ms = barrier_max(t0.elapsed_time(t1) / reps, ws)
+
+    # node-sharded full-graph layout (mass = degree + 1, unit springs)
+    from paper_2108_00529_b200.layout import _device_model, _init_positions_dev
+    mass, ed, ew = _device_model(g)
+    P = sh._layout_params(cv.LayoutParams(iterations=FULL_ITERS))
+    pos0 = _init_positions_dev(g.node_count, 0)
+    sh._run_shard(comm, g.node_count, mass, ed, ew, P, pos0, 2, False)  # warm-up
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0.record()
+    sh._run_shard(comm, g.node_count, mass, ed, ew, P, pos0, FULL_ITERS, False)
+    t1.record()
+    torch.cuda.synchronize()
+    fa2_ms = barrier_max(t0.elapsed_time(t1), ws)
+    return {"scaling": "strong", "ranks": ws, "graph": f"{args.config} seed 0 (same graph on all ranks)",
+            "ingest_sketch_ms": ing_ms, "ingest_sketch_edges_per_s": len(e) / (ing_ms / 1e3),
+            "full_graph_fa2_ms_per_iter": fa2_ms / FULL_ITERS,
+            "full_graph_fa2_iters": FULL_ITERS, "n": g.node_count, "m": g.edge_count,
+            "note": "edge-sharded ingest+degrees+sketch (all-reduce of int64 degrees and "
+                    "sketch counters); node-sharded full-graph ForceAtlas2 incl. CSR build "
+                    "(2 all-reduces + 1 all-gather per iteration)"}
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -346,7 +429,7 @@ def main():
             "impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32+f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": sample},
+            "data": "synthetic", "config": {"workload": workload(args.config), "sample": sample},
             "cpu_baseline": {"value": v, "unit": "edges/s", "cores": orc.num_threads(),
                              "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0,
@@ -354,6 +437,7 @@ def main():
         return
 
     r = run_ours(args, rank, ws)
+    shard = None if args.no_sharded else run_sharded(args, rank, ws)
     if rank != 0:
         return
     st = r["stage"]
@@ -371,7 +455,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_step"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int32 ids / f64 layout", "data": "synthetic (seeded DC-SBM, no network)",
-        "config": {"workload": WORKLOAD, "edges_in": r["m_in"], "n": st["n"], "m": st["m"],
+        "config": {"workload": workload(args.config), "edges_in": r["m_in"], "n": st["n"], "m": st["m"],
                    "rounds": st["rounds"], "supernodes": st["k"], "superedges": st["se"],
                    "layout_iterations": ITERS, "community_mode": "deterministic",
                    "parallelism": f"replicas x{ws}",
@@ -389,6 +473,7 @@ def main():
         "roofline": roof,
         "top_kernels": top,
         "gpu_launches": r["launches"],
+        "sharded": shard,
         "clocks": r["clocks"],
         "e2e": {"value": r["m_in"] * ws / (r["e2e_ms"] / 1000.0), "unit": "edges/s",
                 "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
