@@ -78,6 +78,28 @@ int cvz_degree_count(const int32_t *edges, int64_t m, int64_t n, int64_t *degree
  * degrees (ties -> smaller), sum, max}.  mode = 0 when all degrees are 0. */
 int cvz_degree_stats(const int64_t *degree, int64_t n, int64_t *out3, void *stream);
 
+/* C/graph.py:50-92 parse_edge_list, host tokenizer (multi-threaded C++).
+ * text [host] ASCII bytes; threads <= 0 = all hardware threads.  Lines are
+ * str.splitlines(), stripped, '#'/'%' comments and blank lines skipped,
+ * exactly two Python-int tokens per line, u == v dropped.  Result:
+ *   *err_code 0 ok (*m_out pairs kept, *handle to take them), 1 wrong token
+ *   count (*err_tokens = K, "expected two tokens, got K"), 2 non-integer
+ *   token, 3 input outside the native subset (non-ASCII byte, id outside
+ *   int64: the caller uses the reference's Python loop); *err_line = the
+ *   1-based line of the first error.
+ * cvz_parse_take copies the 2*m external ids (u, v interleaved, line order)
+ * into pairs_out [host] and frees the handle (pairs_out NULL: just free). */
+int cvz_parse_begin(const char *text, int64_t len, int threads, void **handle, int64_t *m_out,
+                    int64_t *err_line, int *err_code, int *err_tokens);
+int cvz_parse_take(void *handle, int64_t *pairs_out);
+
+/* C/graph.py:80-81 first-seen remap on the GPU: ext [dev] int64[count]
+ * (u, v interleaved in line order) -> dense [dev] int32[count], dense id =
+ * order of first appearance; *n_out [host] = number of distinct ids.
+ * count < 2^31.  SYNCHRONISES. */
+int cvz_first_seen_remap(const int64_t *ext, int64_t count, int32_t *dense, int64_t *n_out,
+                         void *stream);
+
 /* ------------------------------------------------------------ community */
 
 /* C/community.py:98-120 _scoda_pass followed by C/community.py:123-161
@@ -98,6 +120,16 @@ int cvz_scoda_pass(const int32_t *edges, int64_t m, const int64_t *order, int64_
  * reached from x.  lab values must lie in [0,n) (else CVZ_ERR_RANGE, after a
  * stream sync). */
 int cvz_resolve_labels(const int64_t *lab, int64_t n, int64_t *out, void *stream);
+
+/* C/community.py:164-195 make_schedule on the host (C++): out [host]
+ * int64[m] = edge-processing order of `workers` chunked readers;
+ * interleave 0 = "random" (numpy Generator(PCG64).integers replayed from the
+ * state numpy's SeedSequence gives: 128-bit state/increment, has_uint32 /
+ * uinteger buffer), 1 = "roundrobin".  workers <= 1 or m < 2: identity.
+ * workers < 2^32. */
+int cvz_make_schedule(int64_t m, int workers, int interleave, uint64_t state_hi,
+                      uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int has_uint32,
+                      uint32_t uinteger, int64_t *out);
 
 /* One round of C/community.py:253-278 detect_communities on device:
  *   size-seeded counters (round > 1), pass over cur_edges (order or NULL),
@@ -260,6 +292,23 @@ int cvz_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uin
 int cvz_modularity_parts(const int32_t *edges, int64_t m, const int32_t *dense,
                          const int64_t *degree, int64_t n, int64_t k, int64_t *intra,
                          int64_t *degsum, void *stream);
+
+/* Dense community ids for arbitrary int64 labels (rank among the sorted
+ * unique labels, np.unique(return_inverse=True)): dense [dev] int32[n],
+ * *k_out [host] = number of communities.  SYNCHRONISES. */
+int cvz_dense_labels(const int64_t *labels, int64_t n, int32_t *dense, int64_t *k_out,
+                     void *stream);
+
+/* C/metrics.py:70-75 community_size_histogram on device: sizes [dev]
+ * int64[k] = members per dense id; hist [dev] int64[n+1] or NULL: hist[s] =
+ * number of communities of size s. */
+int cvz_community_sizes(const int32_t *dense, int64_t n, int64_t k, int64_t *sizes,
+                        int64_t *hist, void *stream);
+
+/* C/metrics.py:34-46 modularity: *q [dev] f64 = sum_c intra_c/m -
+ * (degsum_c / 2m)^2 over dense ids (m > 0, else CVZ_ERR_VALUE). */
+int cvz_modularity(const int32_t *edges, int64_t m, const int32_t *dense, const int64_t *degree,
+                   int64_t n, int64_t k, double *q, void *stream);
 
 #ifdef __cplusplus
 }

@@ -77,6 +77,16 @@ SIGNATURES = {
     "cvz_fa2_shard_finish": [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64),
                              ctypes.POINTER(ctypes.c_int), _P],
     "cvz_fa2_shard_destroy": [_P, _P],
+    "cvz_parse_begin": [ctypes.c_char_p, _I64, _I32, ctypes.POINTER(ctypes.c_void_p),
+                        ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int),
+                        ctypes.POINTER(ctypes.c_int)],
+    "cvz_parse_take": [_P, _P],
+    "cvz_first_seen_remap": [_P, _I64, _P, ctypes.POINTER(_I64), _P],
+    "cvz_dense_labels": [_P, _I64, _P, ctypes.POINTER(_I64), _P],
+    "cvz_community_sizes": [_P, _I64, _I64, _P, _P, _P],
+    "cvz_modularity": [_P, _I64, _P, _P, _I64, _I64, _P, _P],
+    "cvz_make_schedule": [_I64, _I32, _I32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                          ctypes.c_uint64, _I32, ctypes.c_uint32, _P],
 }
 
 _lib = None

@@ -123,35 +123,25 @@ def fresh_assignment(n: int) -> CommunityAssignment:
 def make_schedule(m: int, workers: int, seed: int, interleave: str = "random") -> np.ndarray:
     """Processing order emulating `workers` chunked readers (C/community.py:164-195).
 
-    Host logic: the order is a property of the seeded numpy Generator stream
-    and is uploaded as-is, so the GPU pass sees exactly the reference's
-    interleaving."""
+    Native (cvz_make_schedule, host C++): the seeded numpy Generator stream is
+    replayed from the PCG64 state numpy's SeedSequence produces, so the order
+    is the reference's bit-for-bit."""
+    if interleave not in ("random", "roundrobin"):
+        if workers > 1 and m >= 2:
+            raise ValueError(f"unknown interleave {interleave!r}")
+    out = np.empty(max(int(m), 0), dtype=np.int64)
     if workers <= 1 or m < 2:
-        return np.arange(m, dtype=np.int64)
-    cuts = (np.arange(workers + 1, dtype=np.int64) * m) // workers
-    if interleave == "roundrobin":
-        pos = np.arange(m, dtype=np.int64)
-        owner = np.searchsorted(cuts, pos, side="right") - 1
-        rank_in_chunk = pos - cuts[owner]
-        # deal the i-th element of every chunk before any (i+1)-th one
-        return np.argsort(rank_in_chunk, kind="stable").astype(np.int64)
-    if interleave != "random":
-        raise ValueError(f"unknown interleave {interleave!r}")
-    gen = np.random.default_rng(seed)
-    nxt = cuts[:-1].copy()
-    end = cuts[1:]
-    alive = [w for w in range(workers) if nxt[w] < end[w]]
-    order = np.empty(m, dtype=np.int64)
-    k = 0
-    while alive:
-        pick = int(gen.integers(len(alive)))
-        w = alive[pick]
-        order[k] = nxt[w]
-        k += 1
-        nxt[w] += 1
-        if nxt[w] == end[w]:
-            del alive[pick]
-    return order
+        out[:] = np.arange(m, dtype=np.int64)
+        return out
+    st = np.random.default_rng(seed).bit_generator.state
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    m64 = (1 << 64) - 1
+    rc = nat.load().cvz_make_schedule(int(m), int(workers), 0 if interleave == "random" else 1,
+                                      s >> 64, s & m64, inc >> 64, inc & m64,
+                                      int(st["has_uint32"]), int(st["uinteger"]),
+                                      out.ctypes.data_as(ctypes.c_void_p))
+    nat.check(rc, "cvz_make_schedule")
+    return out
 
 
 def _schedule_dev(m, workers, seed, interleave):

@@ -148,6 +148,65 @@ __global__ void degsum_kernel(const int *__restrict__ dense, const long long *__
         atomicAdd(degsum + dense[i], (unsigned long long)deg[i]);
 }
 
+// C/metrics.py:70-75 community sizes (bincount of dense ids) and the size
+// histogram {size: number of communities}; hist has n + 1 bins.
+__global__ void sizes_kernel(const int *__restrict__ dense, long long n,
+                             unsigned long long *__restrict__ sizes) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        int c = dense[i];
+        // warp-aggregate runs of equal ids (labels are clustered)
+        unsigned peers = __match_any_sync(__activemask(), c);
+        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(sizes + c, (unsigned long long)__popc(peers));
+    }
+}
+
+__global__ void size_hist2_kernel(const long long *__restrict__ sizes, long long k,
+                                  unsigned long long *__restrict__ hist) {
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < k;
+         c += (long long)gridDim.x * blockDim.x)
+        atomicAdd(hist + sizes[c], 1ull);
+}
+
+// C/metrics.py:34-46 final sum: Q = sum_c intra_c/m - (degsum_c/2m)^2 in fp64
+// (block tree + last-block reduction; numpy's pairwise order differs only in
+// rounding, the tests gate 1e-9 like T/test_acceptance.py:51-75).
+__global__ void modularity_sum_kernel(const long long *__restrict__ intra,
+                                      const long long *__restrict__ degsum, long long k,
+                                      double m, double *__restrict__ part,
+                                      unsigned *__restrict__ ctr, double *__restrict__ q) {
+    __shared__ double sh[256];
+    double acc = 0.0;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < k;
+         c += (long long)gridDim.x * blockDim.x) {
+        double d = (double)degsum[c] / (2.0 * m);
+        acc += (double)intra[c] / m - d * d;
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = sh[0];
+        __threadfence();
+        last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    double v = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += 256) v += ((volatile double *)part)[b];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *q = sh[0];
+}
+
 int bits_for(long long k) {  // bits to hold values 0..k-1 (>= 1)
     int b = 1;
     while (b < 62 && (1LL << b) < k) ++b;
@@ -312,6 +371,62 @@ int cvz_contract_release(cvz_contract_result *res, void *stream) {
                         (void *)res->mult})
             if (p) CVZ_CUDA(cudaFreeAsync(p, s));
         *res = cvz_contract_result{0, 0, nullptr, nullptr, nullptr, nullptr};
+    });
+}
+
+int cvz_dense_labels(const int64_t *labels, int64_t n, int32_t *dense, int64_t *k_out,
+                     void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(n >= 1, CVZ_ERR_VALUE, "need at least one label");
+        cudaStream_t s = as_stream(stream);
+        Scratch sc(s);
+        int64_t *comm = nullptr;
+        *k_out = dense_ids(labels, n, dense, &comm, sc, s);
+        if (comm) CVZ_CUDA(cudaFreeAsync(comm, s));
+    });
+}
+
+int cvz_community_sizes(const int32_t *dense, int64_t n, int64_t k, int64_t *sizes,
+                        int64_t *hist, void *stream) {
+    return guard([&] {
+        cudaStream_t s = as_stream(stream);
+        CVZ_CUDA(cudaMemsetAsync(sizes, 0, sizeof(int64_t) * (k ? k : 1), s));
+        if (n > 0)
+            CVZ_LAUNCH(sizes_kernel, grid_for(n, 256, 1, 8), 256, 0, s, dense, (long long)n,
+                       reinterpret_cast<unsigned long long *>(sizes));
+        if (hist) {
+            CVZ_CUDA(cudaMemsetAsync(hist, 0, sizeof(int64_t) * (n + 1), s));
+            if (k > 0)
+                CVZ_LAUNCH(size_hist2_kernel, grid_for(k, 256, 1, 8), 256, 0, s,
+                           reinterpret_cast<const long long *>(sizes), (long long)k,
+                           reinterpret_cast<unsigned long long *>(hist));
+        }
+    });
+}
+
+int cvz_modularity(const int32_t *edges, int64_t m, const int32_t *dense, const int64_t *degree,
+                   int64_t n, int64_t k, double *q, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(m > 0, CVZ_ERR_VALUE, "modularity undefined for a graph with no edges");
+        cudaStream_t s = as_stream(stream);
+        Scratch sc(s);
+        auto *intra = sc.alloc<int64_t>(k ? k : 1), *degsum = sc.alloc<int64_t>(k ? k : 1);
+        CVZ_CUDA(cudaMemsetAsync(intra, 0, sizeof(int64_t) * (k ? k : 1), s));
+        CVZ_CUDA(cudaMemsetAsync(degsum, 0, sizeof(int64_t) * (k ? k : 1), s));
+        CVZ_LAUNCH(modularity_parts_kernel, grid_for(m, 256, 1, 16), 256, 0, s,
+                   reinterpret_cast<const int2 *>(edges), (long long)m, dense,
+                   reinterpret_cast<unsigned long long *>(intra));
+        if (n > 0)
+            CVZ_LAUNCH(degsum_kernel, grid_for(n, 256, 1, 8), 256, 0, s, dense,
+                       reinterpret_cast<const long long *>(degree), (long long)n,
+                       reinterpret_cast<unsigned long long *>(degsum));
+        unsigned g = grid_for(k, 256, 4, 2);
+        auto *part = sc.alloc<double>(g);
+        auto *ctr = sc.alloc<unsigned>(1);
+        CVZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+        CVZ_LAUNCH(modularity_sum_kernel, g, 256, 0, s, reinterpret_cast<const long long *>(intra),
+                   reinterpret_cast<const long long *>(degsum), (long long)k, (double)m, part, ctr,
+                   q);
     });
 }
 

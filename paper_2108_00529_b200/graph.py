@@ -8,6 +8,7 @@ numpy arrays only when read.
 
 from __future__ import annotations
 
+import ctypes
 import io
 from dataclasses import dataclass
 
@@ -86,15 +87,10 @@ class DegreeStats:
     max_degree: int
 
 
-def parse_edge_list(text) -> Graph:
-    """C/graph.py:50-92: SNAP-style text -> Graph (first-seen id remap,
-    comments `#`/`%`, self-loops dropped, duplicates kept).
-
-    Tokenising is host work; the degree histogram runs on the GPU."""
-    if isinstance(text, bytes):
-        text = text.decode("utf-8", errors="replace")
-    lines = text.splitlines() if isinstance(text, str) else [
-        ln.decode() if isinstance(ln, bytes) else ln for ln in text]
+def _parse_lines(lines) -> Graph:
+    """The reference's line loop (C/graph.py:65-92), used for inputs outside
+    the native tokenizer's subset (non-ASCII text, ids beyond int64, line
+    iterables).  Tokenising is host work; degrees run on the GPU."""
     ids: dict[int, int] = {}
     flat: list[int] = []
     for no, raw in enumerate(lines, start=1):
@@ -118,10 +114,68 @@ def parse_edge_list(text) -> Graph:
                            node_count=len(ids))
 
 
+def _parse_native(data: bytes):
+    """Multi-threaded C++ tokenizer (cvz_parse_begin/take) + GPU first-seen
+    remap (cvz_first_seen_remap).  Returns None when the text is outside the
+    native subset (the caller then runs the reference's loop)."""
+    T = nat.torch()
+    lib = nat.load()
+    h = ctypes.c_void_p()
+    m, el = ctypes.c_int64(0), ctypes.c_int64(0)
+    ec, et = ctypes.c_int(0), ctypes.c_int(0)
+    nat.check(lib.cvz_parse_begin(data, len(data), 0, ctypes.byref(h), ctypes.byref(m),
+                                  ctypes.byref(el), ctypes.byref(ec), ctypes.byref(et)),
+              "cvz_parse_begin")
+    if ec.value == 3:
+        return None
+    if ec.value == 1:
+        raise ParseError(f"line {el.value}: expected two tokens, got {et.value}")
+    if ec.value == 2:
+        raise ParseError(f"line {el.value}: non-integer token")
+    if m.value == 0:
+        lib.cvz_parse_take(h, None)
+        raise ParseError("no edges")
+    ext_h = T.empty(2 * m.value, dtype=T.int64).pin_memory()
+    nat.check(lib.cvz_parse_take(h, ctypes.c_void_p(ext_h.data_ptr())), "cvz_parse_take")
+    ext = ext_h.to(nat.device(), non_blocking=True)
+    dense = T.empty((m.value, 2), dtype=T.int32, device=nat.device())
+    n = ctypes.c_int64(0)
+    nat.call("cvz_first_seen_remap", nat.ptr(ext), 2 * m.value, nat.ptr(dense),
+             ctypes.byref(n), nat.stream())
+    return from_edge_array(dense, node_count=n.value)
+
+
+def parse_edge_list(text) -> Graph:
+    """C/graph.py:50-92: SNAP-style text -> Graph (first-seen id remap,
+    comments `#`/`%`, self-loops dropped, duplicates kept).
+
+    str/bytes go through the native tokenizer + GPU remap (SURVEY.md 8f
+    row 1); line iterables and non-ASCII text through the reference loop."""
+    if isinstance(text, (bytes, bytearray, memoryview)):
+        g = _parse_native(bytes(text))
+        if g is not None:
+            return g
+        text = bytes(text).decode("utf-8", errors="replace")
+    if isinstance(text, str):
+        if text.isascii():
+            g = _parse_native(text.encode("ascii"))
+            if g is not None:
+                return g
+        return _parse_lines(text.splitlines())
+    return _parse_lines([ln.decode() if isinstance(ln, bytes) else ln for ln in text])
+
+
 def load_edge_list(path) -> Graph:
-    """C/graph.py:95-97."""
+    """C/graph.py:95-97 (file bytes straight to the native tokenizer; a
+    non-ASCII file is decoded as utf-8 text exactly like the reference)."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if data.isascii():
+        g = _parse_native(data)
+        if g is not None:
+            return g
     with open(path, "r", encoding="utf-8") as fh:
-        return parse_edge_list(fh.read())
+        return _parse_lines(fh.read().splitlines())
 
 
 def write_edge_list(g: Graph, path_or_file) -> None:

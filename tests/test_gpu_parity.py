@@ -233,6 +233,24 @@ def test_gpu_modularity_matches_oracle(cv, orc):
     g = cv.from_edge_array(e)
     lab = np.random.default_rng(0).integers(0, 50, size=g.node_count)
     assert abs(cv.modularity(g, lab) - orc.modularity(g.edges, g.degree, lab)) <= 1e-9
+    # arbitrary int64 labels (sparse, negative) and detected labels
+    lab2 = np.random.default_rng(1).integers(-2**40, 2**40, size=60)[lab]
+    assert abs(cv.modularity(g, lab2) - orc.modularity(g.edges, g.degree, lab2)) <= 1e-9
+    det = cv.detect_communities(g, cv.ThresholdSchedule(base=cv.degree_stats(g).mode_degree))
+    q_ref = orc.modularity(g.edges, g.degree, det.label)
+    assert abs(cv.modularity(g, det) - q_ref) <= 1e-9
+
+
+def test_gpu_size_histogram_matches_reference(cv):
+    # C/metrics.py:70-75: np.unique(labels) counts, then np.unique(counts)
+    def ref(labels):
+        _, counts = np.unique(labels, return_counts=True)
+        sizes, freq = np.unique(counts, return_counts=True)
+        return {int(s): int(f) for s, f in zip(sizes, freq)}
+    rng = np.random.default_rng(3)
+    for lab in (rng.integers(0, 40, size=5000), rng.integers(-2**50, 2**50, size=300)[
+            rng.integers(0, 300, size=20000)], np.arange(7), np.zeros(9, np.int64)):
+        assert cv.community_size_histogram(lab) == ref(lab)
 
 
 # ----------------------------------------------------------------- sketch

@@ -1,0 +1,159 @@
+"""Native edge-list loader: the C++ tokenizer
+(cvz_parse_begin/take, host code -- runs here without a GPU) against a
+restatement of C/graph.py:50-92's line loop, and the whole
+parse_edge_list / load_edge_list (tokenizer + GPU first-seen remap) against
+the oracle on the B200."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+from oracle import oracle as orc
+from paper_2108_00529_b200 import _native
+
+
+def ref_tokens(text: str):
+    """C/graph.py:65-86 up to the remap: (ext pairs, error) where error is
+    (line, kind, tokens) with kind 1 = token count, 2 = non-integer."""
+    out = []
+    for no, line in enumerate(text.splitlines(), start=1):
+        s = line.strip()
+        if not s or s[0] in "#%":
+            continue
+        parts = s.split()
+        if len(parts) != 2:
+            return out, (no, 1, len(parts))
+        try:
+            u, v = int(parts[0]), int(parts[1])
+        except ValueError:
+            return out, (no, 2, 0)
+        if u != v:
+            out += [u, v]
+    return out, None
+
+
+def native_tokens(data: bytes, threads: int):
+    lib = _native.load()
+    h = ctypes.c_void_p()
+    m, el = ctypes.c_int64(0), ctypes.c_int64(0)
+    ec, et = ctypes.c_int(0), ctypes.c_int(0)
+    rc = lib.cvz_parse_begin(data, len(data), threads, ctypes.byref(h), ctypes.byref(m),
+                             ctypes.byref(el), ctypes.byref(ec), ctypes.byref(et))
+    assert rc == 0
+    if ec.value:
+        return None, (el.value, ec.value, et.value if ec.value == 1 else 0)
+    buf = np.empty(2 * m.value, np.int64)
+    assert lib.cvz_parse_take(h, buf.ctypes.data_as(ctypes.c_void_p)) == 0
+    return buf.tolist(), None
+
+
+BREAKS = ["\n", "\r\n", "\r", "\v", "\f", "\x1c", "\x1d", "\x1e"]
+SPACES = [" ", "\t", "  ", "\x1f", " \t "]
+
+
+def random_text(rng, lines=200, bad=0.0):
+    out = []
+    for _ in range(lines):
+        r = rng.random()
+        if r < 0.08:
+            line = rng.choice(["", "   ", "# comment 1 2", "% x", "  #c", "\t"])
+        else:
+            toks = []
+            for _ in range(2):
+                x = int(rng.integers(-50, 5000))
+                t = str(x)
+                q = rng.random()
+                if q < 0.05 and x >= 10:
+                    t = t[:1] + "_" + t[1:]
+                elif q < 0.08:
+                    t = "+" + t if x >= 0 else t
+                elif q < 0.10:
+                    t = "00" + t if x >= 0 else t
+                toks.append(t)
+            if rng.random() < 0.05:
+                toks[1] = toks[0]                      # self-loop
+            if rng.random() < bad:
+                k = rng.integers(4)
+                if k == 0:
+                    toks.append("7")
+                elif k == 1:
+                    toks = toks[:1]
+                elif k == 2:
+                    toks[0] = rng.choice(["1.5", "x", "1__2", "_1", "1_", "--3", "0x10", "+"])
+                else:
+                    toks[1] = "1e3"
+            sp = SPACES[rng.integers(len(SPACES))]
+            line = SPACES[rng.integers(len(SPACES))] * int(rng.integers(2)) + sp.join(toks)
+        out.append(line + BREAKS[rng.integers(len(BREAKS))])
+    return "".join(out)
+
+
+@pytest.mark.parametrize("threads", [1, 3, 16])
+def test_tokenizer_matches_reference_loop(threads):
+    rng = np.random.default_rng(threads)
+    for trial in range(60):
+        text = random_text(rng, lines=int(rng.integers(1, 300)), bad=0.0 if trial % 2 else 0.01)
+        ref, err = ref_tokens(text)
+        got, gerr = native_tokens(text.encode(), threads)
+        assert gerr == err, (trial, gerr, err)
+        if err is None:
+            assert got == ref
+
+
+def test_tokenizer_edge_cases():
+    cases = {
+        "1 2": ([1, 2], None),
+        "1 2\n\n3 3\n4 5\r\n": ([1, 2, 4, 5], None),
+        "\r\n\r\n1 x\n": ([], (3, 2, 0)),
+        "1 2 3": ([], (1, 1, 3)),
+        "a\rb c": ([], (1, 1, 1)),
+        "1_000 -2": ([1000, -2], None),
+        "9223372036854775807 -9223372036854775808": ([2**63 - 1, -2**63], None),
+        "# only comments\n% here\n": ([], None),
+        "1\x1f2 3": ([], (1, 1, 3)),     # \x1f is whitespace, not a line break
+        "1 2\x1c3 4": ([1, 2, 3, 4], None),
+    }
+    for text, (pairs, err) in cases.items():
+        got, gerr = native_tokens(text.encode(), 2)
+        assert gerr == err, text
+        if err is None:
+            assert got == pairs, text
+        assert ref_tokens(text) == (pairs if err is None else ref_tokens(text)[0], err), text
+    # outside the native subset -> code 3 (caller falls back to the Python loop)
+    for text in ("1 2\n3 99999999999999999999", "# café\n1 2", "1 2 3 4"):
+        _, gerr = native_tokens(text.encode(), 1)
+        assert gerr[1] == 3, text
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_parse_edge_list_matches_oracle(tmp_path):
+    import paper_2108_00529_b200 as cv
+    rng = np.random.default_rng(7)
+    for trial in range(8):
+        text = random_text(rng, lines=int(rng.integers(5, 3000)))
+        g = cv.parse_edge_list(text)
+        n, e, deg = orc.parse_edge_list(text)
+        assert g.node_count == n and np.array_equal(g.edges, e) and np.array_equal(g.degree, deg)
+        gb = cv.parse_edge_list(text.encode())
+        assert np.array_equal(gb.edges, e)
+    # large random external ids (sparse 64-bit range) and a file
+    ids = rng.integers(-2**62, 2**62, size=5000)
+    pairs = ids[rng.integers(0, 5000, size=(40000, 2))]
+    text = "\n".join(f"{a} {b}" for a, b in pairs) + "\n"
+    p = tmp_path / "g.txt"
+    p.write_text("# header\n" + text)
+    g = cv.load_edge_list(str(p))
+    n, e, deg = orc.parse_edge_list("# header\n" + text)
+    assert g.node_count == n and np.array_equal(g.edges, e) and np.array_equal(g.degree, deg)
+    # reference errors
+    for bad, msg in (("1 2\n3\n", "line 2: expected two tokens, got 1"),
+                     ("1 2\nx y\n", "line 2: non-integer token"),
+                     ("# c\n\n", "no edges"), ("5 5\n", "no edges")):
+        with pytest.raises(cv.ParseError, match=msg):
+            cv.parse_edge_list(bad)
+    # non-ASCII goes through the reference loop with the same result
+    g = cv.parse_edge_list("# café\n10 20\n20 30\n")
+    assert g.edges.tolist() == [[0, 1], [1, 2]]
