@@ -310,6 +310,25 @@ int cvz_community_sizes(const int32_t *dense, int64_t n, int64_t k, int64_t *siz
 int cvz_modularity(const int32_t *edges, int64_t m, const int32_t *dense, const int64_t *degree,
                    int64_t n, int64_t k, double *q, void *stream);
 
+/* ------------------------------------------------------------- writers */
+
+/* Output formats, host C++, multi-threaded.  Results
+ * are library-owned text: *handle + *bytes; cvz_text_take copies the text
+ * into out [host, bytes long] (NULL: discard) and frees the handle.
+ * format_table: nrows rows of ncols `sep`-separated fields + '\n'; kinds[c]
+ * 0 = int64 column cols[c], 1 = double column "%.3f", 2 = the row index
+ * (cols[c] unused) -- C/supergraph.py:79-91, C/community.py:284-294,
+ * C/graph.py:100-111, C/sketch.py:101-102, C/cli.py:200-215.
+ * format_svg: C/render.py:96-139 byte for byte (viewBox from positions and
+ * radii, optional edges with multiplicity opacity, circles in (class,
+ * index) order); pos [host] f64[n*2], classes in [0, ncolors). */
+int cvz_format_table(int64_t nrows, int ncols, const int *kinds, const void *const *cols,
+                     char sep, void **handle, int64_t *bytes);
+int cvz_format_svg(int64_t n, const double *pos, const double *radii, const int64_t *classes,
+                   const char *const *palette, int ncolors, int64_t ne, const int64_t *edges,
+                   const double *mult, double margin, void **handle, int64_t *bytes);
+int cvz_text_take(void *handle, char *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,11 @@ SIGNATURES = {
     "cvz_dense_labels": [_P, _I64, _P, ctypes.POINTER(_I64), _P],
     "cvz_community_sizes": [_P, _I64, _I64, _P, _P, _P],
     "cvz_modularity": [_P, _I64, _P, _P, _I64, _I64, _P, _P],
+    "cvz_format_table": [_I64, _I32, _P, _P, ctypes.c_char, ctypes.POINTER(ctypes.c_void_p),
+                         ctypes.POINTER(_I64)],
+    "cvz_format_svg": [_I64, _P, _P, _P, _P, _I32, _I64, _P, _P, _D,
+                       ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_I64)],
+    "cvz_text_take": [_P, _P],
     "cvz_make_schedule": [_I64, _I32, _I32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                           ctypes.c_uint64, _I32, ctypes.c_uint32, _P],
 }

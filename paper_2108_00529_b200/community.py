@@ -248,13 +248,12 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
 
 
 def export_hierarchy_tsv(a: CommunityAssignment, path) -> None:
-    """C/community.py:284-294: node, label, one column per round."""
-    cols = [np.arange(len(a.label), dtype=np.int64), a.label] + list(a.round_history)
-    table = np.stack(cols, axis=1)
+    """C/community.py:284-294: node, label, one column per round (native
+    multi-threaded formatting)."""
+    from .render import format_table, write_text
     header = "\t".join(["node", "label"] + [f"round{i + 1}" for i in range(len(a.round_history))])
-    with open(path, "w", encoding="utf-8") as fh:
-        fh.write(header + "\n")
-        np.savetxt(fh, table, fmt="%d", delimiter="\t")
+    body = format_table([None, a.label] + list(a.round_history)) if len(a.label) else b""
+    write_text(path, header + "\n", body)
 
 
 # ---- private kernel seams used by the reference's own tests -----------------

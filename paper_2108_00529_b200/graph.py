@@ -179,17 +179,17 @@ def load_edge_list(path) -> Graph:
 
 
 def write_edge_list(g: Graph, path_or_file) -> None:
-    """C/graph.py:100-111: dense ids, stream order, one `u v` per line."""
+    """C/graph.py:100-111: dense ids, stream order, one `u v` per line
+    (native multi-threaded formatting)."""
+    from .render import format_table
+    e = g.edges
+    body = format_table([e[:, 0], e[:, 1]], sep=" ") if len(e) else b""
     own = isinstance(path_or_file, (str, bytes)) or hasattr(path_or_file, "__fspath__")
-    fh = open(path_or_file, "w", encoding="utf-8") if own else path_or_file
-    try:
-        e = g.edges
-        buf = io.StringIO()
-        np.savetxt(buf, e, fmt="%d", delimiter=" ")
-        fh.write(buf.getvalue())
-    finally:
-        if own:
-            fh.close()
+    if own:
+        with open(path_or_file, "wb") as fh:
+            fh.write(body)
+    else:
+        path_or_file.write(body.decode("ascii"))
 
 
 def from_edge_array(edges, node_count=None) -> Graph:

@@ -137,5 +137,7 @@ def sketch_estimate_many(s: CountMinSketch, keys) -> np.ndarray:
 
 
 def dump_tsv(s: CountMinSketch, path) -> None:
-    """C/sketch.py:101-102."""
-    np.savetxt(path, s.table, fmt="%d", delimiter="\t")
+    """C/sketch.py:101-102 (np.savetxt "%d", tab): native formatting."""
+    from .render import format_table, write_text
+    t = np.asarray(s.table, dtype=np.int64)
+    write_text(path, "", format_table(list(np.ascontiguousarray(t.T))))

@@ -124,17 +124,15 @@ def _memcpy_d2d(dst, src_ptr, nbytes):
 
 
 def export_supernodes_tsv(sg: SuperGraph, path) -> None:
-    """C/supergraph.py:79-83."""
-    table = np.stack([np.arange(sg.node_count, dtype=np.int64), sg.community_id, sg.weight], 1)
-    with open(path, "w", encoding="utf-8") as fh:
-        fh.write("supernode\tcommunity\tweight\n")
-        np.savetxt(fh, table, fmt="%d", delimiter="\t")
+    """C/supergraph.py:79-83 (native multi-threaded formatting)."""
+    from .render import format_table, write_text
+    write_text(path, "supernode\tcommunity\tweight\n",
+               format_table([None, sg.community_id, sg.weight]) if sg.node_count else b"")
 
 
 def export_superedges_tsv(sg: SuperGraph, path) -> None:
-    """C/supergraph.py:86-91."""
-    table = np.concatenate([sg.edges, sg.multiplicity[:, None]], axis=1) if sg.edge_count else \
-        np.empty((0, 3), np.int64)
-    with open(path, "w", encoding="utf-8") as fh:
-        fh.write("source\ttarget\tmultiplicity\n")
-        np.savetxt(fh, table, fmt="%d", delimiter="\t")
+    """C/supergraph.py:86-91 (native multi-threaded formatting)."""
+    from .render import format_table, write_text
+    e = sg.edges
+    write_text(path, "source\ttarget\tmultiplicity\n",
+               format_table([e[:, 0], e[:, 1], sg.multiplicity]) if sg.edge_count else b"")

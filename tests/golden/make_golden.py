@@ -257,10 +257,91 @@ def layout_cases():
     return d
 
 
+def _text(s):
+    return np.frombuffer(s.encode("utf-8"), dtype=np.uint8)
+
+
+def writers_cases():
+    """Output formats (C/render.py, C/supergraph.py:79-91,
+    C/community.py:284-294, C/graph.py:100-111, C/sketch.py:101-102,
+    C/cli.py:200-215): the reference's exact text for small inputs."""
+    import io
+    import tempfile
+
+    from commviz.cli import _export_nodes_tsv
+    from commviz.render import ColorAssignment
+    d = {}
+    rng = np.random.default_rng(11)
+    tmp = tempfile.mkdtemp()
+    for i, n in enumerate([1, 7, 40, 300]):
+        pos = rng.normal(size=(n, 2)) * (10.0 ** rng.integers(-4, 4))
+        if n >= 7:
+            pos[0] = [-0.0, -1e-4]          # "-0.000"
+            pos[1] = [0.0005, -0.0005]       # exact ties of the decimal grid
+            pos[2] = [1.0005, 2.5e-3]
+        w = rng.integers(0, 50, size=n).astype(np.int64)
+        alpha = [1.0, 0.5, 2.0, 1.3][i]
+        col = cv.assign_colors(w, alpha=alpha)
+        rad = cv.node_radii(pos, w)
+        ne = 3 * n
+        e = rng.integers(0, n, size=(ne, 2))
+        mult = rng.integers(1, 9, size=ne)
+        k = f"s{i}"
+        d[k + "_pos"], d[k + "_w"], d[k + "_alpha"] = pos, w, np.float64(alpha)
+        d[k + "_classes"], d[k + "_radii"] = col.classes, rad
+        d[k + "_edges"], d[k + "_mult"] = e, mult
+        for tag, kw in (("plain", {}), ("edges", dict(edges=e, multiplicity=mult)),
+                        ("edges1", dict(edges=e))):
+            buf = io.StringIO()
+            cv.export_svg(buf, pos, rad, col, **kw)
+            d[f"{k}_svg_{tag}"] = _text(buf.getvalue())
+    # TSVs over a real pipeline result
+    e = sbm(3, 300, 12, 2000, 0.1)
+    g = cv.from_edge_array(e)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=cv.degree_stats(g).mode_degree),
+                              seed=0, workers=4)
+    s = cv.sketch_new(4, 97, seed=0)
+    cv.accumulate_sizes(s, a.label, g.degree)
+    sg = cv.contract(g, a.label, s)
+    res = cv.layout(sg, cv.LayoutParams(iterations=5))
+    col = cv.assign_colors(sg.weight)
+    d["t_edges"] = e
+    d["t_label"], d["t_hist"] = a.label, np.stack(a.round_history)
+    d["t_table"], d["t_hash_a"], d["t_hash_b"] = s.table, s.hash_a, s.hash_b
+    d["t_sg_edges"], d["t_sg_weight"] = sg.edges, sg.weight
+    d["t_sg_mult"], d["t_sg_comm"] = sg.multiplicity, sg.community_id
+    d["t_pos"] = res.positions
+    d["t_full_pos"] = rng.normal(size=(g.node_count, 2))
+    d["t_full_classes"] = cv.color_full_graph(a.label, sg.community_id, col)
+    files = {
+        "supernodes": lambda p: cv.export_supernodes_tsv(sg, p),
+        "superedges": lambda p: cv.export_superedges_tsv(sg, p),
+        "hierarchy": lambda p: cv.export_hierarchy_tsv(a, p),
+        "edgelist": lambda p: cv.write_edge_list(g, p),
+        "sketch": lambda p: cv.dump_tsv(s, p),
+        "nodes": lambda p: _export_nodes_tsv(p, g, a, sg, col, res),
+        "nodes_full": lambda p: _export_nodes_tsv(
+            p, g, a, sg, col, cv.LayoutResult(d["t_full_pos"], np.zeros(1), 1), full=True),
+    }
+    for name, fn in files.items():
+        path = os.path.join(tmp, name)
+        fn(path)
+        with open(path, encoding="utf-8") as fh:
+            d["f_" + name] = _text(fh.read())
+    full = ColorAssignment(classes=d["t_full_classes"])
+    buf = io.StringIO()
+    cv.export_svg(buf, d["t_full_pos"], np.full(g.node_count, 0.5), full, edges=g.edges)
+    d["f_svg_full"] = _text(buf.getvalue())
+    return d
+
+
 def main():
+    only = sys.argv[1:]
     for name, fn in [("graph", graph_cases), ("community", community_cases),
                      ("sketch", sketch_cases), ("contract", contract_cases),
-                     ("layout", layout_cases)]:
+                     ("layout", layout_cases), ("writers", writers_cases)]:
+        if only and name not in only:
+            continue
         d = fn()
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **d)
