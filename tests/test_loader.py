@@ -157,3 +157,42 @@ def test_parse_edge_list_matches_oracle(tmp_path):
     # non-ASCII goes through the reference loop with the same result
     g = cv.parse_edge_list("# café\n10 20\n20 30\n")
     assert g.edges.tolist() == [[0, 1], [1, 2]]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_run_pipeline_end_to_end(tmp_path):
+    """C/cli.py:120-170 through the drop-in API: file -> artifacts, checked
+    against the oracle run on the same edge list."""
+    import json
+
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import synth
+    e = synth.planted_partition(3000, 30000, 30, seed=2)
+    path = tmp_path / "g.txt"
+    path.write_text("# planted\n" + "\n".join(f"{a + 1000}\t{b + 1000}" for a, b in e) + "\n")
+    cv.warmup_jit()
+    rep, sg, res = cv.run_pipeline(cv.PipelineConfig(input=str(path), outdir=str(tmp_path / "o"),
+                                                     workers=1, iterations=20))
+    n, ee, deg = orc.parse_edge_list(path.read_text())
+    lab, _, hist = orc.detect_communities(n, ee, deg, orc.degree_stats(deg)[0], 10, 0, workers=1)
+    A, B = orc.sketch_params(4, 0)
+    t = np.zeros((4, orc.default_cols(len(ee))), np.int64)
+    orc.sketch_add_many(t, A, B, lab, deg)
+    k, se, w, mult, comm = orc.contract(ee, lab, t, A, B)
+    assert (rep.node_count, rep.edge_count, rep.supernode_count, rep.superedge_count) == (
+        n, len(ee), k, len(se))
+    assert rep.rounds_run == len(hist)
+    assert abs(rep.modularity - orc.modularity(ee, deg, lab)) <= 1e-9
+    out = tmp_path / "o"
+    for f in ("layout.svg", "nodes.tsv", "supernodes.tsv", "superedges.tsv", "hierarchy.tsv",
+              "report.json"):
+        assert (out / f).exists(), f
+    se_f = np.loadtxt(out / "superedges.tsv", dtype=np.int64, skiprows=1).reshape(-1, 3)
+    assert np.array_equal(se_f[:, :2], se) and np.array_equal(se_f[:, 2], mult)
+    sn = np.loadtxt(out / "supernodes.tsv", dtype=np.int64, skiprows=1).reshape(-1, 3)
+    assert np.array_equal(sn[:, 1], comm) and np.array_equal(sn[:, 2], w)
+    assert json.loads((out / "report.json").read_text())["supernode_count"] == k
+    with pytest.raises(cv.PipelineStageError, match="parse"):
+        cv.run_pipeline(cv.PipelineConfig(input=str(tmp_path / "missing.txt"),
+                                          outdir=str(out)))
