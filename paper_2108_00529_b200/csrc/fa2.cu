@@ -697,109 +697,125 @@ __global__ void __launch_bounds__(FB) bh_kernel(const Body *__restrict__ bodies,
     }
 }
 
-// ---- flattened traversal --------------------------------------------------
+// ---- flattened traversal: DFS-preorder 32-byte nodes -----------------------
 // The binary radix tree has "transparent" nodes (the inner halves of a quad
 // cell) that the reference tree does not have and that are always opened.
-// After the COM pass every non-transparent node and every body leaf is
-// written into one flat array whose open/skip links already step over the
-// transparent nodes, so the walk visits exactly the reference's cells and
-// leaves, and a leaf is just a node that always passes the opening test
-// (side2 = -1) -- one uniform loop body, no leaf/cell divergence.
-struct __align__(16) FNode {
-    double x, y, m, side2;  // COM (body position for a leaf), mass, cell side^2
-    int open, skip;         // flat links: first child / DFS successor (-1 = end)
-    int kind;               // 1 cell, 2 depth-40 aggregate, 3 body leaf
-    int aux;                // cell: binary node id; leaf: sorted body index
+// After the COM pass, every quad cell / aggregate and every body leaf is
+// written into one array in DFS preorder (children in key order = the
+// reference's pop order), so a node's first child is the next node and its
+// subtree is a contiguous index range ending before `skip`.  A node is one
+// 32-byte sector: COM (body position for a leaf), mass, skip, and meta =
+// kind | level << 2; a cell's side^2 is a per-level table (the reference
+// halves the root side exactly, C/layout.py:171-208).  Rarely needed ids
+// (binary node / sorted body) live in a parallel aux[] array.
+//
+// Preorder index without a sort: with C_le(f) = #cells whose first body is
+// <= f, a cell covering bodies [f, l] sits at f + C_lt(f) + A (A = its
+// ancestors that share its first body), its DFS successor is l + 1 + C_le(l),
+// and leaf q sits at q + C_le(q).
+struct __align__(32) PNode {
+    double x, y, m;
+    int skip;  // preorder index of the DFS successor, -1 = end
+    int meta;  // kind (1 cell, 2 depth-40 aggregate, 3 body leaf) | level << 2
 };
 
-__device__ __forceinline__ int flat_resolve(int raw, int n, const TNode *__restrict__ nodes,
-                                            const int *__restrict__ left) {
-    while (true) {
-        if (raw == END) return -1;
-        if (raw < 0) return n - 1 + ~raw;
-        if (nodes[raw].kind != 0) return raw;
-        raw = left[raw];
+__global__ void cell_first_hist_kernel(int n, const TNode *__restrict__ nodes,
+                                       const int *__restrict__ first, unsigned *__restrict__ cnt) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n - 1; b += gridDim.x * blockDim.x)
+        if (nodes[b].kind != 0) atomicAdd(cnt + first[b], 1u);
+}
+
+__global__ void preorder_cells_kernel(int n, const TNode *__restrict__ nodes,
+                                      const int *__restrict__ first, const int *__restrict__ last,
+                                      const int *__restrict__ delta,
+                                      const int *__restrict__ parent_int,
+                                      const unsigned *__restrict__ cnt,
+                                      const unsigned *__restrict__ cle, PNode *__restrict__ pn,
+                                      int *__restrict__ aux) {
+    const int total = n + (int)cle[n - 1];
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n - 1; b += gridDim.x * blockDim.x) {
+        const TNode c = nodes[b];
+        if (c.kind == 0) continue;
+        const int f = first[b], l = last[b];
+        int A = 0;
+        for (int a = b == 0 ? -1 : parent_int[b]; a >= 0 && first[a] == f;
+             a = a == 0 ? -1 : parent_int[a])
+            A += nodes[a].kind != 0;
+        const int idx = f + (int)(cle[f] - cnt[f]) + A;
+        const int nxt = l + 1 + (int)cle[l];
+        PNode t;
+        t.x = c.comx;
+        t.y = c.comy;
+        t.m = c.mass;
+        t.skip = nxt >= total ? -1 : nxt;
+        t.meta = c.kind | ((c.kind == 1 ? (delta[b] >> 1) : 0) << 2);
+        pn[idx] = t;
+        aux[idx] = b;
     }
 }
 
-__global__ void flatten_kernel(int n, const TNode *__restrict__ nodes,
-                               const int *__restrict__ left, const int *__restrict__ rc_by_split,
-                               const Body *__restrict__ bodies, FNode *__restrict__ fn) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 2 * n - 1;
-         t += gridDim.x * blockDim.x) {
-        FNode f;
-        if (t < n - 1) {
-            TNode c = nodes[t];
-            if (c.kind == 0) continue;
-            f.x = c.comx;
-            f.y = c.comy;
-            f.m = c.mass;
-            f.side2 = c.kind == 2 ? -1.0 : c.side2;
-            f.open = flat_resolve(c.left, n, nodes, left);
-            f.skip = flat_resolve(c.skip, n, nodes, left);
-            f.kind = c.kind;
-            f.aux = t;
-        } else {
-            int q = t - (n - 1);
-            Body b = bodies[q];
-            f.x = b.x;
-            f.y = b.y;
-            f.m = b.m;
-            f.side2 = -1.0;
-            f.open = -1;
-            f.skip = flat_resolve(q == n - 1 ? END : rc_by_split[q], n, nodes, left);
-            f.kind = 3;
-            f.aux = q;
-        }
-        fn[t] = f;
+__global__ void preorder_leaves_kernel(int n, const Body *__restrict__ bodies,
+                                       const unsigned *__restrict__ cle, PNode *__restrict__ pn,
+                                       int *__restrict__ aux) {
+    const int total = n + (int)cle[n - 1];
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const Body b = bodies[q];
+        const int idx = q + (int)cle[q];
+        PNode t;
+        t.x = b.x;
+        t.y = b.y;
+        t.m = b.m;
+        t.skip = idx + 1 >= total ? -1 : idx + 1;
+        t.meta = 3;
+        pn[idx] = t;
+        aux[idx] = q;
     }
 }
 
-template <int MINB>
-__global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(const Body *__restrict__ bodies, int n,
-                                                     const FNode *__restrict__ fn,
-                                                     const int *__restrict__ first,
-                                                     const int *__restrict__ last,
-                                                     const double *__restrict__ smass,
-                                                     const double *__restrict__ sx,
-                                                     const double *__restrict__ sy, double kr,
-                                                     double theta, double2 *__restrict__ out,
-                                                     const long long *__restrict__ bad,
-                                                     CellRef cr, const int *__restrict__ work,
-                                                     const int *__restrict__ nwork) {
-    if (bad && *bad) return;
-    const double th2 = mul(theta, theta);
-    // work == nullptr: every body; else the sorted bodies this rank owns
-    // (node-sharded layout), still in key order
-    const int count = work ? *nwork : n;
-    for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < count;
-         t0 += gridDim.x * blockDim.x) {
-        const int p = work ? work[t0] : t0;
-        Body me = bodies[p];
-        const long long i = me.orig;
-        const double xi = me.x, yi = me.y, mi = me.m;
-        const double kmi = mul(kr, mi);  // (kr * mi) * mj, the reference's order
-        double fx = 0.0, fy = 0.0;
-        int c = 0;  // root cell (n >= 2)
-        while (c >= 0) {
-            const FNode t = fn[c];
-            double mc = t.m, dx = sub(xi, t.x), dy = sub(yi, t.y);
-            double d2 = add(mul(dx, dx), mul(dy, dy));
-            bool self_out = false;
-            if (t.kind == 2 && p >= first[t.aux] && p <= last[t.aux]) {
+// side^2 per level (C/layout.py:171-208: exact halvings of the root side)
+__device__ __forceinline__ void side2_table(double *tab, const double *bbox) {
+    if (threadIdx.x < MAX_DEPTH) {
+        double side = 2.0 * ldexp(root_geo(bbox).half, -(int)threadIdx.x);
+        tab[threadIdx.x] = mul(side, side);
+    }
+    __syncthreads();
+}
+
+// One node evaluated for body (p, i): the reference's per-body decision and
+// force term.  Returns 1 = accepted (force added, or nothing to add), 0 =
+// open.  Shared by the per-thread and the warp-cooperative walks.
+struct Walker {
+    const Body *__restrict__ bodies;
+    int n;
+    const int *__restrict__ aux;
+    const int *__restrict__ nfirst;
+    const int *__restrict__ nlast;
+    const double *__restrict__ smass;
+    const double *__restrict__ sx;
+    const double *__restrict__ sy;
+    const double *s2tab;
+    double th2;
+    CellRef cr;
+
+    __device__ __forceinline__ bool visit(const PNode &t, int c, int p, int self, long long i,
+                                          double xi, double yi, double mi, double kmi, double &fx,
+                                          double &fy) const {
+        const int kind = t.meta & 3;
+        double mc = t.m, dx = sub(xi, t.x), dy = sub(yi, t.y);
+        double d2 = add(mul(dx, dx), mul(dy, dy));
+        bool self_out = false;
+        if (kind == 2) {
+            const int a = aux[c];
+            if (p >= nfirst[a] && p <= nlast[a]) {
                 // aggregate holding i: the reference tests the single-child
                 // cells above it with the FULL COM (self included) and
-                // approximates there if one passes (C/layout.py:253-261); only
-                // the depth-40 cell itself subtracts self (:247-252)
-                int a = t.aux;
+                // approximates there if one passes (C/layout.py:253-261);
+                // only the depth-40 cell itself subtracts self (:247-252)
                 int ltop = a == 0 ? 0 : (cr.pdelta[a] >> 1) + 1;
                 double s39 = 2.0 * ldexp(root_geo(cr.bbox).half, -(MAX_DEPTH - 1));
                 if (!(ltop <= MAX_DEPTH - 1 && mul(s39, s39) < mul(th2, d2))) {
                     double m2 = sub(smass[a], mi);
-                    if (m2 <= 0.0) {
-                        c = t.skip;
-                        continue;
-                    }
+                    if (m2 <= 0.0) return true;  // nothing left: skip the cell
                     double x2 = sub(sx[a], mul(mi, xi)), y2 = sub(sy[a], mul(mi, yi));
                     mc = m2;
                     dx = sub(xi, x2 / m2);
@@ -808,37 +824,115 @@ __global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(const Body *__restric
                     self_out = true;
                 }
             }
-            // leaves and aggregates carry side2 = -1: always approximated
-            if (t.side2 < mul(th2, d2)) {  // C/layout.py:256-261
-                if (!(t.kind == 3 && t.aux == p)) {  // j == i skipped (:237-238)
-                    double f;
-                    if (d2 >= EPS * EPS) {
-                        f = mul(mul(kmi, mc), inv_d2(d2));
-                    } else {  // coincident: reference jitter (C/layout.py:85-94)
-                        long long key;
-                        if (t.kind == 3) {
-                            key = bodies[t.aux].orig;
-                        } else if (cr.idslot) {
-                            key = (long long)n + ref_cell_id(t.aux, cr.delta, cr.pdelta,
-                                                             cr.idslot, t.kind,
-                                                             root_geo(cr.bbox).half,
-                                                             mul(th2, d2), self_out);
-                        } else {
-                            atomicOr(cr.jflag, 1u);
-                            key = (long long)n + t.aux;
-                        }
-                        double d = separation(dx, dy, i, key);
-                        f = mul(kmi, mc) / mul(d, d);
-                    }
-                    fx = add(fx, mul(f, dx));
-                    fy = add(fy, mul(f, dy));
-                }
-                c = t.skip;
+        }
+        // leaves and aggregates are always approximated (C/layout.py:256-261)
+        if (kind == 1 && !(s2tab[t.meta >> 2] < mul(th2, d2))) return false;
+        if (c == self) return true;  // j == i skipped (:237-238)
+        double f;
+        if (d2 >= EPS * EPS) {
+            f = mul(mul(kmi, mc), inv_d2(d2));
+        } else {  // coincident: reference jitter (C/layout.py:85-94)
+            long long key;
+            if (kind == 3) {
+                key = bodies[aux[c]].orig;
+            } else if (cr.idslot) {
+                key = (long long)n + ref_cell_id(aux[c], cr.delta, cr.pdelta, cr.idslot, kind,
+                                                 root_geo(cr.bbox).half, mul(th2, d2), self_out);
             } else {
-                c = t.open;
+                atomicOr(cr.jflag, 1u);
+                key = (long long)n + aux[c];
             }
+            double d = separation(dx, dy, i, key);
+            f = mul(kmi, mc) / mul(d, d);
+        }
+        fx = add(fx, mul(f, dx));
+        fy = add(fy, mul(f, dy));
+        return true;
+    }
+};
+
+// per-thread walk: one body per thread, bodies in key order
+template <int MINB>
+__global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(Walker w, const PNode *__restrict__ pn,
+                                                     const unsigned *__restrict__ cle, double kr,
+                                                     double theta, double2 *__restrict__ out,
+                                                     const long long *__restrict__ bad,
+                                                     const int *__restrict__ work,
+                                                     const int *__restrict__ nwork) {
+    if (bad && *bad) return;
+    __shared__ double s2tab[MAX_DEPTH];
+    side2_table(s2tab, w.cr.bbox);
+    w.s2tab = s2tab;
+    w.th2 = mul(theta, theta);
+    const int count = work ? *nwork : w.n;
+    for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < count;
+         t0 += gridDim.x * blockDim.x) {
+        const int p = work ? work[t0] : t0;
+        const Body me = w.bodies[p];
+        const long long i = me.orig;
+        const double kmi = mul(kr, me.m);  // (kr * mi) * mj, the reference's order
+        const int self = p + (int)cle[p];
+        double fx = 0.0, fy = 0.0;
+        int c = 0;  // root cell (n >= 2)
+        while (c >= 0) {
+            const PNode t = pn[c];
+            c = w.visit(t, c, p, self, i, me.x, me.y, me.m, kmi, fx, fy) ? t.skip : c + 1;
         }
         out[i] = make_double2(fx, fy);
+    }
+}
+
+// ---- warp-cooperative walk ----------------------------------------------------
+// One warp walks for 32 consecutive (key-ordered) bodies with warp-uniform
+// node loads.  A lane evaluates node c only if it opened every ancestor of
+// c: after accepting c it resumes at c.skip (preorder: c's subtree is
+// [c, skip)).  The warp descends iff some active lane opens, so each lane
+// visits exactly its per-thread traversal in the same order (identical
+// sums).  Wins when a warp's bodies are tightly clustered (full-graph
+// layouts); persistent CTAs pull 32-body groups from a counter.
+template <int MINB>
+__global__ void __launch_bounds__(FB, MINB) bh_warp_kernel(Walker w, const PNode *__restrict__ pn,
+                                                     const unsigned *__restrict__ cle, double kr,
+                                                     double theta, double2 *__restrict__ out,
+                                                     const long long *__restrict__ bad,
+                                                     const int *__restrict__ work,
+                                                     const int *__restrict__ nwork,
+                                                     unsigned *__restrict__ wctr) {
+    if (bad && *bad) return;
+    __shared__ double s2tab[MAX_DEPTH];
+    side2_table(s2tab, w.cr.bbox);
+    w.s2tab = s2tab;
+    w.th2 = mul(theta, theta);
+    const int count = work ? *nwork : w.n;
+    const int lane = lane_id();
+    const int groups = (count + 31) >> 5;
+    while (true) {
+        int grp = 0;
+        if (lane == 0) grp = (int)atomicAdd(wctr, 1u);
+        grp = __shfl_sync(0xffffffffu, grp, 0);
+        if (grp >= groups) break;
+        const int t0 = grp * 32 + lane;
+        const bool valid = t0 < count;
+        const int p = valid ? (work ? work[t0] : t0) : 0;
+        const Body me = w.bodies[p];
+        const long long i = me.orig;
+        const double kmi = mul(kr, me.m);
+        const int self = p + (int)cle[p];
+        double fx = 0.0, fy = 0.0;
+        int resume = valid ? 0 : INT_MAX;  // active while c >= resume
+        int c = 0;
+        while (c >= 0) {
+            const PNode t = pn[c];
+            bool open = false;
+            if (c >= resume) {
+                if (w.visit(t, c, p, self, i, me.x, me.y, me.m, kmi, fx, fy))
+                    resume = t.skip < 0 ? INT_MAX : t.skip;
+                else
+                    open = true;
+            }
+            c = __any_sync(0xffffffffu, open) ? c + 1 : t.skip;
+        }
+        if (valid) out[i] = make_double2(fx, fy);
     }
 }
 
@@ -966,11 +1060,33 @@ __global__ void __launch_bounds__(FB) springs_heavy_kernel(
     }
 }
 
+// Springs of the light rows (<= HEAVY half-edges), one thread per row, in
+// edge order from zero.  Runs on a side stream concurrently with the tree
+// build + repulsion (it needs only positions); forces_kernel adds the sum.
+__global__ void __launch_bounds__(FB) springs_light_kernel(
+    const double2 *__restrict__ pos, const long long *__restrict__ rowptr,
+    const int *__restrict__ col, const double *__restrict__ cw, const int *__restrict__ hidx,
+    int lo, int hi, double2 *__restrict__ spr, const StepScalars *__restrict__ sc) {
+    if (sc && sc->bad) return;
+    for (int u = lo + blockIdx.x * blockDim.x + threadIdx.x; u < hi;
+         u += gridDim.x * blockDim.x) {
+        if (hidx[u] >= 0) continue;  // heavy row: springs_heavy_kernel
+        double2 pu = pos[u];
+        double fx = 0.0, fy = 0.0;
+        for (long long j = rowptr[u]; j < rowptr[u + 1]; ++j) {
+            double2 pv = pos[col[j]];
+            double w = cw[j];
+            fx = add(fx, mul(w, sub(pv.x, pu.x)));
+            fy = add(fy, mul(w, sub(pv.y, pu.y)));
+        }
+        spr[u] = make_double2(fx, fy);
+    }
+}
+
 __global__ void __launch_bounds__(FB) forces_kernel(
     const double2 *__restrict__ pos, const double *__restrict__ mass, int n,
-    const long long *__restrict__ rowptr, const int *__restrict__ col,
-    const double *__restrict__ cw, const int *__restrict__ hidx,
-    const double2 *__restrict__ hsum, const double2 *__restrict__ frep, double gravity,
+    const int *__restrict__ hidx, const double2 *__restrict__ hsum,
+    const double2 *__restrict__ spr, const double2 *__restrict__ frep, double gravity,
     const double2 *__restrict__ prev, double2 *__restrict__ force, double *__restrict__ swing,
     double *__restrict__ part, unsigned *__restrict__ ctr, StepScalars *__restrict__ sc,
     double jt, int lo, double *__restrict__ sums_out) {
@@ -981,19 +1097,11 @@ __global__ void __launch_bounds__(FB) forces_kernel(
         double2 pu = pos[u];
         double2 f = frep[u];
         int h = hidx[u];
-        if (h >= 0) {  // heavy row: warp-summed by springs_heavy_kernel
-            double2 hs = hsum[h];
-            f.x = add(f.x, hs.x);
-            f.y = add(f.y, hs.y);
-        } else {
-            // springs in edge order (CSR rows are stably sorted by edge id)
-            for (long long j = rowptr[u]; j < rowptr[u + 1]; ++j) {
-                double2 pv = pos[col[j]];
-                double w = cw[j];
-                f.x = add(f.x, mul(w, sub(pv.x, pu.x)));
-                f.y = add(f.y, mul(w, sub(pv.y, pu.y)));
-            }
-        }
+        // spring sum of the row (C/layout.py:293-304, edge order within the
+        // row): warp-summed for heavy rows, per-thread for light rows
+        double2 sp = h >= 0 ? hsum[h] : spr[u];
+        f.x = add(f.x, sp.x);
+        f.y = add(f.y, sp.y);
         double mu = mass[u];
         if (gravity > 0) {  // C/layout.py:307-309,370-371
             double gm = mul(-gravity, mu);
@@ -1194,6 +1302,17 @@ size_t sort_bytes(int n, int bits) {
 
 }  // namespace
 
+// CTAs of a persistent kernel: all that fit at once on every SM.
+template <class K>
+unsigned persist_blocks(K kernel) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        CVZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, FB, 0));
+        if (per_sm < 1) per_sm = 1;
+    }
+    return (unsigned)(per_sm * num_sms());
+}
+
 // ---------------------------------------------------------------------------
 // Tree workspace: everything one repulsion evaluation needs, preallocated so
 // an iteration can be captured in a CUDA graph.
@@ -1208,9 +1327,14 @@ struct Tree {
     TNode *nodes;
     DD3 *prefix, *tile_tot;
     int2 *i12;
-    FNode *fn;
+    PNode *pn;
+    int *paux;
+    unsigned *pcnt, *pcle;
+    void *ptmp = nullptr;
+    size_t ptmp_bytes = 0;
     double *bbox = nullptr;
     unsigned *jflag = nullptr;
+    unsigned *wctr = nullptr;  // work counter of the persistent BH walk
     // reference cell numbering (allocated on first use)
     Scratch *scr = nullptr;
     int ne = 0;
@@ -1228,9 +1352,15 @@ struct Tree {
         i12 = sc.alloc<int2>(n > 1 ? n - 1 : 1);
         prefix = sc.alloc<DD3>(n);
         tile_tot = sc.alloc<DD3>((n + TILE_DD - 1) / TILE_DD);
-        fn = sc.alloc<FNode>(2 * n - 1);
+        pn = sc.alloc<PNode>(2 * n - 1);
+        paux = sc.alloc<int>(2 * n - 1);
+        pcnt = sc.alloc<unsigned>(n);
+        pcle = sc.alloc<unsigned>(n);
+        CVZ_CUDA(cub::DeviceScan::InclusiveSum(nullptr, ptmp_bytes, pcnt, pcle, n, sc.stream()));
+        ptmp = sc.alloc<char>(ptmp_bytes);
         jflag = sc.alloc<unsigned>(1);
         CVZ_CUDA(cudaMemsetAsync(jflag, 0, sizeof(unsigned), sc.stream()));
+        wctr = sc.alloc<unsigned>(1);
         khi = sc.alloc<unsigned long long>(n);
         khi2 = sc.alloc<unsigned long long>(n);
         khi3 = sc.alloc<unsigned long long>(n);
@@ -1288,9 +1418,21 @@ struct Tree {
         CVZ_LAUNCH(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix, tile_tot,
                    left, first,
                    last, delta, pdelta, rc_by_split, bbox, smass, sx, sy, nodes);
-        if (flat())
-            CVZ_LAUNCH(flatten_kernel, grid_for(2LL * n, FB, 1, 8), FB, 0, s, n, nodes, left,
-                       rc_by_split, bodies, fn);
+        if (flat()) {
+            CVZ_CUDA(cudaMemsetAsync(pcnt, 0, sizeof(unsigned) * n, s));
+            CVZ_LAUNCH(cell_first_hist_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, nodes,
+                       first, pcnt);
+            {
+                CVZ_REGION("cub_scan:preorder", s);
+                size_t tb = ptmp_bytes;
+                CVZ_CUDA(cub::DeviceScan::InclusiveSum(ptmp, tb, pcnt, pcle, n, s));
+                count_launches(2);
+            }
+            CVZ_LAUNCH(preorder_cells_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, nodes, first,
+                       last, delta, parent_int, pcnt, pcle, pn, paux);
+            CVZ_LAUNCH(preorder_leaves_kernel, grid_for(n, FB, 1, 8), FB, 0, s, n, bodies, pcle,
+                       pn, paux);
+        }
     }
     bool force_flat = false;  // node-sharded runs always walk the flat tree
     bool flat() const { return force_flat || getenv("CVZ_BH_BINARY") == nullptr; }
@@ -1337,11 +1479,24 @@ struct Tree {
     void repulse(double kr, double theta, double2 *out, const long long *bad, bool ids,
                  cudaStream_t s, const int *work = nullptr, const int *nwork = nullptr) {
         CellRef cr{delta, pdelta, ids ? idslot : nullptr, jflag, bbox};
+        CVZ_CUDA(cudaMemsetAsync(wctr, 0, sizeof(unsigned), s));
         if (flat()) {
             static const int minb = getenv("CVZ_BH_MINB") ? atoi(getenv("CVZ_BH_MINB")) : 5;
-#define CVZ_BH_FLAT(B)                                                                     \
-    CVZ_LAUNCH(bh_flat_kernel<B>, blocks_for(n, FB), FB, 0, s, bodies, n, fn, first, last, \
-               smass, sx, sy, kr, theta, out, bad, cr, work, nwork)
+// per-thread walk by default; CVZ_BH_WARP=1 forces the warp-cooperative
+            // walk, CVZ_BH_WARP=auto picks it for large n (clustered full graphs)
+            static const char *wenv = getenv("CVZ_BH_WARP");
+            const bool warp = wenv && (std::string(wenv) == "1" ||
+                                       (std::string(wenv) == "auto" && n >= (1 << 21)));
+            Walker w{bodies, n, paux, first, last, smass, sx, sy, nullptr, 0.0, cr};
+#define CVZ_BH_FLAT(B)                                                                        \
+    do {                                                                                      \
+        if (warp)                                                                             \
+            CVZ_LAUNCH(bh_warp_kernel<B>, persist_blocks(bh_warp_kernel<B>), FB, 0, s, w, pn, \
+                       pcle, kr, theta, out, bad, work, nwork, wctr);                         \
+        else                                                                                  \
+            CVZ_LAUNCH(bh_flat_kernel<B>, blocks_for(n, FB), FB, 0, s, w, pn, pcle, kr, theta,\
+                       out, bad, work, nwork);                                                \
+    } while (0)
             if (minb >= 6)
                 CVZ_BH_FLAT(6);
             else if (minb == 5)
@@ -1459,11 +1614,15 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
     return c;
 }
 
-static void springs_heavy(const double2 *pos, const Csr &c, const StepScalars *sc,
-                          cudaStream_t s) {
-    if (c.nheavy == 0) return;
-    CVZ_LAUNCH(springs_heavy_kernel, blocks_for((long long)c.nheavy * 32, FB), FB, 0, s, pos,
-               c.rowptr, c.col, c.w, c.heavy, c.nheavy, c.hsum, sc);
+// all spring sums of rows [lo, hi) into c.hsum (heavy) / spr (light)
+static void springs(const double2 *pos, const Csr &c, const StepScalars *sc, int lo, int hi,
+                    double2 *spr, cudaStream_t s) {
+    if (c.nheavy > 0)
+        CVZ_LAUNCH(springs_heavy_kernel, blocks_for((long long)c.nheavy * 32, FB), FB, 0, s, pos,
+                   c.rowptr, c.col, c.w, c.heavy, c.nheavy, c.hsum, sc);
+    if (hi > lo)
+        CVZ_LAUNCH(springs_light_kernel, blocks_for(hi - lo, FB), FB, 0, s, pos, c.rowptr, c.col,
+                   c.w, c.hidx, lo, hi, spr, sc);
 }
 
 __global__ void attraction_only_kernel(const double2 *__restrict__ pos, int n,
@@ -1535,7 +1694,7 @@ struct cvz_fa2_shard {
     const double *mass = nullptr;
     cvz::Csr csr;
     cvz::Tree tree;
-    double2 *frep = nullptr, *force = nullptr, *prev = nullptr;
+    double2 *frep = nullptr, *force = nullptr, *prev = nullptr, *spr = nullptr;
     double *swing = nullptr, *fpart = nullptr, *upart = nullptr, *bbox = nullptr;
     unsigned *ctrs = nullptr;
     cvz::StepScalars *scal = nullptr;
@@ -1571,6 +1730,7 @@ int cvz_fa2_shard_create(const double *pos, const double *mass, int64_t n, const
             h->csr = build_csr(reinterpret_cast<const int2 *>(edges), m, n, weight, sign, sc, s,
                                lo, hi);
             h->frep = sc.alloc<double2>(n);
+            h->spr = sc.alloc<double2>(n);
             h->force = sc.alloc<double2>(n);
             h->prev = sc.alloc<double2>(n);
             CVZ_CUDA(cudaMemsetAsync(h->prev, 0, sizeof(double2) * n, s));  // C/layout.py:363
@@ -1629,10 +1789,10 @@ int cvz_fa2_shard_forces(cvz_fa2_shard *h, const double *pos, double *sums_out, 
             }
             h->tree.repulse(P.repulsion, P.theta, h->frep, badp, h->ids, s, h->work, h->nwork);
         }
-        springs_heavy(p2, h->csr, h->scal, s);
-        CVZ_LAUNCH(forces_kernel, h->nb, FB, 0, s, p2, h->mass, h->hi, h->csr.rowptr, h->csr.col,
-                   h->csr.w, h->csr.hidx, h->csr.hsum, h->frep, P.gravity, h->prev, h->force,
-                   h->swing, h->fpart, h->ctrs, h->scal, P.jitter_tolerance, h->lo, sums_out);
+        springs(p2, h->csr, h->scal, h->lo, h->hi, h->spr, s);
+        CVZ_LAUNCH(forces_kernel, h->nb, FB, 0, s, p2, h->mass, h->hi, h->csr.hidx, h->csr.hsum,
+                   h->spr, h->frep, P.gravity, h->prev, h->force, h->swing, h->fpart, h->ctrs,
+                   h->scal, P.jitter_tolerance, h->lo, sums_out);
     });
 }
 
@@ -1740,7 +1900,29 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
         CVZ_CUDA(cudaMemcpyAsync(pos0, p2, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
         CVZ_CUDA(cudaMemcpyAsync(prev0, prev, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
 
+        double2 *spr = sc.alloc<double2>(n);
+        // springs only need positions: they run on a side stream while the
+        // tree is built and walked (fork/join events, captured into the graph)
+        cudaStream_t side;
+        CVZ_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        cudaEvent_t ev_fork, ev_join;
+        CVZ_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        CVZ_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        struct SideGuard {
+            cudaStream_t s;
+            cudaEvent_t a, b;
+            ~SideGuard() {
+                cudaStreamSynchronize(s);
+                cudaStreamDestroy(s);
+                cudaEventDestroy(a);
+                cudaEventDestroy(b);
+            }
+        } side_guard{side, ev_fork, ev_join};
         auto one_iteration = [&](cudaStream_t st, bool ids) {
+            CVZ_CUDA(cudaEventRecord(ev_fork, st));
+            CVZ_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+            springs(p2, csr, scal, 0, N, spr, side);
+            CVZ_CUDA(cudaEventRecord(ev_join, side));
             if (exact) {
                 CVZ_LAUNCH(exact_kernel, blocks_for(n, XT), XT, 0, st, p2, mass, N, P->repulsion,
                            frep, 0, N);
@@ -1749,9 +1931,8 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                 if (ids) tree.build_ids(st);
                 tree.repulse(P->repulsion, P->theta, frep, badp, ids, st);
             }
-            springs_heavy(p2, csr, scal, st);
-            CVZ_LAUNCH(forces_kernel, nb, FB, 0, st, p2, mass, N, csr.rowptr, csr.col, csr.w,
-                       csr.hidx, csr.hsum, frep,
+            CVZ_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+            CVZ_LAUNCH(forces_kernel, nb, FB, 0, st, p2, mass, N, csr.hidx, csr.hsum, spr, frep,
                        P->gravity, prev, force, swing, fpart, ctrs, scal, P->jitter_tolerance, 0,
                        nullptr);
             CVZ_LAUNCH(update_kernel, nb, FB, 0, st, p2, N, force, swing, prev, P->speed_form,
