@@ -140,13 +140,20 @@ int cvz_make_schedule(int64_t m, int workers, int interleave, uint64_t state_hi,
  * node_lab [dev] int64[n] in/out; prev_lab [dev] int64[n] (in, ignored in
  * round 1; then overwritten with the new node_lab); deg_out [dev] int64[n];
  * history_out [dev] int64[n] or NULL; next_edges [dev] int32 capacity
- * max(m_cur, m_orig) pairs.  SYNCHRONISES: *next_m and *changed [host]. */
+ * max(m_cur, m_orig) pairs.  SYNCHRONISES: *next_m and *changed [host].
+ * next_threshold >= 0 (contract stream, identity order, every later round's
+ * threshold == next_threshold): crossing edges whose two communities both
+ * have >= next_threshold + 2 members are no-ops in every later round and are
+ * dropped from next_edges; *next_dead [host] counts them (the reference's
+ * stream still holds them: m_{r+1} = *next_m + dropped so far).  -1 keeps
+ * every crossing edge. */
 int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *order,
                      const int32_t *orig_edges, int64_t m_orig, int64_t n,
                      int64_t threshold, int tie_code, int mode, int round_index,
                      int round_stream, int64_t *node_lab, int64_t *prev_lab,
                      int64_t *deg_out, int64_t *history_out, int32_t *next_edges,
-                     int64_t *next_m, int *changed, void *stream);
+                     int64_t *next_m, int *changed, int64_t next_threshold,
+                     int64_t *next_dead, void *stream);
 
 /* --------------------------------------------------------------- sketch */
 

@@ -52,7 +52,7 @@ SIGNATURES = {
     "cvz_resolve_labels": [_P, _I64, _P, _P],
     "cvz_detect_round": [_P, _I64, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _I32,
                          _P, _P, _P, _P, _P, ctypes.POINTER(_I64),
-                         ctypes.POINTER(ctypes.c_int), _P],
+                         ctypes.POINTER(ctypes.c_int), _I64, ctypes.POINTER(_I64), _P],
     "cvz_sketch_indices": [_P, _P, _I32, _I64, _P, _I64, _P, _P],
     "cvz_sketch_add": [_P, _I32, _I64, _P, _P, _P, _P, _I64, _I32, _P, _P],
     "cvz_sketch_estimate": [_P, _I32, _I64, _P, _P, _P, _I64, _P, _P],

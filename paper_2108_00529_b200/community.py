@@ -224,11 +224,18 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
     changed = ctypes.c_int(0)
     rs = 0 if round_stream == "contract" else 1
     streamed = []  # m_r per executed round (bench roofline bytes; no reference counterpart)
+    # Edges between two saturated communities are no-ops in every later round
+    # once the threshold is pinned at its cap; with the identity order they
+    # can leave the device stream (counted in `dead`, see cvz_detect_round).
+    dead = 0
+    next_dead = nat._I64(0)
     for i in range(1, schedule.rounds + 1):
-        if m_cur == 0:
+        if m_cur + dead == 0:
             break
-        streamed.append(m_cur)
+        streamed.append(m_cur + dead)
         thr = min(schedule.threshold(i), cap)
+        nthr = min(schedule.threshold(i + 1), cap)
+        drop = workers <= 1 and rs == 0 and nthr == cap
         order = _schedule_dev(m_cur, workers, seed + i, interleave)
         snap = T.empty(n, dtype=T.int64, device=dev)
         out = bufs[(i - 1) % 2]
@@ -236,11 +243,12 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
                  int(thr), _TIE_CODES[tie_rule], mcode, i, rs, nat.ptr(node_lab),
                  nat.ptr(prev), nat.ptr(deg), nat.ptr(snap), nat.ptr(out),
                  ctypes.byref(next_m), ctypes.byref(changed),
-                 nat.stream())
+                 int(nthr) if drop else -1, ctypes.byref(next_dead), nat.stream())
         history.append(snap)
         if not changed.value:
             break
         cur, m_cur = out, int(next_m.value)
+        dead += int(next_dead.value)
     a = CommunityAssignment(label=Dual(dev=node_lab), counter_degree=Dual(dev=deg),
                             round_history=_History(history))
     a.stream_edges = streamed

@@ -158,54 +158,162 @@ __global__ void bbox_kernel(const double2 *__restrict__ pos, long long n,
 // ---- keys ------------------------------------------------------------------
 // The reference's descent (C/layout.py:171-208): q = (x >= cx) + 2 (y >= cy),
 // child centre c +- h with h = 0.5 * parent half.  fp64, same op order.
+// Key split for the sort: k32 = digits 0..15 (the radix-sorted part),
+// krest = digits 16..39 (48 bits; only breaks ties inside a level-16 cell).
 __global__ void keys_kernel(const double2 *__restrict__ pos, long long n,
                             const double *__restrict__ bbox,
-                            unsigned long long *__restrict__ khi, unsigned *__restrict__ klo,
+                            unsigned long long *__restrict__ krest, unsigned *__restrict__ k32,
                             unsigned *__restrict__ idx) {
     Geo g = root_geo(bbox);
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         double2 p = pos[i];
         double cx = g.cx, cy = g.cy, h = g.half;
-        unsigned long long hi = 0;
-        unsigned lo = 0;
+        unsigned long long rest = 0;
+        unsigned top = 0;
 #pragma unroll 4
         for (int dpt = 0; dpt < MAX_DEPTH; ++dpt) {
             int qx = p.x >= cx, qy = p.y >= cy;
             unsigned digit = 3u - (unsigned)(qx + 2 * qy);
-            if (dpt < 32)
-                hi = (hi << 2) | digit;
+            if (dpt < 16)
+                top = (top << 2) | digit;
             else
-                lo = (lo << 2) | digit;
+                rest = (rest << 2) | digit;
             h = 0.5 * h;
             cx = qx ? cx + h : cx - h;
             cy = qy ? cy + h : cy - h;
         }
-        khi[i] = hi;
-        klo[i] = lo << 16;  // 8 digits in the top 16 bits
+        k32[i] = top;
+        krest[i] = rest;
         idx[i] = (unsigned)i;
     }
 }
 
-__global__ void gather_hi_kernel(const unsigned long long *__restrict__ khi,
-                                 const unsigned *__restrict__ idx, long long n,
-                                 unsigned long long *__restrict__ out) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        out[i] = khi[idx[i]];
+// ---- tie fix-up after the 32-bit radix sort ------------------------------------
+// The stable sort by k32 leaves runs of bodies sharing their level-16 cell in
+// index order; the full 80-bit order (ties by index, as the stable LSD sort
+// gave) sorts each run by (krest, index).  Runs are rare and short: a thread
+// insertion-sorts runs of <= FIX_SMALL; longer runs go to a list for
+// tie_fixup_long_kernel (one CTA per run).
+constexpr int FIX_SMALL = 32;
+constexpr int FIX_SHARED = 2048;
+
+__device__ __forceinline__ bool key_less(unsigned long long ka, unsigned ia,
+                                         unsigned long long kb, unsigned ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+__global__ void tie_fixup_kernel(const unsigned *__restrict__ k32s, unsigned *__restrict__ idxs,
+                                 const unsigned long long *__restrict__ krest, int n,
+                                 int *__restrict__ long_runs, unsigned *__restrict__ nlong) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned k = k32s[i];
+        if (i + 1 >= n || k32s[i + 1] != k) continue;  // last of its run (or singleton)
+        if (i > 0 && k32s[i - 1] == k) continue;       // not the run head
+        int L = 2;
+        while (i + L < n && L <= FIX_SMALL && k32s[i + L] == k) ++L;
+        if (L > FIX_SMALL) {
+            long_runs[atomicAdd(nlong, 1u)] = i;
+            continue;
+        }
+        unsigned id[FIX_SMALL];
+        unsigned long long kk[FIX_SMALL];
+        for (int j = 0; j < L; ++j) {
+            unsigned x = idxs[i + j];
+            unsigned long long kx = krest[x];
+            int t = j;
+            while (t > 0 && key_less(kx, x, kk[t - 1], id[t - 1])) {
+                kk[t] = kk[t - 1];
+                id[t] = id[t - 1];
+                --t;
+            }
+            kk[t] = kx;
+            id[t] = x;
+        }
+        for (int j = 0; j < L; ++j) idxs[i + j] = id[j];
+    }
+}
+
+// One CTA per long run: bitonic sort of (krest, index) in shared memory, or
+// in global scratch (offset 2*start, disjoint per run) past FIX_SHARED.
+// Runs whose krest are all equal are already in order and are skipped.
+__global__ void __launch_bounds__(1024) tie_fixup_long_kernel(
+    const unsigned *__restrict__ k32s, unsigned *__restrict__ idxs,
+    const unsigned long long *__restrict__ krest, int n, const int *__restrict__ long_runs,
+    const unsigned *__restrict__ nlong, unsigned long long *__restrict__ gk,
+    unsigned *__restrict__ gi) {
+    __shared__ unsigned long long sk[FIX_SHARED];
+    __shared__ unsigned si[FIX_SHARED];
+    __shared__ int s_end;
+    const unsigned runs = *nlong;
+    for (unsigned r = blockIdx.x; r < runs; r += gridDim.x) {
+        const int start = long_runs[r];
+        const unsigned k = k32s[start];
+        if (threadIdx.x == 0) s_end = n;
+        __syncthreads();
+        for (int base = start; base < n; base += blockDim.x) {
+            int j = base + threadIdx.x;
+            if (j < n && k32s[j] != k) atomicMin(&s_end, j);
+            if (__syncthreads_or(j < n && k32s[j] != k)) break;
+        }
+        const int L = s_end - start;
+        const unsigned long long k0 = krest[idxs[start]];
+        bool differ = false;
+        for (int j = threadIdx.x; j < L; j += blockDim.x) differ |= krest[idxs[start + j]] != k0;
+        if (!__syncthreads_or(differ)) continue;
+        int P = 1;
+        while (P < L) P <<= 1;
+        unsigned long long *K = P <= FIX_SHARED ? sk : gk + 2LL * start;
+        unsigned *I = P <= FIX_SHARED ? si : gi + 2LL * start;
+        for (int j = threadIdx.x; j < P; j += blockDim.x) {
+            if (j < L) {
+                unsigned x = idxs[start + j];
+                K[j] = krest[x];
+                I[j] = x;
+            } else {
+                K[j] = ~0ull;
+                I[j] = 0xffffffffu;
+            }
+        }
+        __syncthreads();
+        for (int size = 2; size <= P; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
+                    int a = 2 * t - (t & (stride - 1));
+                    int b = a + stride;
+                    bool up = (a & size) == 0;
+                    unsigned long long ka = K[a], kb = K[b];
+                    unsigned ia = I[a], ib = I[b];
+                    if (key_less(kb, ib, ka, ia) == up) {
+                        K[a] = kb;
+                        K[b] = ka;
+                        I[a] = ib;
+                        I[b] = ia;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int j = threadIdx.x; j < L; j += blockDim.x) idxs[start + j] = I[j];
+        __syncthreads();
+    }
 }
 
 __global__ void gather_bodies_kernel(const double2 *__restrict__ pos,
                                      const double *__restrict__ mass,
                                      const unsigned *__restrict__ idx,
-                                     const unsigned *__restrict__ klo_unsorted, long long n,
-                                     Body *__restrict__ bodies, unsigned *__restrict__ klo) {
+                                     const unsigned *__restrict__ k32s,
+                                     const unsigned long long *__restrict__ krest, long long n,
+                                     Body *__restrict__ bodies, unsigned long long *__restrict__ khi,
+                                     unsigned *__restrict__ klo) {
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
         unsigned i = idx[p];
         double2 q = pos[i];
         bodies[p] = Body{q.x, q.y, mass[i], (int)i, 0};
-        klo[p] = klo_unsorted[i];
+        unsigned long long r = krest[i];
+        khi[p] = ((unsigned long long)k32s[p] << 32) | (r >> 16);  // digits 0..31
+        klo[p] = (unsigned)(r & 0xffffu) << 16;                    // digits 32..39 on top
     }
 }
 
@@ -1318,8 +1426,12 @@ unsigned persist_blocks(K kernel) {
 // an iteration can be captured in a CUDA graph.
 struct Tree {
     int n = 0;
-    unsigned long long *khi, *khi2, *khi3;
-    unsigned *klo, *klo2, *klo3, *idx, *idx2, *idx3;
+    unsigned long long *khi, *khi3;
+    int *long_runs;            // tie fix-up: heads of runs longer than FIX_SMALL
+    unsigned *nlong;
+    unsigned long long *fix_k;  // global bitonic scratch for very long runs
+    unsigned *fix_i;
+    unsigned *klo, *klo2, *klo3, *idx, *idx2;
     Body *bodies;
     int *left, *first, *last, *delta, *parent_int, *parent_leaf, *pdelta, *rc_by_split;
     unsigned *visit;
@@ -1362,14 +1474,12 @@ struct Tree {
         CVZ_CUDA(cudaMemsetAsync(jflag, 0, sizeof(unsigned), sc.stream()));
         wctr = sc.alloc<unsigned>(1);
         khi = sc.alloc<unsigned long long>(n);
-        khi2 = sc.alloc<unsigned long long>(n);
         khi3 = sc.alloc<unsigned long long>(n);
         klo = sc.alloc<unsigned>(n);
         klo2 = sc.alloc<unsigned>(n);
         klo3 = sc.alloc<unsigned>(n);
         idx = sc.alloc<unsigned>(n);
         idx2 = sc.alloc<unsigned>(n);
-        idx3 = sc.alloc<unsigned>(n);
         bodies = sc.alloc<Body>(n);
         int ni = n > 1 ? n - 1 : 1;
         left = sc.alloc<int>(ni);
@@ -1385,7 +1495,11 @@ struct Tree {
         sx = sc.alloc<double>(ni);
         sy = sc.alloc<double>(ni);
         nodes = sc.alloc<TNode>(ni);
-        tmp_bytes = std::max(sort_bytes<unsigned>(n, 32), sort_bytes<unsigned long long>(n, 64));
+        tmp_bytes = sort_bytes<unsigned>(n, 32);
+        long_runs = sc.alloc<int>(n);
+        nlong = sc.alloc<unsigned>(1);
+        fix_k = sc.alloc<unsigned long long>(2LL * n);
+        fix_i = sc.alloc<unsigned>(2LL * n);
         tmp = sc.alloc<char>(tmp_bytes);
     }
     // build from pos + bbox (bbox already on device)
@@ -1394,21 +1508,19 @@ struct Tree {
         unsigned g = grid_for(n, FB, 1, 8);
         CVZ_LAUNCH(keys_kernel, g, FB, 0, s, pos, (long long)n, bbox, khi, klo, idx);
         size_t tb = tmp_bytes;
-        // LSD: low 8 digits first (16 bits), then the high 32 digits (64 bits)
+        // stable sort by the top 16 levels (4 radix passes), then the tie
+        // fix-up orders bodies sharing a level-16 cell by the other 24 levels
         {
-            CVZ_REGION("cub_sort:tree_keys_lo", s);
-            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, klo, klo2, idx, idx2, n, 16, 32, s));
+            CVZ_REGION("cub_sort:tree_keys", s);
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, klo, klo2, idx, idx2, n, 0, 32, s));
         }
-        count_launches(3);
-        CVZ_LAUNCH(gather_hi_kernel, g, FB, 0, s, khi, idx2, (long long)n, khi2);
-        tb = tmp_bytes;
-        {
-            CVZ_REGION("cub_sort:tree_keys_hi", s);
-            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, khi2, khi3, idx2, idx3, n, 0, 64, s));
-        }
-        count_launches(9);
-        CVZ_LAUNCH(gather_bodies_kernel, g, FB, 0, s, pos, mass, idx3, klo, (long long)n, bodies,
-                   klo3);
+        count_launches(5);
+        CVZ_CUDA(cudaMemsetAsync(nlong, 0, sizeof(unsigned), s));
+        CVZ_LAUNCH(tie_fixup_kernel, g, FB, 0, s, klo2, idx2, khi, n, long_runs, nlong);
+        CVZ_LAUNCH(tie_fixup_long_kernel, num_sms(), 1024, 0, s, klo2, idx2, khi, n, long_runs,
+                   nlong, fix_k, fix_i);
+        CVZ_LAUNCH(gather_bodies_kernel, g, FB, 0, s, pos, mass, idx2, klo2, khi, (long long)n,
+                   bodies, khi3, klo3);
         Keys K{khi3, klo3, n};
         CVZ_LAUNCH(karras_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, K, left, first, last, delta,
                    parent_int, parent_leaf, pdelta, rc_by_split);

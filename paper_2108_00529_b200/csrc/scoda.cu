@@ -612,16 +612,24 @@ __global__ void compose_kernel(long long n, const long long *__restrict__ rep,
 constexpr int RITEMS = 16;
 constexpr int RTILE = TB * RITEMS;
 
+// Dead-edge drop (identity order, threshold pinned at its cap): an edge
+// whose two communities both have >= Tn + 2 members is a no-op in every later
+// round -- their seeded counters exceed Tn, so neither end can adopt, be
+// adopted or change (C/community.py:104-120, :258-261), its relabelled ends
+// stay equal to themselves, and sizes only grow.  Such edges are counted
+// (*d_dead) instead of written.  size == nullptr disables the drop.
 __global__ void __launch_bounds__(TB) relabel_compact_kernel(
     const int2 *__restrict__ in, long long m, const long long *__restrict__ map,
     int2 *__restrict__ out, LookbackState st, unsigned long long *__restrict__ d_count,
-    unsigned num_tiles) {
+    unsigned num_tiles, const unsigned *__restrict__ size, long long Tn,
+    unsigned long long *__restrict__ d_dead) {
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_prefix;
     const unsigned tile = acquire_tile(st, &s_tile);
     const long long base = (long long)tile * RTILE;
     int2 e[RITEMS];
     bool keep[RITEMS];
+    unsigned dead = 0;
 #pragma unroll
     for (int j = 0; j < RITEMS; ++j) {
         long long i = base + (long long)j * TB + threadIdx.x;
@@ -631,7 +639,15 @@ __global__ void __launch_bounds__(TB) relabel_compact_kernel(
             int a = (int)__ldg(map + p.x), b = (int)__ldg(map + p.y);
             e[j] = make_int2(a, b);
             keep[j] = a != b;
+            if (keep[j] && size && __ldg(size + a) >= Tn + 2 && __ldg(size + b) >= Tn + 2) {
+                keep[j] = false;
+                ++dead;
+            }
         }
+    }
+    if (size) {
+        for (int o = 16; o > 0; o >>= 1) dead += __shfl_xor_sync(0xffffffffu, dead, o);
+        if (lane_id() == 0 && dead) atomicAdd(d_dead, (unsigned long long)dead);
     }
     // warp ballots -> per (item, warp) counts -> one 64-entry scan by warp 0:
     // two block barriers per tile instead of one block scan per item
@@ -903,7 +919,7 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
                      int tie_code, int mode, int round_index, int round_stream,
                      int64_t *node_lab, int64_t *prev_lab, int64_t *deg_out,
                      int64_t *history_out, int32_t *next_edges, int64_t *next_m, int *changed,
-                     void *stream) {
+                     int64_t next_threshold, int64_t *next_dead, void *stream) {
     return guard([&] {
         CVZ_REQUIRE(n >= 1, CVZ_ERR_VALUE, "detect needs n >= 1");
         CVZ_REQUIRE(tie_code >= 0 && tie_code <= 2, CVZ_ERR_VALUE, "unknown tie rule");
@@ -948,6 +964,7 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
         }
         *changed = hchg;
         *next_m = 0;
+        if (next_dead) *next_dead = 0;
         if (!hchg) return;
         // 5. next stream: contract (:272-278) or restream (:274-276)
         const int2 *src = round_stream == 0 ? cur : reinterpret_cast<const int2 *>(orig_edges);
@@ -957,16 +974,27 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
         if (tiles == 0) tiles = 1;
         auto *status = sc.alloc<unsigned long long>(tiles);
         auto *ctr = sc.alloc<unsigned>(1);
-        auto *dcount = sc.alloc<unsigned long long>(1);
+        auto *dcount = sc.alloc<unsigned long long>(2);
         CVZ_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * tiles, s));
         CVZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
-        CVZ_CUDA(cudaMemsetAsync(dcount, 0, sizeof(unsigned long long), s));
+        CVZ_CUDA(cudaMemsetAsync(dcount, 0, 2 * sizeof(unsigned long long), s));
+        // next round's community sizes (what its seeding computes) for the
+        // dead-edge drop; contract streams only (restream rebuilds each round)
+        unsigned *nsize = nullptr;
+        if (next_threshold >= 0 && round_stream == 0) {
+            nsize = sc.alloc<unsigned>(n);
+            CVZ_CUDA(cudaMemsetAsync(nsize, 0, sizeof(unsigned) * n, s));
+            CVZ_LAUNCH(size_hist_kernel, grid_for(n, TB, 1, 8), TB, 0, s,
+                       reinterpret_cast<const long long *>(node_lab), (long long)n, nsize);
+        }
         CVZ_LAUNCH(relabel_compact_kernel, tiles, TB, 0, s, src, msrc, map,
-                   reinterpret_cast<int2 *>(next_edges), LookbackState{status, ctr}, dcount, tiles);
-        unsigned long long hm = 0;
-        CVZ_CUDA(cudaMemcpyAsync(&hm, dcount, sizeof(hm), cudaMemcpyDeviceToHost, s));
+                   reinterpret_cast<int2 *>(next_edges), LookbackState{status, ctr}, dcount, tiles,
+                   nsize, (long long)next_threshold, dcount + 1);
+        unsigned long long hm[2] = {0, 0};
+        CVZ_CUDA(cudaMemcpyAsync(hm, dcount, sizeof(hm), cudaMemcpyDeviceToHost, s));
         CVZ_CUDA(cudaStreamSynchronize(s));
-        *next_m = (int64_t)hm;
+        *next_m = (int64_t)hm[0];
+        if (next_dead) *next_dead = (int64_t)hm[1];
     });
 }
 

@@ -385,6 +385,22 @@ def test_repulsion_clusters_vs_oracle(cv, orc, seed):
         assert err <= 1e-9 * np.abs(ref).max(), (theta, err / np.abs(ref).max())
 
 
+def test_repulsion_long_tie_runs_vs_oracle(cv, orc):
+    """Thousands of bodies inside one level-16 cell (tiny clouds next to far
+    outliers) exercise the tree sort's tie fix-up: shared-memory runs
+    (<= 2048) and the global bitonic path (> 2048)."""
+    rng = np.random.default_rng(5)
+    for k, spread in ((2000, 1e-6), (5000, 3e-7)):
+        cloud = rng.uniform(0, spread, (k, 2)) + np.array([3.0, -2.0])
+        far = rng.uniform(-500, 500, (40, 2))
+        pos = np.concatenate([cloud, far, cloud[:7]])  # + exact duplicates
+        mass = rng.uniform(1, 5, len(pos))
+        ref = orc.repulsion_forces(pos, mass, 80.0, 0.5)
+        out = cv.repulsion_forces(pos, mass, 80.0, 0.5)
+        scale = np.abs(ref).max()
+        assert np.max(np.abs(out - ref)) <= 1e-9 * scale, k
+
+
 def test_bh_vs_exact_properties(cv):
     # /root/reference/pkg/tests/test_layout.py:110-132 and criterion 4
     rng = np.random.default_rng(3)
