@@ -61,9 +61,16 @@ __device__ __forceinline__ double separation(double &dx, double &dy, long long a
 // with d = sqrt(d2) (C/layout.py:240,260); d*d and d2 differ by <= 1 ulp, so
 // f = kr*mi*mj * (1/d2) agrees to ~1e-15 relative while skipping the fp64
 // sqrt + divide sequences that bound the traversal on the FP64 pipe.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ double inv_d2(double d2) {
-    if (d2 > 1e30) return 1.0 / d2;  // outside the fp32 seed's range
-    double r = (double)__frcp_rn((float)d2);
+    if (d2 > 1e30 || d2 < 1e-30) return 1.0 / d2;  // outside the fp32 seed's range
+    // 2^-22 seed, two Newton steps -> ~2^-88 before the final rounding
+    double r = (double)rcp_approx((float)d2);
     double e = fma(-d2, r, 1.0);
     r = fma(r, e, r);
     e = fma(-d2, r, 1.0);
@@ -959,6 +966,64 @@ struct Walker {
     }
 };
 
+// Rare paths of the walk, out of line so the hot loop stays small; all
+// arguments by value and the running force returned in registers (reference
+// outputs would spill the loop state to the stack).
+// coincident pair / cell closer than COINCIDE_EPS: reference jitter
+// (C/layout.py:85-94) keyed by the body id or the reference cell number
+__device__ __forceinline__ double2 jitter_add(const Body *bodies, int n, const int *aux, CellRef cr,
+                                           double th2, int c, int kind, long long i, double kmi,
+                                           double mc, double dx, double dy, double d2,
+                                           bool self_out, double fx, double fy) {
+    long long key;
+    if (kind == 3) {
+        key = bodies[aux[c]].orig;
+    } else if (cr.idslot) {
+        key = (long long)n + ref_cell_id(aux[c], cr.delta, cr.pdelta, cr.idslot, kind,
+                                         root_geo(cr.bbox).half, mul(th2, d2), self_out);
+    } else {
+        atomicOr(cr.jflag, 1u);
+        key = (long long)n + aux[c];
+    }
+    double d = separation(dx, dy, i, key);
+    double f = mul(kmi, mc) / mul(d, d);
+    return make_double2(add(fx, mul(f, dx)), add(fy, mul(f, dy)));
+}
+
+// Aggregate cell (always approximated).  If it holds body p, the reference
+// tests the single-child cells above it with the FULL COM (self included)
+// and approximates there if one passes (C/layout.py:253-261); only the
+// depth-40 cell itself subtracts self (:247-252), skipping it when nothing
+// is left.
+__device__ __forceinline__ double2 aggregate_add(const Walker w, const PNode t, int c, int p,
+                                              long long i, double xi, double yi, double mi,
+                                              double kmi, double fx, double fy) {
+    const int a = w.aux[c];
+    double mc = t.m, dx = sub(xi, t.x), dy = sub(yi, t.y);
+    double d2 = add(mul(dx, dx), mul(dy, dy));
+    bool self_out = false;
+    if (p >= w.nfirst[a] && p <= w.nlast[a]) {
+        int ltop = a == 0 ? 0 : (w.cr.pdelta[a] >> 1) + 1;
+        double s39 = 2.0 * ldexp(root_geo(w.cr.bbox).half, -(MAX_DEPTH - 1));
+        if (!(ltop <= MAX_DEPTH - 1 && mul(s39, s39) < mul(w.th2, d2))) {
+            double m2 = sub(w.smass[a], mi);
+            if (m2 <= 0.0) return make_double2(fx, fy);
+            double x2 = sub(w.sx[a], mul(mi, xi)), y2 = sub(w.sy[a], mul(mi, yi));
+            mc = m2;
+            dx = sub(xi, x2 / m2);
+            dy = sub(yi, y2 / m2);
+            d2 = add(mul(dx, dx), mul(dy, dy));
+            self_out = true;
+        }
+    }
+    if (d2 >= EPS * EPS) {
+        double f = mul(mul(kmi, mc), inv_d2(d2));
+        return make_double2(add(fx, mul(f, dx)), add(fy, mul(f, dy)));
+    }
+    return jitter_add(w.bodies, w.n, w.aux, w.cr, w.th2, c, 2, i, kmi, mc, dx, dy, d2, self_out,
+                      fx, fy);
+}
+
 // per-thread walk: one body per thread, bodies in key order
 template <int MINB>
 __global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(Walker w, const PNode *__restrict__ pn,
@@ -972,19 +1037,49 @@ __global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(Walker w, const PNode
     side2_table(s2tab, w.cr.bbox);
     w.s2tab = s2tab;
     w.th2 = mul(theta, theta);
+    const double th2 = w.th2;
     const int count = work ? *nwork : w.n;
     for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < count;
          t0 += gridDim.x * blockDim.x) {
         const int p = work ? work[t0] : t0;
         const Body me = w.bodies[p];
         const long long i = me.orig;
-        const double kmi = mul(kr, me.m);  // (kr * mi) * mj, the reference's order
+        const double xi = me.x, yi = me.y, mi = me.m;
+        const double kmi = mul(kr, mi);  // (kr * mi) * mj, the reference's order
         const int self = p + (int)cle[p];
         double fx = 0.0, fy = 0.0;
         int c = 0;  // root cell (n >= 2)
         while (c >= 0) {
             const PNode t = pn[c];
-            c = w.visit(t, c, p, self, i, me.x, me.y, me.m, kmi, fx, fy) ? t.skip : c + 1;
+            const int kind = t.meta & 3;
+            if (kind == 2) {
+                double2 r = aggregate_add(w, t, c, p, i, xi, yi, mi, kmi, fx, fy);
+                fx = r.x;
+                fy = r.y;
+                c = t.skip;
+                continue;
+            }
+            const double dx = sub(xi, t.x), dy = sub(yi, t.y);
+            const double d2 = add(mul(dx, dx), mul(dy, dy));
+            // cells open unless side^2 < theta^2 d^2; leaves are always
+            // approximated (C/layout.py:256-261)
+            if (kind == 1 && !(s2tab[t.meta >> 2] < mul(th2, d2))) {
+                ++c;
+                continue;
+            }
+            if (c != self) {  // j == i skipped (:237-238)
+                if (d2 >= EPS * EPS) {
+                    const double f = mul(mul(kmi, t.m), inv_d2(d2));
+                    fx = add(fx, mul(f, dx));
+                    fy = add(fy, mul(f, dy));
+                } else {
+                    double2 r = jitter_add(w.bodies, w.n, w.aux, w.cr, th2, c, kind, i, kmi, t.m,
+                                           dx, dy, d2, false, fx, fy);
+                    fx = r.x;
+                    fy = r.y;
+                }
+            }
+            c = t.skip;
         }
         out[i] = make_double2(fx, fy);
     }
