@@ -12,6 +12,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <tuple>
 #include <type_traits>
 #include <stdexcept>
@@ -81,6 +82,38 @@ struct ProfScope {
         ::cvz::g_launches.fetch_add(1, std::memory_order_relaxed);      \
         CVZ_CUDA(cudaGetLastError());                                   \
     } while (0)
+
+// Programmatic dependent launch (PDL): the kernel may be scheduled while its
+// stream predecessor drains; it must call griddep_wait() before touching
+// anything the predecessor produces (a no-op when launched without PDL).
+// Used for the chains of small kernels in a layout iteration, where launch
+// gaps are a visible share of each ~10-20 us kernel.  CVZ_NO_PDL disables.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    static const bool on = getenv("CVZ_NO_PDL") == nullptr;
+    return on;
+}
+
+template <class... KArgs, class... Args>
+void pdl_launch(const char *name, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                cudaStream_t s, Args... args) {
+    ProfScope ps(name, s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CVZ_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+#define CVZ_LAUNCH_PDL(kernel, grid, block, smem, stream, ...) \
+    ::cvz::pdl_launch(#kernel, kernel, dim3(grid), dim3(block), (smem), (stream), __VA_ARGS__)
 
 // Cooperative launch (grid-wide barriers inside the kernel): the grid is the
 // number of CTAs that can be co-resident on all SMs.

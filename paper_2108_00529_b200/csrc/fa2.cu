@@ -170,7 +170,15 @@ __global__ void bbox_kernel(const double2 *__restrict__ pos, long long n,
 __global__ void keys_kernel(const double2 *__restrict__ pos, long long n,
                             const double *__restrict__ bbox,
                             unsigned long long *__restrict__ krest, unsigned *__restrict__ k32,
-                            unsigned *__restrict__ idx) {
+                            unsigned *__restrict__ idx, unsigned *__restrict__ zero_n,
+                            unsigned *__restrict__ zero_1) {
+    griddep_wait();
+    // clear this iteration's counters (no memset node: keeps the PDL chain)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && zero_1) *zero_1 = 0;
+    if (zero_n)
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x)
+            zero_n[i] = 0;
     Geo g = root_geo(bbox);
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
@@ -213,6 +221,7 @@ __device__ __forceinline__ bool key_less(unsigned long long ka, unsigned ia,
 __global__ void tie_fixup_kernel(const unsigned *__restrict__ k32s, unsigned *__restrict__ idxs,
                                  const unsigned long long *__restrict__ krest, int n,
                                  int *__restrict__ long_runs, unsigned *__restrict__ nlong) {
+    griddep_wait();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const unsigned k = k32s[i];
         if (i + 1 >= n || k32s[i + 1] != k) continue;  // last of its run (or singleton)
@@ -249,6 +258,7 @@ __global__ void __launch_bounds__(1024) tie_fixup_long_kernel(
     const unsigned long long *__restrict__ krest, int n, const int *__restrict__ long_runs,
     const unsigned *__restrict__ nlong, unsigned long long *__restrict__ gk,
     unsigned *__restrict__ gi) {
+    griddep_wait();
     __shared__ unsigned long long sk[FIX_SHARED];
     __shared__ unsigned si[FIX_SHARED];
     __shared__ int s_end;
@@ -313,6 +323,7 @@ __global__ void gather_bodies_kernel(const double2 *__restrict__ pos,
                                      const unsigned long long *__restrict__ krest, long long n,
                                      Body *__restrict__ bodies, unsigned long long *__restrict__ khi,
                                      unsigned *__restrict__ klo) {
+    griddep_wait();
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n;
          p += (long long)gridDim.x * blockDim.x) {
         unsigned i = idx[p];
@@ -343,6 +354,7 @@ __global__ void karras_kernel(Keys K, int *__restrict__ left, int *__restrict__ 
                               int *__restrict__ last, int *__restrict__ delta_out,
                               int *__restrict__ parent_int, int *__restrict__ parent_leaf,
                               int *__restrict__ pdelta, int *__restrict__ rc_by_split) {
+    griddep_wait();
     const int n = K.n;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
         int d = (K.delta(i, i + 1) - K.delta(i, i - 1)) >= 0 ? 1 : -1;
@@ -447,6 +459,7 @@ __device__ DD3 block_scan_dd3(DD3 v, DD3 *warp_tot, DD3 &block_total) {
 __global__ void __launch_bounds__(FB) dd_tile_scan_kernel(const Body *__restrict__ bodies, int n,
                                                           DD3 *__restrict__ local,
                                                           DD3 *__restrict__ tile_tot) {
+    griddep_wait();
     __shared__ DD3 warp_tot[FB / 32];
     const long long base = (long long)blockIdx.x * TILE_DD + (long long)threadIdx.x * DD_ITEMS;
     DD3 acc{{0, 0}, {0, 0}, {0, 0}};
@@ -485,6 +498,7 @@ __global__ void __launch_bounds__(FB) dd_tile_scan_kernel(const Body *__restrict
 
 // exclusive scan of the tile totals, one CTA
 __global__ void __launch_bounds__(FB) dd_tiles_kernel(DD3 *__restrict__ tile_tot, int tiles) {
+    griddep_wait();
     __shared__ DD3 warp_tot[FB / 32];
     DD3 carry{{0, 0}, {0, 0}, {0, 0}};
     for (int t0 = 0; t0 < tiles; t0 += FB) {
@@ -523,6 +537,7 @@ __global__ void node_sums_kernel(int n, const DD3 *__restrict__ local,
                                  const double *__restrict__ bbox, double *__restrict__ smass,
                                  double *__restrict__ sx, double *__restrict__ sy,
                                  TNode *__restrict__ nodes) {
+    griddep_wait();
     Geo g = root_geo(bbox);
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < n - 1;
          node += gridDim.x * blockDim.x) {
@@ -836,6 +851,7 @@ struct __align__(32) PNode {
 
 __global__ void cell_first_hist_kernel(int n, const TNode *__restrict__ nodes,
                                        const int *__restrict__ first, unsigned *__restrict__ cnt) {
+    griddep_wait();
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n - 1; b += gridDim.x * blockDim.x)
         if (nodes[b].kind != 0) atomicAdd(cnt + first[b], 1u);
 }
@@ -847,6 +863,7 @@ __global__ void preorder_cells_kernel(int n, const TNode *__restrict__ nodes,
                                       const unsigned *__restrict__ cnt,
                                       const unsigned *__restrict__ cle, PNode *__restrict__ pn,
                                       int *__restrict__ aux) {
+    griddep_wait();
     const int total = n + (int)cle[n - 1];
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n - 1; b += gridDim.x * blockDim.x) {
         const TNode c = nodes[b];
@@ -872,6 +889,7 @@ __global__ void preorder_cells_kernel(int n, const TNode *__restrict__ nodes,
 __global__ void preorder_leaves_kernel(int n, const Body *__restrict__ bodies,
                                        const unsigned *__restrict__ cle, PNode *__restrict__ pn,
                                        int *__restrict__ aux) {
+    griddep_wait();
     const int total = n + (int)cle[n - 1];
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
         const Body b = bodies[q];
@@ -1032,6 +1050,7 @@ __global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(Walker w, const PNode
                                                      const long long *__restrict__ bad,
                                                      const int *__restrict__ work,
                                                      const int *__restrict__ nwork) {
+    griddep_wait();
     if (bad && *bad) return;
     __shared__ double s2tab[MAX_DEPTH];
     side2_table(s2tab, w.cr.bbox);
@@ -1242,6 +1261,7 @@ __global__ void __launch_bounds__(FB) springs_heavy_kernel(
     const double2 *__restrict__ pos, const long long *__restrict__ rowptr,
     const int *__restrict__ col, const double *__restrict__ cw, const int *__restrict__ heavy,
     int nheavy, double2 *__restrict__ hsum, const StepScalars *__restrict__ sc) {
+    griddep_wait();
     if (sc && sc->bad) return;
     const int lane = lane_id();
     for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nheavy;
@@ -1270,6 +1290,7 @@ __global__ void __launch_bounds__(FB) springs_light_kernel(
     const double2 *__restrict__ pos, const long long *__restrict__ rowptr,
     const int *__restrict__ col, const double *__restrict__ cw, const int *__restrict__ hidx,
     int lo, int hi, double2 *__restrict__ spr, const StepScalars *__restrict__ sc) {
+    griddep_wait();
     if (sc && sc->bad) return;
     for (int u = lo + blockIdx.x * blockDim.x + threadIdx.x; u < hi;
          u += gridDim.x * blockDim.x) {
@@ -1293,6 +1314,7 @@ __global__ void __launch_bounds__(FB) forces_kernel(
     const double2 *__restrict__ prev, double2 *__restrict__ force, double *__restrict__ swing,
     double *__restrict__ part, unsigned *__restrict__ ctr, StepScalars *__restrict__ sc,
     double jt, int lo, double *__restrict__ sums_out) {
+    griddep_wait();
     if (sc->bad) return;
     double s_sw = 0.0, s_tr = 0.0;
     int u = lo + blockIdx.x * blockDim.x + threadIdx.x;
@@ -1381,6 +1403,7 @@ __global__ void __launch_bounds__(FB) update_kernel(
     double max_step, double *__restrict__ bpart, unsigned *__restrict__ ctr,
     double *__restrict__ bbox, StepScalars *__restrict__ sc, double *__restrict__ disp_hist,
     int lo, double *__restrict__ red_out) {
+    griddep_wait();
     if (sc->bad) return;
     const double speed = sc->speed;
     int u = lo + blockIdx.x * blockDim.x + threadIdx.x;
@@ -1601,7 +1624,8 @@ struct Tree {
     void build(const double2 *pos, const double *mass, const double *bbox_, cudaStream_t s) {
         bbox = const_cast<double *>(bbox_);
         unsigned g = grid_for(n, FB, 1, 8);
-        CVZ_LAUNCH(keys_kernel, g, FB, 0, s, pos, (long long)n, bbox, khi, klo, idx);
+        CVZ_LAUNCH_PDL(keys_kernel, g, FB, 0, s, pos, (long long)n, bbox, khi, klo, idx,
+                       flat() ? pcnt : nullptr, nlong);
         size_t tb = tmp_bytes;
         // stable sort by the top 16 levels (4 radix passes), then the tie
         // fix-up orders bodies sharing a level-16 cell by the other 24 levels
@@ -1610,24 +1634,22 @@ struct Tree {
             CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, klo, klo2, idx, idx2, n, 0, 32, s));
         }
         count_launches(5);
-        CVZ_CUDA(cudaMemsetAsync(nlong, 0, sizeof(unsigned), s));
-        CVZ_LAUNCH(tie_fixup_kernel, g, FB, 0, s, klo2, idx2, khi, n, long_runs, nlong);
-        CVZ_LAUNCH(tie_fixup_long_kernel, num_sms(), 1024, 0, s, klo2, idx2, khi, n, long_runs,
+        CVZ_LAUNCH_PDL(tie_fixup_kernel, g, FB, 0, s, klo2, idx2, khi, n, long_runs, nlong);
+        CVZ_LAUNCH_PDL(tie_fixup_long_kernel, num_sms(), 1024, 0, s, klo2, idx2, khi, n, long_runs,
                    nlong, fix_k, fix_i);
-        CVZ_LAUNCH(gather_bodies_kernel, g, FB, 0, s, pos, mass, idx2, klo2, khi, (long long)n,
+        CVZ_LAUNCH_PDL(gather_bodies_kernel, g, FB, 0, s, pos, mass, idx2, klo2, khi, (long long)n,
                    bodies, khi3, klo3);
         Keys K{khi3, klo3, n};
-        CVZ_LAUNCH(karras_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, K, left, first, last, delta,
+        CVZ_LAUNCH_PDL(karras_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, K, left, first, last, delta,
                    parent_int, parent_leaf, pdelta, rc_by_split);
         const int tiles = (n + TILE_DD - 1) / TILE_DD;
-        CVZ_LAUNCH(dd_tile_scan_kernel, tiles, FB, 0, s, bodies, n, prefix, tile_tot);
-        CVZ_LAUNCH(dd_tiles_kernel, 1, FB, 0, s, tile_tot, tiles);
-        CVZ_LAUNCH(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix, tile_tot,
+        CVZ_LAUNCH_PDL(dd_tile_scan_kernel, tiles, FB, 0, s, bodies, n, prefix, tile_tot);
+        CVZ_LAUNCH_PDL(dd_tiles_kernel, 1, FB, 0, s, tile_tot, tiles);
+        CVZ_LAUNCH_PDL(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix, tile_tot,
                    left, first,
                    last, delta, pdelta, rc_by_split, bbox, smass, sx, sy, nodes);
         if (flat()) {
-            CVZ_CUDA(cudaMemsetAsync(pcnt, 0, sizeof(unsigned) * n, s));
-            CVZ_LAUNCH(cell_first_hist_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, nodes,
+            CVZ_LAUNCH_PDL(cell_first_hist_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, nodes,
                        first, pcnt);
             {
                 CVZ_REGION("cub_scan:preorder", s);
@@ -1635,9 +1657,9 @@ struct Tree {
                 CVZ_CUDA(cub::DeviceScan::InclusiveSum(ptmp, tb, pcnt, pcle, n, s));
                 count_launches(2);
             }
-            CVZ_LAUNCH(preorder_cells_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, nodes, first,
+            CVZ_LAUNCH_PDL(preorder_cells_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, nodes, first,
                        last, delta, parent_int, pcnt, pcle, pn, paux);
-            CVZ_LAUNCH(preorder_leaves_kernel, grid_for(n, FB, 1, 8), FB, 0, s, n, bodies, pcle,
+            CVZ_LAUNCH_PDL(preorder_leaves_kernel, grid_for(n, FB, 1, 8), FB, 0, s, n, bodies, pcle,
                        pn, paux);
         }
     }
@@ -1686,7 +1708,6 @@ struct Tree {
     void repulse(double kr, double theta, double2 *out, const long long *bad, bool ids,
                  cudaStream_t s, const int *work = nullptr, const int *nwork = nullptr) {
         CellRef cr{delta, pdelta, ids ? idslot : nullptr, jflag, bbox};
-        CVZ_CUDA(cudaMemsetAsync(wctr, 0, sizeof(unsigned), s));
         if (flat()) {
             static const int minb = getenv("CVZ_BH_MINB") ? atoi(getenv("CVZ_BH_MINB")) : 5;
 // per-thread walk by default; CVZ_BH_WARP=1 forces the warp-cooperative
@@ -1695,13 +1716,14 @@ struct Tree {
             const bool warp = wenv && (std::string(wenv) == "1" ||
                                        (std::string(wenv) == "auto" && n >= (1 << 21)));
             Walker w{bodies, n, paux, first, last, smass, sx, sy, nullptr, 0.0, cr};
+            if (warp) CVZ_CUDA(cudaMemsetAsync(wctr, 0, sizeof(unsigned), s));
 #define CVZ_BH_FLAT(B)                                                                        \
     do {                                                                                      \
         if (warp)                                                                             \
             CVZ_LAUNCH(bh_warp_kernel<B>, persist_blocks(bh_warp_kernel<B>), FB, 0, s, w, pn, \
                        pcle, kr, theta, out, bad, work, nwork, wctr);                         \
         else                                                                                  \
-            CVZ_LAUNCH(bh_flat_kernel<B>, blocks_for(n, FB), FB, 0, s, w, pn, pcle, kr, theta,\
+            CVZ_LAUNCH_PDL(bh_flat_kernel<B>, blocks_for(n, FB), FB, 0, s, w, pn, pcle, kr, theta,\
                        out, bad, work, nwork);                                                \
     } while (0)
             if (minb >= 6)
@@ -2139,10 +2161,10 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                 tree.repulse(P->repulsion, P->theta, frep, badp, ids, st);
             }
             CVZ_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
-            CVZ_LAUNCH(forces_kernel, nb, FB, 0, st, p2, mass, N, csr.hidx, csr.hsum, spr, frep,
+            CVZ_LAUNCH_PDL(forces_kernel, nb, FB, 0, st, p2, mass, N, csr.hidx, csr.hsum, spr, frep,
                        P->gravity, prev, force, swing, fpart, ctrs, scal, P->jitter_tolerance, 0,
                        nullptr);
-            CVZ_LAUNCH(update_kernel, nb, FB, 0, st, p2, N, force, swing, prev, P->speed_form,
+            CVZ_LAUNCH_PDL(update_kernel, nb, FB, 0, st, p2, N, force, swing, prev, P->speed_form,
                        P->max_step, upart, ctrs + 1, bbox, scal, disp_hist, 0, nullptr);
         };
 

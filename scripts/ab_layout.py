@@ -44,5 +44,5 @@ print(f"{a.config} {'full' if a.full else 'super'} n={obj.node_count} m={obj.edg
       f"pos0={r.positions[0].tolist()}")
 with cv._native.profile() as prof:
     cv.layout(obj, cv.LayoutParams(iterations=10))
-for name, (c, ms) in sorted(prof.kernels.items(), key=lambda kv: -kv[1][1])[:16]:
+for name, (c, ms) in sorted(prof.kernels.items(), key=lambda kv: -kv[1][1])[:int(os.environ.get("AB_TOP", "40"))]:
     print(f"   {ms / c * 1000:8.1f} us/launch  {name}")
