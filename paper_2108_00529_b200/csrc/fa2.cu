@@ -165,13 +165,14 @@ __global__ void bbox_kernel(const double2 *__restrict__ pos, long long n,
 // ---- keys ------------------------------------------------------------------
 // The reference's descent (C/layout.py:171-208): q = (x >= cx) + 2 (y >= cy),
 // child centre c +- h with h = 0.5 * parent half.  fp64, same op order.
-// Key split for the sort: k32 = digits 0..15 (the radix-sorted part),
-// krest = digits 16..39 (48 bits; only breaks ties inside a level-16 cell).
+// Key split for the sort: k32 = digits 0..D-1 (the radix-sorted part, D =
+// top_digits <= 16), krest = digits D..39 (80 - 2D <= 64 bits; only breaks
+// ties between bodies sharing a level-D cell).
 __global__ void keys_kernel(const double2 *__restrict__ pos, long long n,
                             const double *__restrict__ bbox,
                             unsigned long long *__restrict__ krest, unsigned *__restrict__ k32,
                             unsigned *__restrict__ idx, unsigned *__restrict__ zero_n,
-                            unsigned *__restrict__ zero_1) {
+                            unsigned *__restrict__ zero_1, int top_digits) {
     griddep_wait();
     // clear this iteration's counters (no memset node: keeps the PDL chain)
     if (blockIdx.x == 0 && threadIdx.x == 0 && zero_1) *zero_1 = 0;
@@ -190,7 +191,7 @@ __global__ void keys_kernel(const double2 *__restrict__ pos, long long n,
         for (int dpt = 0; dpt < MAX_DEPTH; ++dpt) {
             int qx = p.x >= cx, qy = p.y >= cy;
             unsigned digit = 3u - (unsigned)(qx + 2 * qy);
-            if (dpt < 16)
+            if (dpt < top_digits)
                 top = (top << 2) | digit;
             else
                 rest = (rest << 2) | digit;
@@ -316,25 +317,6 @@ __global__ void __launch_bounds__(1024) tie_fixup_long_kernel(
     }
 }
 
-__global__ void gather_bodies_kernel(const double2 *__restrict__ pos,
-                                     const double *__restrict__ mass,
-                                     const unsigned *__restrict__ idx,
-                                     const unsigned *__restrict__ k32s,
-                                     const unsigned long long *__restrict__ krest, long long n,
-                                     Body *__restrict__ bodies, unsigned long long *__restrict__ khi,
-                                     unsigned *__restrict__ klo) {
-    griddep_wait();
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-         p += (long long)gridDim.x * blockDim.x) {
-        unsigned i = idx[p];
-        double2 q = pos[i];
-        bodies[p] = Body{q.x, q.y, mass[i], (int)i, 0};
-        unsigned long long r = krest[i];
-        khi[p] = ((unsigned long long)k32s[p] << 32) | (r >> 16);  // digits 0..31
-        klo[p] = (unsigned)(r & 0xffffu) << 16;                    // digits 32..39 on top
-    }
-}
-
 // ---- Karras radix tree -----------------------------------------------------
 struct Keys {
     const unsigned long long *hi;
@@ -350,13 +332,12 @@ struct Keys {
     }
 };
 
-__global__ void karras_kernel(Keys K, int *__restrict__ left, int *__restrict__ first,
+__device__ __forceinline__ void karras_body(int bid, int nblk, Keys K, int *__restrict__ left, int *__restrict__ first,
                               int *__restrict__ last, int *__restrict__ delta_out,
                               int *__restrict__ parent_int, int *__restrict__ parent_leaf,
                               int *__restrict__ pdelta, int *__restrict__ rc_by_split) {
-    griddep_wait();
     const int n = K.n;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
+    for (int i = bid * blockDim.x + threadIdx.x; i < n - 1; i += nblk * blockDim.x) {
         int d = (K.delta(i, i + 1) - K.delta(i, i - 1)) >= 0 ? 1 : -1;
         int dmin = K.delta(i, i - d);
         int lmax = 2;
@@ -394,7 +375,7 @@ __global__ void karras_kernel(Keys K, int *__restrict__ left, int *__restrict__ 
             parent_leaf[~rc] = i;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) pdelta[0] = -2;  // root
+    if (bid == 0 && threadIdx.x == 0) pdelta[0] = -2;  // root
 }
 
 // ---- cell sums from double-double prefix sums ----------------------------------
@@ -456,9 +437,14 @@ __device__ DD3 block_scan_dd3(DD3 v, DD3 *warp_tot, DD3 &block_total) {
     return wid ? dd3_add(before, x) : x;
 }
 
-__global__ void __launch_bounds__(FB) dd_tile_scan_kernel(const Body *__restrict__ bodies, int n,
-                                                          DD3 *__restrict__ local,
-                                                          DD3 *__restrict__ tile_tot) {
+// Gather the key-sorted bodies of one tile (bodies, 80-bit keys for karras)
+// and run the tile-local double-double prefix over them in the same CTA.
+__global__ void __launch_bounds__(FB) gather_scan_kernel(
+    const double2 *__restrict__ pos, const double *__restrict__ mass,
+    const unsigned *__restrict__ idx, const unsigned *__restrict__ k32s,
+    const unsigned long long *__restrict__ krest, int n, Body *__restrict__ bodies,
+    unsigned long long *__restrict__ khi, unsigned *__restrict__ klo, DD3 *__restrict__ local,
+    DD3 *__restrict__ tile_tot, int top_digits) {
     griddep_wait();
     __shared__ DD3 warp_tot[FB / 32];
     const long long base = (long long)blockIdx.x * TILE_DD + (long long)threadIdx.x * DD_ITEMS;
@@ -466,11 +452,17 @@ __global__ void __launch_bounds__(FB) dd_tile_scan_kernel(const Body *__restrict
     DD3 item[DD_ITEMS];
 #pragma unroll
     for (int j = 0; j < DD_ITEMS; ++j) {
-        long long i = base + j;
+        long long p = base + j;
         DD3 v{{0, 0}, {0, 0}, {0, 0}};
-        if (i < n) {
-            Body q = bodies[i];
-            v = DD3{DD{q.m, 0.0}, DD{mul(q.m, q.x), 0.0}, DD{mul(q.m, q.y), 0.0}};
+        if (p < n) {
+            unsigned i = idx[p];
+            double2 q = pos[i];
+            double mi = mass[i];
+            bodies[p] = Body{q.x, q.y, mi, (int)i, 0};
+            unsigned long long r = krest[i];
+            khi[p] = ((unsigned long long)k32s[p] << (64 - 2 * top_digits)) | (r >> 16);  // 0..31
+            klo[p] = (unsigned)(r & 0xffffu) << 16;                    // digits 32..39 on top
+            v = DD3{DD{mi, 0.0}, DD{mul(mi, q.x), 0.0}, DD{mul(mi, q.y), 0.0}};
         }
         acc = dd3_add(acc, v);
         item[j] = acc;
@@ -497,8 +489,7 @@ __global__ void __launch_bounds__(FB) dd_tile_scan_kernel(const Body *__restrict
 }
 
 // exclusive scan of the tile totals, one CTA
-__global__ void __launch_bounds__(FB) dd_tiles_kernel(DD3 *__restrict__ tile_tot, int tiles) {
-    griddep_wait();
+__device__ __forceinline__ void dd_tiles_body(DD3 *__restrict__ tile_tot, int tiles) {
     __shared__ DD3 warp_tot[FB / 32];
     DD3 carry{{0, 0}, {0, 0}, {0, 0}};
     for (int t0 = 0; t0 < tiles; t0 += FB) {
@@ -528,6 +519,27 @@ __device__ __forceinline__ DD3 dd_prefix_at(const DD3 *__restrict__ local,
     return dd3_add(tile_off[i / TILE_DD], local[i]);
 }
 
+
+// karras (blocks [0, gridDim.x - 1)) and the tile-total scan (last block) are
+// independent: one launch runs both side by side
+__global__ void __launch_bounds__(FB) karras_tiles_kernel(Keys K, int *__restrict__ left,
+                                                          int *__restrict__ first,
+                                                          int *__restrict__ last,
+                                                          int *__restrict__ delta_out,
+                                                          int *__restrict__ parent_int,
+                                                          int *__restrict__ parent_leaf,
+                                                          int *__restrict__ pdelta,
+                                                          int *__restrict__ rc_by_split,
+                                                          DD3 *__restrict__ tile_tot, int tiles) {
+    griddep_wait();
+    if (blockIdx.x == gridDim.x - 1) {
+        dd_tiles_body(tile_tot, tiles);
+        return;
+    }
+    karras_body(blockIdx.x, gridDim.x - 1, K, left, first, last, delta_out, parent_int,
+                parent_leaf, pdelta, rc_by_split);
+}
+
 __global__ void node_sums_kernel(int n, const DD3 *__restrict__ local,
                                  const DD3 *__restrict__ tile_off,
                                  const int *__restrict__ left, const int *__restrict__ first,
@@ -536,7 +548,7 @@ __global__ void node_sums_kernel(int n, const DD3 *__restrict__ local,
                                  const int *__restrict__ rc_by_split,
                                  const double *__restrict__ bbox, double *__restrict__ smass,
                                  double *__restrict__ sx, double *__restrict__ sy,
-                                 TNode *__restrict__ nodes) {
+                                 TNode *__restrict__ nodes, unsigned *__restrict__ cnt) {
     griddep_wait();
     Geo g = root_geo(bbox);
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < n - 1;
@@ -576,6 +588,7 @@ __global__ void node_sums_kernel(int n, const DD3 *__restrict__ local,
         t.kind = kind;
         t.pad = 0;
         nodes[node] = t;
+        if (cnt && kind != 0) atomicAdd(cnt + f0, 1u);  // preorder: cells per first body
     }
 }
 
@@ -849,23 +862,15 @@ struct __align__(32) PNode {
     int meta;  // kind (1 cell, 2 depth-40 aggregate, 3 body leaf) | level << 2
 };
 
-__global__ void cell_first_hist_kernel(int n, const TNode *__restrict__ nodes,
-                                       const int *__restrict__ first, unsigned *__restrict__ cnt) {
-    griddep_wait();
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n - 1; b += gridDim.x * blockDim.x)
-        if (nodes[b].kind != 0) atomicAdd(cnt + first[b], 1u);
-}
-
-__global__ void preorder_cells_kernel(int n, const TNode *__restrict__ nodes,
+__device__ __forceinline__ void preorder_cells_body(int tid, int nthr, int n, const TNode *__restrict__ nodes,
                                       const int *__restrict__ first, const int *__restrict__ last,
                                       const int *__restrict__ delta,
                                       const int *__restrict__ parent_int,
                                       const unsigned *__restrict__ cnt,
                                       const unsigned *__restrict__ cle, PNode *__restrict__ pn,
                                       int *__restrict__ aux) {
-    griddep_wait();
     const int total = n + (int)cle[n - 1];
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n - 1; b += gridDim.x * blockDim.x) {
+    for (int b = tid; b < n - 1; b += nthr) {
         const TNode c = nodes[b];
         if (c.kind == 0) continue;
         const int f = first[b], l = last[b];
@@ -886,12 +891,11 @@ __global__ void preorder_cells_kernel(int n, const TNode *__restrict__ nodes,
     }
 }
 
-__global__ void preorder_leaves_kernel(int n, const Body *__restrict__ bodies,
+__device__ __forceinline__ void preorder_leaves_body(int tid, int nthr, int n, const Body *__restrict__ bodies,
                                        const unsigned *__restrict__ cle, PNode *__restrict__ pn,
                                        int *__restrict__ aux) {
-    griddep_wait();
     const int total = n + (int)cle[n - 1];
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    for (int q = tid; q < n; q += nthr) {
         const Body b = bodies[q];
         const int idx = q + (int)cle[q];
         PNode t;
@@ -903,6 +907,24 @@ __global__ void preorder_leaves_kernel(int n, const Body *__restrict__ bodies,
         pn[idx] = t;
         aux[idx] = q;
     }
+}
+
+// cells and leaves of the preorder layout in one launch (first half of the
+// grid: cells, second half: leaves)
+__global__ void preorder_kernel(int n, const TNode *__restrict__ nodes,
+                                const int *__restrict__ first, const int *__restrict__ last,
+                                const int *__restrict__ delta, const int *__restrict__ parent_int,
+                                const unsigned *__restrict__ cnt, const unsigned *__restrict__ cle,
+                                const Body *__restrict__ bodies, PNode *__restrict__ pn,
+                                int *__restrict__ aux) {
+    griddep_wait();
+    const int half = gridDim.x / 2;
+    if ((int)blockIdx.x < half)
+        preorder_cells_body(blockIdx.x * blockDim.x + threadIdx.x, half * blockDim.x, n, nodes,
+                            first, last, delta, parent_int, cnt, cle, pn, aux);
+    else
+        preorder_leaves_body((blockIdx.x - half) * blockDim.x + threadIdx.x,
+                             (gridDim.x - half) * blockDim.x, n, bodies, cle, pn, aux);
 }
 
 // side^2 per level (C/layout.py:171-208: exact halvings of the root side)
@@ -1624,43 +1646,46 @@ struct Tree {
     void build(const double2 *pos, const double *mass, const double *bbox_, cudaStream_t s) {
         bbox = const_cast<double *>(bbox_);
         unsigned g = grid_for(n, FB, 1, 8);
+        // radix-sorted levels: 12 (3 passes) measured best for supergraph-sized
+        // n, 16 for multi-million-body full graphs (denser level-12 cells);
+        // CVZ_TREE_TOP overrides (8..16)
+        static const char *tenv = getenv("CVZ_TREE_TOP");
+        const int top_digits =
+            tenv ? std::max(8, std::min(16, atoi(tenv))) : (n < (1 << 21) ? 12 : 16);
         CVZ_LAUNCH_PDL(keys_kernel, g, FB, 0, s, pos, (long long)n, bbox, khi, klo, idx,
-                       flat() ? pcnt : nullptr, nlong);
+                       flat() ? pcnt : nullptr, nlong, top_digits);
         size_t tb = tmp_bytes;
         // stable sort by the top 16 levels (4 radix passes), then the tie
         // fix-up orders bodies sharing a level-16 cell by the other 24 levels
         {
             CVZ_REGION("cub_sort:tree_keys", s);
-            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, klo, klo2, idx, idx2, n, 0, 32, s));
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, klo, klo2, idx, idx2, n, 0,
+                                                     2 * top_digits, s));
         }
-        count_launches(5);
+        count_launches(1 + (2 * top_digits + 7) / 8);
         CVZ_LAUNCH_PDL(tie_fixup_kernel, g, FB, 0, s, klo2, idx2, khi, n, long_runs, nlong);
         CVZ_LAUNCH_PDL(tie_fixup_long_kernel, num_sms(), 1024, 0, s, klo2, idx2, khi, n, long_runs,
                    nlong, fix_k, fix_i);
-        CVZ_LAUNCH_PDL(gather_bodies_kernel, g, FB, 0, s, pos, mass, idx2, klo2, khi, (long long)n,
-                   bodies, khi3, klo3);
-        Keys K{khi3, klo3, n};
-        CVZ_LAUNCH_PDL(karras_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, K, left, first, last, delta,
-                   parent_int, parent_leaf, pdelta, rc_by_split);
         const int tiles = (n + TILE_DD - 1) / TILE_DD;
-        CVZ_LAUNCH_PDL(dd_tile_scan_kernel, tiles, FB, 0, s, bodies, n, prefix, tile_tot);
-        CVZ_LAUNCH_PDL(dd_tiles_kernel, 1, FB, 0, s, tile_tot, tiles);
+        CVZ_LAUNCH_PDL(gather_scan_kernel, tiles, FB, 0, s, pos, mass, idx2, klo2, khi, n, bodies,
+                       khi3, klo3, prefix, tile_tot, top_digits);
+        Keys K{khi3, klo3, n};
+        CVZ_LAUNCH_PDL(karras_tiles_kernel, grid_for(n - 1, FB, 1, 8) + 1, FB, 0, s, K, left,
+                       first, last, delta, parent_int, parent_leaf, pdelta, rc_by_split, tile_tot,
+                       tiles);
         CVZ_LAUNCH_PDL(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix, tile_tot,
-                   left, first,
-                   last, delta, pdelta, rc_by_split, bbox, smass, sx, sy, nodes);
+                       left, first, last, delta, pdelta, rc_by_split, bbox, smass, sx, sy, nodes,
+                       flat() ? pcnt : nullptr);
         if (flat()) {
-            CVZ_LAUNCH_PDL(cell_first_hist_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, nodes,
-                       first, pcnt);
             {
                 CVZ_REGION("cub_scan:preorder", s);
                 size_t tb = ptmp_bytes;
                 CVZ_CUDA(cub::DeviceScan::InclusiveSum(ptmp, tb, pcnt, pcle, n, s));
                 count_launches(2);
             }
-            CVZ_LAUNCH_PDL(preorder_cells_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, nodes, first,
-                       last, delta, parent_int, pcnt, pcle, pn, paux);
-            CVZ_LAUNCH_PDL(preorder_leaves_kernel, grid_for(n, FB, 1, 8), FB, 0, s, n, bodies, pcle,
-                       pn, paux);
+            const unsigned half = grid_for(n, FB, 1, 8);
+            CVZ_LAUNCH_PDL(preorder_kernel, 2 * half, FB, 0, s, n, nodes, first, last, delta,
+                           parent_int, pcnt, pcle, bodies, pn, paux);
         }
     }
     bool force_flat = false;  // node-sharded runs always walk the flat tree

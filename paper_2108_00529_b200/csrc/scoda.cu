@@ -612,6 +612,20 @@ __global__ void compose_kernel(long long n, const long long *__restrict__ rep,
 constexpr int RITEMS = 16;
 constexpr int RTILE = TB * RITEMS;
 
+constexpr long long SAT_BIT = 1LL << 62;
+constexpr long long SAT_MASK = SAT_BIT - 1;
+
+// map[x] = rep[x] | SAT_BIT if rep[x]'s community has >= Tn + 2 members
+__global__ void pack_map_kernel(const long long *__restrict__ rep, long long n,
+                                const unsigned *__restrict__ size, long long Tn,
+                                long long *__restrict__ out) {
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (long long)gridDim.x * blockDim.x) {
+        long long r = rep[x];
+        out[x] = (long long)size[r] >= Tn + 2 ? (r | SAT_BIT) : r;
+    }
+}
+
 // Dead-edge drop (identity order, threshold pinned at its cap): an edge
 // whose two communities both have >= Tn + 2 members is a no-op in every later
 // round -- their seeded counters exceed Tn, so neither end can adopt, be
@@ -636,12 +650,23 @@ __global__ void __launch_bounds__(TB) relabel_compact_kernel(
         keep[j] = false;
         if (i < m) {
             int2 p = __ldg(in + i);
-            int a = (int)__ldg(map + p.x), b = (int)__ldg(map + p.y);
-            e[j] = make_int2(a, b);
-            keep[j] = a != b;
-            if (keep[j] && size && __ldg(size + a) >= Tn + 2 && __ldg(size + b) >= Tn + 2) {
-                keep[j] = false;
-                ++dead;
+            int a = 0, b = 0;
+            if (!size) {
+                a = (int)__ldg(map + p.x);
+                b = (int)__ldg(map + p.y);
+                e[j] = make_int2(a, b);
+                keep[j] = a != b;
+            }
+            if (size) {  // map carries the saturation flag in bit 62 (pack_map_kernel)
+                const long long ma = __ldg(map + p.x), mb = __ldg(map + p.y);
+                a = (int)(ma & SAT_MASK);
+                b = (int)(mb & SAT_MASK);
+                e[j] = make_int2(a, b);
+                keep[j] = a != b;
+                if (keep[j] && (ma & mb & SAT_BIT)) {
+                    keep[j] = false;
+                    ++dead;
+                }
             }
         }
     }
@@ -986,6 +1011,12 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
             CVZ_CUDA(cudaMemsetAsync(nsize, 0, sizeof(unsigned) * n, s));
             CVZ_LAUNCH(size_hist_kernel, grid_for(n, TB, 1, 8), TB, 0, s,
                        reinterpret_cast<const long long *>(node_lab), (long long)n, nsize);
+        }
+        if (nsize) {
+            long long *packed = sc.alloc<long long>(n);
+            CVZ_LAUNCH(pack_map_kernel, grid_for(n, TB, 1, 8), TB, 0, s, map, (long long)n, nsize,
+                       (long long)next_threshold, packed);
+            map = packed;
         }
         CVZ_LAUNCH(relabel_compact_kernel, tiles, TB, 0, s, src, msrc, map,
                    reinterpret_cast<int2 *>(next_edges), LookbackState{status, ctr}, dcount, tiles,
