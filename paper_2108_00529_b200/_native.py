@@ -195,4 +195,13 @@ def to_dev(a, dtype):
 
 
 def to_host(t):
-    return t.detach().cpu().numpy()
+    """Device -> numpy through a pinned (page-locked, allocator-cached) host
+    buffer: DMA at full link speed and no first-touch page faults, so result
+    read-back time is steady (a pageable .cpu() of a 24 MB label array
+    measured 1.5-14 ms)."""
+    t = t.detach()
+    if not t.is_cuda:
+        return t.numpy()
+    out = torch().empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t)
+    return out.numpy()

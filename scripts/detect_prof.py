@@ -13,6 +13,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
 torch.cuda.set_device(0)
 g = cv.from_edge_array(torch.from_numpy(synth.config_graph(cfg)).cuda())
 base = cv.degree_stats(g).mode_degree
+print("mode degree (threshold) =", base)
 for mode in ("deterministic", "fast"):
     for _ in range(2):
         a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1, mode=mode)
