@@ -95,23 +95,52 @@ template <class K>
 __global__ void cross_keys_kernel(const int2 *__restrict__ e, long long m,
                                   const int *__restrict__ dense, int B, K *__restrict__ out,
                                   unsigned long long *__restrict__ count) {
-    long long stride = (long long)gridDim.x * blockDim.x;
-    long long mm = (m + 31) / 32 * 32;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < mm; i += stride) {
-        bool cross = false;
-        K key = 0;
-        if (i < m) {
-            int2 p = __ldg(e + i);
-            int a = __ldg(dense + p.x), b = __ldg(dense + p.y);
-            cross = a != b;
-            int lo = min(a, b), hi = max(a, b);
-            key = ((K)lo << B) | (K)hi;
+    // ITEMS edges per thread per step and one append atomic per block and
+    // step (per-warp atomics on the single counter serialised ~700K warps
+    // at C4)
+    constexpr int ITEMS = 4;
+    __shared__ unsigned s_w[32];
+    __shared__ unsigned long long s_base;
+    const long long stride = (long long)gridDim.x * blockDim.x * ITEMS;
+    const int wid = threadIdx.x >> 5, lane = lane_id();
+    for (long long i0 = (long long)blockIdx.x * blockDim.x * ITEMS; i0 < m; i0 += stride) {
+        bool cross[ITEMS];
+        K key[ITEMS];
+        unsigned mask[ITEMS], mine = 0;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            long long i = i0 + (long long)j * blockDim.x + threadIdx.x;
+            cross[j] = false;
+            key[j] = 0;
+            if (i < m) {
+                int2 p = __ldg(e + i);
+                int a = __ldg(dense + p.x), b = __ldg(dense + p.y);
+                cross[j] = a != b;
+                int lo = min(a, b), hi = max(a, b);
+                key[j] = ((K)lo << B) | (K)hi;
+            }
+            mask[j] = __ballot_sync(0xffffffffu, cross[j]);
+            mine += __popc(mask[j]);
         }
-        unsigned mask = __ballot_sync(0xffffffffu, cross);
-        unsigned long long base = 0;
-        if (lane_id() == 0 && mask) base = atomicAdd(count, (unsigned long long)__popc(mask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (cross) out[base + __popc(mask & ((1u << lane_id()) - 1))] = key;
+        if (lane == 0) s_w[wid] = mine;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned tot = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                unsigned c = s_w[w];
+                s_w[w] = tot;
+                tot += c;
+            }
+            s_base = tot ? atomicAdd(count, (unsigned long long)tot) : 0;
+        }
+        __syncthreads();
+        unsigned long long base = s_base + s_w[wid];
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            if (cross[j]) out[base + __popc(mask[j] & ((1u << lane) - 1))] = key[j];
+            base += __popc(mask[j]);
+        }
+        __syncthreads();
     }
 }
 

@@ -229,9 +229,9 @@ __global__ void events_init_kernel(const int2 *__restrict__ E, long long m,
                                    const int *__restrict__ parent, int *__restrict__ origin,
                                    int *__restrict__ ptr, int *__restrict__ work,
                                    unsigned *__restrict__ nwork) {
-    long long mm = (m + 31) / 32 * 32;
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < mm;
-         k += (long long)gridDim.x * blockDim.x) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long k0 = (long long)blockIdx.x * blockDim.x; k0 < m; k0 += stride) {
+        const long long k = k0 + threadIdx.x;  // block-uniform trip count
         bool pend = false;
         if (k < m) {
             signed char r = role[k];
@@ -248,11 +248,26 @@ __global__ void events_init_kernel(const int2 *__restrict__ E, long long m,
                 }
             }
         }
-        unsigned mask = __ballot_sync(0xffffffffu, pend);
-        unsigned base = 0;
-        if (lane_id() == 0 && mask) base = atomicAdd(nwork, (unsigned)__popc(mask));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (pend) work[base + __popc(mask & ((1u << lane_id()) - 1))] = (int)k;
+        // one worklist atomic per block and sweep (a per-warp atomic on the
+        // single counter serialised ~1M warps in round 1 at C4)
+        __shared__ unsigned s_wcnt[TB / 32], s_base;
+        const unsigned mask = __ballot_sync(0xffffffffu, pend);
+        const int wid = threadIdx.x >> 5;
+        if (lane_id() == 0) s_wcnt[wid] = __popc(mask);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned tot = 0;
+            for (int w = 0; w < TB / 32; ++w) {
+                unsigned c = s_wcnt[w];
+                s_wcnt[w] = tot;
+                tot += c;
+            }
+            s_base = tot ? atomicAdd(nwork, tot) : 0;
+        }
+        __syncthreads();
+        if (pend)
+            work[s_base + s_wcnt[wid] + __popc(mask & ((1u << lane_id()) - 1))] = (int)k;
+        __syncthreads();
     }
 }
 
@@ -271,12 +286,29 @@ __device__ __forceinline__ unsigned ld_count(const unsigned *c) {
     return *reinterpret_cast<const volatile unsigned *>(c);
 }
 
-__device__ __forceinline__ void push_compact(bool keep, int v, unsigned *counter, int *out) {
-    unsigned mask = __ballot_sync(0xffffffffu, keep);
-    unsigned b = 0;
-    if (lane_id() == 0 && mask) b = atomicAdd(counter, (unsigned)__popc(mask));
-    b = __shfl_sync(0xffffffffu, b, 0);
-    if (keep) out[b + __popc(mask & ((1u << lane_id()) - 1))] = v;
+// Worklist compaction with one atomic per block: every thread of the block
+// must call it (block-uniform trip counts).  Per-warp atomics would put
+// ~n/32 serialised updates on one counter for a multi-million worklist.
+__device__ __forceinline__ void push_compact_block(bool keep, int v, unsigned *counter,
+                                                   int *out) {
+    __shared__ unsigned s_w[32];
+    __shared__ unsigned s_base;
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    const int wid = threadIdx.x >> 5;
+    if (lane_id() == 0) s_w[wid] = __popc(mask);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            unsigned c = s_w[w];
+            s_w[w] = tot;
+            tot += c;
+        }
+        s_base = tot ? atomicAdd(counter, tot) : 0;
+    }
+    __syncthreads();
+    if (keep) out[s_base + s_w[wid] + __popc(mask & ((1u << lane_id()) - 1))] = v;
+    __syncthreads();
 }
 
 // event values: origin[k] = node whose initial label event k carries; a
@@ -296,7 +328,7 @@ __global__ void events_coop_kernel(int *__restrict__ wa, int *__restrict__ wb,
         }
         const unsigned start = single ? threadIdx.x : blockIdx.x * blockDim.x + threadIdx.x;
         const unsigned stride = single ? blockDim.x : gridDim.x * blockDim.x;
-        const unsigned cc = (cnt + 31) / 32 * 32;
+        const unsigned cc = (cnt + blockDim.x - 1) / blockDim.x * blockDim.x;
         for (unsigned t = start; t < cc; t += stride) {
             bool keep = false;
             int k = -1;
@@ -311,7 +343,7 @@ __global__ void events_coop_kernel(int *__restrict__ wa, int *__restrict__ wb,
                     keep = true;
                 }
             }
-            push_compact(keep, k, counts + r + 1, nxt);
+            push_compact_block(keep, k, counts + r + 1, nxt);
         }
         if (single)
             __syncthreads();
@@ -341,7 +373,7 @@ __global__ void resolve_coop_kernel(const long long *__restrict__ lab, long long
                                     int *__restrict__ q_a, int *__restrict__ mn_b,
                                     int *__restrict__ q_b, int *__restrict__ bad) {
     cg::grid_group grid = cg::this_grid();
-    const long long nn = (n + 31) / 32 * 32;
+    const long long nn = (n + blockDim.x - 1) / blockDim.x * blockDim.x;
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < nn;
          x += (long long)gridDim.x * blockDim.x) {
         if (x < n) {
@@ -367,7 +399,7 @@ __global__ void resolve_coop_kernel(const long long *__restrict__ lab, long long
             else
                 pend = true;
         }
-        push_compact(pend, (int)x, counts, wa);
+        push_compact_block(pend, (int)x, counts, wa);
     }
     grid.sync();
     int *cur = wa, *nxt = wb;
@@ -383,7 +415,7 @@ __global__ void resolve_coop_kernel(const long long *__restrict__ lab, long long
         }
         const unsigned start = single ? threadIdx.x : blockIdx.x * blockDim.x + threadIdx.x;
         const unsigned stride = single ? blockDim.x : gridDim.x * blockDim.x;
-        const unsigned cc = (cnt + 31) / 32 * 32;
+        const unsigned cc = (cnt + blockDim.x - 1) / blockDim.x * blockDim.x;
         for (unsigned t = start; t < cc; t += stride) {
             bool keep = false;
             int x = -1;
@@ -398,7 +430,7 @@ __global__ void resolve_coop_kernel(const long long *__restrict__ lab, long long
                     keep = true;
                 }
             }
-            push_compact(keep, x, counts + r + 1, nxt);
+            push_compact_block(keep, x, counts + r + 1, nxt);
         }
         if (single)
             __syncthreads();
@@ -605,7 +637,8 @@ __global__ void compose_kernel(long long n, const long long *__restrict__ rep,
         if (check) diff |= prev[x] != v;
         prev[x] = v;
     }
-    if (__any_sync(__activemask(), diff) && lane_id() == 0) atomicExch(changed, 1);
+    // one flag write per block (per-warp atomics on one word serialise)
+    if (__syncthreads_or(diff) && threadIdx.x == 0) atomicExch(changed, 1);
 }
 
 // stable relabel + drop-intra compaction (single pass, decoupled look-back)
