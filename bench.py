@@ -376,13 +376,62 @@ def run_sharded(args, rank, ws, reps=3):
     t1.record()
     torch.cuda.synchronize()
     fa2_ms = barrier_max(t0.elapsed_time(t1), ws)
+    c5 = run_c5(comm, rank, ws)
     return {"scaling": "strong", "ranks": ws, "graph": f"{args.config} seed 0 (same graph on all ranks)",
+            "c5_rmat26_degrees_sketch": c5,
             "ingest_sketch_ms": ing_ms, "ingest_sketch_edges_per_s": len(e) / (ing_ms / 1e3),
             "full_graph_fa2_ms_per_iter": fa2_ms / FULL_ITERS,
             "full_graph_fa2_iters": FULL_ITERS, "n": g.node_count, "m": g.edge_count,
             "note": "edge-sharded ingest+degrees+sketch (all-reduce of int64 degrees and "
                     "sketch counters); node-sharded full-graph ForceAtlas2 incl. CSR build "
                     "(2 all-reduces + 1 all-gather per iteration)"}
+
+
+C5_SCALE = int(os.environ.get("CVZ_C5_SCALE", "26"))
+
+
+def run_c5(comm, rank, ws, reps=3):
+    """BASELINE config C5: R-MAT scale 26 (2^26 nodes, 2^30 edge draws),
+    edge-sharded ingest + degrees + sketch across the ranks.
+    Each rank generates its own slice of the counter-based stream in HBM
+    (cvz_rmat_edges, outside the timed region); the timed region is
+    from_edge_array_sharded (compaction + degrees + all-reduce of 2^26 int64
+    degrees) + accumulate_sizes_sharded (edge-based +1 per endpoint under
+    labels = id // 64, all-reduce of the 4 x 107,375 counters, merge).
+    Device time, max over ranks."""
+    import torch
+
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import sharded as sh
+    from paper_2108_00529_b200 import synth
+    n5, m5 = 1 << C5_SCALE, 16 << C5_SCALE
+    lo, hi = sh.shard_range(m5, rank, ws)
+    e5 = synth.rmat_dev(C5_SCALE, lo, hi - lo, seed=0)
+    labels = torch.arange(n5, dtype=torch.int64, device="cuda") // 64
+
+    def step():
+        g = sh.from_edge_array_sharded(e5, comm, node_count=n5)
+        s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+        sh.accumulate_sizes_sharded(s, labels, g)
+        return g
+
+    g = step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(reps):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = barrier_max(t0.elapsed_time(t1) / reps, ws)
+    out = {"scale": C5_SCALE, "nodes": n5, "edge_draws": m5, "edges_after_self_loops": g.edge_count,
+           "ms": ms, "edges_per_s": m5 / (ms / 1e3),
+           "note": "edge-sharded compaction + degrees + sketch; labels = id // 64 (synthetic "
+                   "communities; the order-dependent community pass is not sharded)"}
+    del e5, labels, g
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------ CPU baseline

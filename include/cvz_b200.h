@@ -291,6 +291,15 @@ int cvz_fa2_shard_destroy(cvz_fa2_shard *h, void *stream);
 int cvz_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                       double low, double range, int64_t count, double *out, void *stream);
 
+/* Synthetic input for BASELINE config C5 (not a reference function): edges
+ * [start, start + count) of a counter-based R-MAT stream (draw l of edge k =
+ * splitmix64(seed * 0x9E3779B97F4A7C15 + 64k + l), top 53 bits; quadrant
+ * thresholds a, a+b, a+b+c), written as int32 pairs to edges_out [dev].
+ * Shard-independent: any split of [0, m) over ranks gives the same stream.
+ * Self-loops are kept (from_edge_array drops them, C/graph.py:117-118). */
+int cvz_rmat_edges(int scale, double a, double b, double c, uint64_t seed, int64_t start,
+                   int64_t count, int32_t *edges_out, void *stream);
+
 /* -------------------------------------------------------------- metrics */
 
 /* C/metrics.py:34-46 modularity ingredients: intra[c] and degsum[c] over

@@ -90,6 +90,7 @@ SIGNATURES = {
     "cvz_format_svg": [_I64, _P, _P, _P, _P, _I32, _I64, _P, _P, _D,
                        ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_I64)],
     "cvz_text_take": [_P, _P],
+    "cvz_rmat_edges": [_I32, _D, _D, _D, ctypes.c_uint64, _I64, _I64, _P, _P],
     "cvz_make_schedule": [_I64, _I32, _I32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                           ctypes.c_uint64, _I32, ctypes.c_uint32, _P],
 }

@@ -62,6 +62,45 @@ __global__ void pcg64_uniform_kernel(unsigned long long shi, unsigned long long 
 }  // namespace
 }  // namespace cvz
 
+namespace cvz {
+namespace {
+
+// Counter-based R-MAT (BASELINE config C5: scale 26, edge factor 16,
+// (a, b, c, d) = (0.57, 0.19, 0.19, 0.05)).  Draw l of edge k
+// is a function of (seed, k, l) only -- splitmix64 of seed * phi + k * 64 +
+// l, top 53 bits as a uniform double -- so every rank generates its own
+// slice of the stream, bit-identical for any number of ranks, and
+// synth.rmat_counter (numpy) reproduces it on the host for the tests.
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__global__ void rmat_kernel(int scale, double a, double ab, double abc,
+                            unsigned long long seed, long long start, long long count,
+                            int2 *__restrict__ out) {
+    const unsigned long long base = seed * 0x9E3779B97F4A7C15ull;
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < count;
+         j += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = (unsigned long long)(start + j);
+        unsigned u = 0, v = 0;
+        for (int l = 0; l < scale; ++l) {
+            double r = (double)(splitmix64(base + k * 64ull + (unsigned long long)l) >> 11) *
+                       0x1.0p-53;
+            unsigned ub = r >= ab;
+            unsigned vb = (r >= a && r < ab) || r >= abc;
+            u = (u << 1) | ub;
+            v = (v << 1) | vb;
+        }
+        out[j] = make_int2((int)u, (int)v);
+    }
+}
+
+}  // namespace
+}  // namespace cvz
+
 using namespace cvz;
 
 extern "C" int cvz_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
@@ -75,5 +114,17 @@ extern "C" int cvz_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t 
                    s, (unsigned long long)state_hi, (unsigned long long)state_lo,
                    (unsigned long long)inc_hi, (unsigned long long)inc_lo, low, range,
                    (long long)count, out);
+    });
+}
+
+extern "C" int cvz_rmat_edges(int scale, double a, double b, double c, uint64_t seed,
+                              int64_t start, int64_t count, int32_t *edges_out, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(scale >= 1 && scale <= 30, CVZ_ERR_VALUE, "R-MAT scale must be in [1, 30]");
+        CVZ_REQUIRE(start >= 0 && count >= 0, CVZ_ERR_VALUE, "bad edge range");
+        if (count == 0) return;
+        CVZ_LAUNCH(rmat_kernel, grid_for(count, 256, 1, 16), 256, 0, as_stream(stream), scale, a,
+                   a + b, a + b + c, (unsigned long long)seed, (long long)start, (long long)count,
+                   reinterpret_cast<int2 *>(edges_out));
     });
 }

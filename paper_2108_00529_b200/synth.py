@@ -82,3 +82,47 @@ def rmat_edges(scale: int, edge_factor: int, seed: int = 0,
         v = (v << 1) | vb
     e = np.stack([u, v], axis=1).astype(np.int32)
     return e[e[:, 0] != e[:, 1]]
+
+
+RMAT_ABCD = (0.57, 0.19, 0.19, 0.05)
+_PHI = np.uint64(0x9E3779B97F4A7C15)
+
+
+def _splitmix64(x):
+    x = x + _PHI
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def rmat_counter(scale: int, start: int, count: int, seed: int = 0,
+                 abcd=RMAT_ABCD) -> np.ndarray:
+    """Edges [start, start + count) of the counter-based R-MAT stream that
+    cvz_rmat_edges generates on the device (self-loops kept), as a (count, 2)
+    int32 array -- the host twin used by the tests."""
+    a, b, c, _ = abcd
+    k = np.arange(start, start + count, dtype=np.uint64)
+    base = np.uint64(seed) * _PHI
+    u = np.zeros(count, dtype=np.int64)
+    v = np.zeros(count, dtype=np.int64)
+    with np.errstate(over="ignore"):
+        for lvl in range(scale):
+            z = _splitmix64(base + k * np.uint64(64) + np.uint64(lvl))
+            r = (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+            ub = (r >= a + b).astype(np.int64)
+            vb = (((r >= a) & (r < a + b)) | (r >= a + b + c)).astype(np.int64)
+            u = (u << 1) | ub
+            v = (v << 1) | vb
+    return np.stack([u, v], axis=1).astype(np.int32)
+
+
+def rmat_dev(scale: int, start: int, count: int, seed: int = 0, abcd=RMAT_ABCD):
+    """Same stream generated in HBM (cvz_rmat_edges): a (count, 2) int32 CUDA
+    tensor -- no host materialisation of a 2^30-edge input."""
+    from . import _native as nat
+    T = nat.torch()
+    out = T.empty((max(count, 1), 2), dtype=T.int32, device=nat.device())
+    a, b, c, _ = abcd
+    nat.call("cvz_rmat_edges", int(scale), float(a), float(b), float(c), int(seed), int(start),
+             int(count), nat.ptr(out), nat.stream())
+    return out[:count]

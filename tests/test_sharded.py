@@ -196,3 +196,32 @@ def test_sharded_matches_single_gpu():
         np.testing.assert_allclose(r["sup_disp"], ref_sup.displacement, rtol=1e-6, atol=1e-9)
     assert np.array_equal(r0["sup_pos"], r1["sup_pos"])
     assert np.array_equal(r0["full_pos"], r1["full_pos"])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_rmat_counter_stream_and_sharded_degrees():
+    """C5 input: the device R-MAT stream equals its numpy twin for any slice
+    (so shards compose), and edge-sharded degrees + sketch over it equal the
+    oracle's np.bincount / node-based sketch (world of 1 here; the 2-rank
+    decomposition is covered above)."""
+    import paper_2108_00529_b200 as cv
+    from oracle import oracle as orc
+    from paper_2108_00529_b200 import synth
+    from paper_2108_00529_b200.sharded import (Comm, accumulate_sizes_sharded,
+                                               from_edge_array_sharded)
+    scale, m = 14, 16 << 14
+    host = synth.rmat_counter(scale, 0, m, seed=3)
+    for lo, hi in ((0, m), (12345, 20000), (m - 7, m)):
+        dev = synth.rmat_dev(scale, lo, hi - lo, seed=3).cpu().numpy()
+        assert np.array_equal(dev, host[lo:hi])
+    g = from_edge_array_sharded(synth.rmat_dev(scale, 0, m, seed=3), Comm(), node_count=1 << scale)
+    n, ee, deg = orc.from_edge_array(host, node_count=1 << scale)
+    assert g.edge_count == len(ee) and np.array_equal(g.degree, deg)
+    labels = np.arange(n, dtype=np.int64) // 64
+    s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    accumulate_sizes_sharded(s, labels, g)
+    A, B = orc.sketch_params(4, 0)
+    t = np.zeros((4, orc.default_cols(len(ee))), np.int64)
+    orc.sketch_add_many(t, A, B, labels, deg)
+    assert np.array_equal(s.table, t)
