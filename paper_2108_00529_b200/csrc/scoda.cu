@@ -41,7 +41,7 @@ namespace {
 
 constexpr int TB = 256;
 // fast mode: edges in flight <= m / FAST_WINDOW_DIV
-constexpr long long FAST_WINDOW_DIV = 64;
+constexpr long long FAST_WINDOW_DIV = 128;
 
 struct MaxOp {
     __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }

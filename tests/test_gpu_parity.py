@@ -215,16 +215,19 @@ def test_fast_mode_within_tolerance(cv, orc, name):
             qs.append(orc.modularity(ee, deg, lab))
             ks.append(len(np.unique(lab)))
             ts.append(_top10(lab))
-    fast = cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1, mode="fast")
-    q_fast = orc.modularity(g.edges, g.degree, fast.label)
+    # the racy pass is a random variable: gate the median of three runs
+    # ("tested statistically"), every run must keep the label invariant
+    runs = [cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1, mode="fast")
+            for _ in range(3)]
+    q_fast = float(np.median([orc.modularity(g.edges, g.degree, f.label) for f in runs]))
     assert min(qs) - 0.02 <= q_fast <= max(qs) + 0.02, (q_fast, min(qs), max(qs))
-    kf = fast.community_count
+    kf = float(np.median([f.community_count for f in runs]))
     assert 0.95 * min(ks) <= kf <= 1.05 * max(ks), (kf, min(ks), max(ks))
-    t = _top10(fast.label)
+    t = float(np.median([_top10(f.label) for f in runs]))
     assert min(ts) - 0.02 <= t <= max(ts) + 0.02, (t, min(ts), max(ts))
-    # every label is one of its own members (C/community.py:123-161 invariant)
-    lab = fast.label
-    assert np.all(lab[lab] == lab)
+    for f in runs:  # every label is one of its own members (C/community.py:123-161)
+        lab = f.label
+        assert np.all(lab[lab] == lab)
 
 
 def test_gpu_modularity_matches_oracle(cv, orc):
