@@ -28,6 +28,13 @@ __device__ __forceinline__ unsigned long long key_mod_p(long long x) {
     return (unsigned long long)r;
 }
 
+// y mod cols for y < 2^32 without a hardware divide: Lemire's fastmod with
+// M = floor((2^64 - 1) / cols) + 1 (exact for 32-bit y and cols).
+__device__ __forceinline__ unsigned fast_mod(unsigned y, unsigned cols) {
+    const unsigned long long M = 0xFFFFFFFFFFFFFFFFull / cols + 1;  // hoisted: cols is uniform
+    return (unsigned)__umul64hi(M * (unsigned long long)y, (unsigned long long)cols);
+}
+
 // ((a*x + b) mod p) mod cols with a, x < 2^31, b < 2^31: y < 2^62 + 2^31.
 __device__ __forceinline__ unsigned hash_col(unsigned long long a, unsigned long long b,
                                              unsigned long long xm, unsigned cols) {
@@ -35,7 +42,7 @@ __device__ __forceinline__ unsigned hash_col(unsigned long long a, unsigned long
     y = (y & P31) + (y >> 31);  // < 2^31 + 2^32
     y = (y & P31) + (y >> 31);  // < 2^31 + 2
     if (y >= P31) y -= P31;
-    return (unsigned)y % cols;
+    return fast_mod((unsigned)y, cols);
 }
 
 __global__ void indices_kernel(const long long *__restrict__ ha, const long long *__restrict__ hb,
@@ -145,10 +152,11 @@ __global__ void add_staged_kernel(unsigned long long *__restrict__ partial,
         unsigned long long amt = 0;
         if (valid) src.get(j, key, amt);
         unsigned long long xm = valid ? key_mod_p(key) : 0;
-        for (int r = 0; r < rows; ++r) {
-            unsigned c = valid ? hash_col(s_a[r], s_b[r], xm, cols) : 0;
-            agg_add<true>(sh + (size_t)r * cols, c, amt, valid && amt != 0);
-        }
+        // shared-memory atomics are cheap and collisions inside a warp are
+        // rare (6,500+ columns): no match_any aggregation on this path
+        if (valid && amt != 0)
+            for (int r = 0; r < rows; ++r)
+                atomicAdd(sh + (size_t)r * cols + hash_col(s_a[r], s_b[r], xm, cols), amt);
     }
     __syncthreads();
     // plain coalesced store of this CTA's partial table; reduce_partials sums
