@@ -558,3 +558,41 @@ def test_device_init_positions_bit_exact(cv, orc, n, seed):
     from paper_2108_00529_b200.layout import _init_positions_dev
     dev = _init_positions_dev(n, seed).cpu().numpy()
     assert np.array_equal(dev, orc.init_positions(n, seed))
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_headline_pipeline_bit_exact(cv, orc, name):
+    """The bench workload itself (BASELINE configs[2..3]: 685K/7.6M and the
+    3M/34M headline graph): degrees, deterministic labels / counters /
+    per-round history, sketch table and every SuperGraph array bit-exact vs
+    the oracle; 5 supergraph layout iterations within the layout gate."""
+    from paper_2108_00529_b200 import synth
+    e = synth.config_graph(name)
+    g = cv.from_edge_array(e)
+    n, ee, deg = orc.from_edge_array(e)
+    assert g.node_count == n and np.array_equal(g.degree, deg)
+    base = orc.degree_stats(deg)[0]
+    ref_lab, ref_cnt, ref_hist = orc.detect_communities(n, ee, deg, base, 10, 0, workers=1)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+    assert np.array_equal(a.label, ref_lab)
+    assert np.array_equal(a.counter_degree, ref_cnt)
+    assert len(a.round_history) == len(ref_hist)
+    for x, y in zip(a.round_history, ref_hist):
+        assert np.array_equal(x, y)
+    s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    cv.accumulate_sizes(s, a, g)
+    A, B = orc.sketch_params(4, 0)
+    t = np.zeros((4, orc.default_cols(len(ee))), np.int64)
+    orc.sketch_add_many(t, A, B, ref_lab, deg)
+    assert np.array_equal(s.table, t)
+    sg = cv.contract(g, a, s)
+    k, se, w, mult, comm = orc.contract(ee, ref_lab, t, A, B)
+    assert sg.node_count == k
+    assert np.array_equal(sg.edges, se) and np.array_equal(sg.multiplicity, mult)
+    assert np.array_equal(sg.weight, w) and np.array_equal(sg.community_id, comm)
+    res = cv.layout(sg, cv.LayoutParams(iterations=5))
+    mass, ew = orc.masses_supergraph(w, mult)
+    pos, disp = orc.layout(k, mass, se, ew, iterations=5)
+    diam = np.hypot(*(pos.max(0) - pos.min(0)))
+    assert np.max(np.abs(res.positions - pos)) <= 1e-7 * diam
+    np.testing.assert_allclose(res.displacement, disp, rtol=1e-9, atol=1e-9)
