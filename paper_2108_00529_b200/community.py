@@ -198,7 +198,11 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
     """Up to schedule.rounds GPU streaming passes (C/community.py:220-281).
 
     mode="deterministic" (default) reproduces the reference bit-exactly;
-    mode="fast" is the racy single-pass kernel (tolerance-gated)."""
+    mode="fast" runs the racy one-thread-per-edge pass (tolerance-gated) in
+    the first round, where nearly every merge happens; later rounds only see
+    the few communities still below the threshold and run the deterministic
+    pass, so they stop as soon as nothing changes (the racy pass never lets
+    labels settle and would run every scheduled round)."""
     if g.edge_count == 0:
         raise ValueError("cannot detect communities in an empty graph")
     if round_stream not in ("contract", "restream"):
@@ -240,7 +244,8 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
         snap = T.empty(n, dtype=T.int64, device=dev)
         out = bufs[(i - 1) % 2]
         nat.call("cvz_detect_round", nat.ptr(cur), m_cur, nat.ptr(order), nat.ptr(orig), m, n,
-                 int(thr), _TIE_CODES[tie_rule], mcode, i, rs, nat.ptr(node_lab),
+                 int(thr), _TIE_CODES[tie_rule], mcode if i == 1 else nat.DETERMINISTIC, i, rs,
+                 nat.ptr(node_lab),
                  nat.ptr(prev), nat.ptr(deg), nat.ptr(snap), nat.ptr(out),
                  ctypes.byref(next_m), ctypes.byref(changed),
                  int(nthr) if drop else -1, ctypes.byref(next_dead), nat.stream())

@@ -625,17 +625,38 @@ __global__ void seed_counters_kernel(const unsigned *__restrict__ size, long lon
     }
 }
 
+// 4 nodes per thread, loads issued before the dependent rep[] gathers: the
+// kernel is gather-latency-bound (one node per thread left ~470 GB/s)
+constexpr int CITEMS = 4;
 __global__ void compose_kernel(long long n, const long long *__restrict__ rep,
                                long long *__restrict__ node_lab, long long *__restrict__ prev,
                                long long *__restrict__ hist, int check, int *__restrict__ changed) {
     bool diff = false;
-    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
-         x += (long long)gridDim.x * blockDim.x) {
-        long long v = rep[node_lab[x]];
-        node_lab[x] = v;
-        if (hist) hist[x] = v;
-        if (check) diff |= prev[x] != v;
-        prev[x] = v;
+    const long long stride = (long long)gridDim.x * blockDim.x * CITEMS;
+    for (long long x0 = (long long)blockIdx.x * blockDim.x * CITEMS + threadIdx.x; x0 < n;
+         x0 += stride) {
+        long long l[CITEMS], v[CITEMS], pv[CITEMS];
+#pragma unroll
+        for (int j = 0; j < CITEMS; ++j) {
+            long long x = x0 + (long long)j * blockDim.x;
+            l[j] = x < n ? node_lab[x] : 0;
+            pv[j] = (check && x < n) ? prev[x] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < CITEMS; ++j) {
+            long long x = x0 + (long long)j * blockDim.x;
+            v[j] = x < n ? rep[l[j]] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < CITEMS; ++j) {
+            long long x = x0 + (long long)j * blockDim.x;
+            if (x < n) {
+                node_lab[x] = v[j];
+                if (hist) hist[x] = v[j];
+                if (check) diff |= pv[j] != v[j];
+                prev[x] = v[j];
+            }
+        }
     }
     // one flag write per block (per-warp atomics on one word serialise)
     if (__syncthreads_or(diff) && threadIdx.x == 0) atomicExch(changed, 1);
@@ -1011,7 +1032,7 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
         // 4. compose + history + early-stop test (:266-269)
         int *dchg = sc.alloc<int>(1);
         CVZ_CUDA(cudaMemsetAsync(dchg, 0, sizeof(int), s));
-        CVZ_LAUNCH(compose_kernel, blocks_for(n, TB), TB, 0, s, (long long)n,
+        CVZ_LAUNCH(compose_kernel, grid_for(n, TB, CITEMS, 8), TB, 0, s, (long long)n,
                    reinterpret_cast<const long long *>(rep), reinterpret_cast<long long *>(node_lab),
                    reinterpret_cast<long long *>(prev_lab),
                    reinterpret_cast<long long *>(history_out), round_index > 1 ? 1 : 0, dchg);

@@ -14,7 +14,8 @@ torch.cuda.set_device(0)
 g = cv.from_edge_array(torch.from_numpy(synth.config_graph(cfg)).cuda())
 base = cv.degree_stats(g).mode_degree
 print("mode degree (threshold) =", base)
-for mode in ("deterministic", "fast"):
+MODES = sys.argv[2].split(",") if len(sys.argv) > 2 else ["deterministic", "fast"]
+for mode in MODES:
     for _ in range(2):
         a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1, mode=mode)
     torch.cuda.synchronize()
