@@ -151,6 +151,9 @@ __global__ void seg_bounds_kernel(const unsigned *__restrict__ key, long long ns
     }
 }
 
+// 4 slots per thread with the seg_start / d0 gathers issued together: the
+// per-slot chain (key -> seg_start[key] -> store) is gather-latency-bound
+constexpr int SCITEMS = 4;
 template <class CT>
 __global__ void slot_counter_kernel(const unsigned *__restrict__ key,
                                     const unsigned *__restrict__ val, long long ns, unsigned n,
@@ -158,17 +161,35 @@ __global__ void slot_counter_kernel(const unsigned *__restrict__ key,
                                     const long long *__restrict__ d0, long long T,
                                     CT *__restrict__ cval) {
     const CT big = (CT)(T + 1);  // > T: marks sentinel slots inactive
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ns;
-         i += (long long)gridDim.x * blockDim.x) {
-        unsigned x = key[i], s = val[i];
-        if (x >= n) {
-            cval[s] = big;
-            continue;
+    const long long stride = (long long)gridDim.x * blockDim.x * SCITEMS;
+    for (long long i0 = (long long)blockIdx.x * blockDim.x * SCITEMS + threadIdx.x; i0 < ns;
+         i0 += stride) {
+        unsigned x[SCITEMS], sv[SCITEMS];
+        int st[SCITEMS];
+        long long d[SCITEMS];
+#pragma unroll
+        for (int j = 0; j < SCITEMS; ++j) {
+            long long i = i0 + (long long)j * blockDim.x;
+            x[j] = i < ns ? key[i] : n;
+            sv[j] = i < ns ? val[i] : 0u;
         }
-        long long r = i - seg_start[x] + 1;
-        long long d = d0 ? d0[x] : 0;
-        long long c = min(d + r, T + 1);  // d <= T here (larger seeds were dropped)
-        cval[s] = (CT)c;
+#pragma unroll
+        for (int j = 0; j < SCITEMS; ++j) {
+            st[j] = x[j] < n ? seg_start[x[j]] : 0;
+            d[j] = (d0 && x[j] < n) ? d0[x[j]] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < SCITEMS; ++j) {
+            long long i = i0 + (long long)j * blockDim.x;
+            if (i >= ns) continue;
+            if (x[j] >= n) {
+                cval[sv[j]] = big;
+                continue;
+            }
+            long long r = i - st[j] + 1;
+            long long c = min(d[j] + r, T + 1);  // d <= T here (larger seeds were dropped)
+            cval[sv[j]] = (CT)c;
+        }
     }
 }
 
@@ -211,15 +232,29 @@ __global__ void parents_kernel(const unsigned *__restrict__ key, const unsigned 
                                long long ns, unsigned n, const signed char *__restrict__ role,
                                const int *__restrict__ lastw, int *__restrict__ parent,
                                int *__restrict__ finalw) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ns;
-         i += (long long)gridDim.x * blockDim.x) {
-        unsigned x = key[i];
-        if (x >= n) continue;
-        unsigned s = val[i];
-        int k = (int)(s >> 1);
-        signed char r = role[k];
-        if (r >= 0 && r != (signed char)(s & 1)) parent[k] = lastw[i];  // source slot
-        if (i == ns - 1 || key[i + 1] != x) finalw[x] = lastw[i];
+    // 4 slots per thread, role[] gathers issued together (latency-bound)
+    const long long stride = (long long)gridDim.x * blockDim.x * SCITEMS;
+    for (long long i0 = (long long)blockIdx.x * blockDim.x * SCITEMS + threadIdx.x; i0 < ns;
+         i0 += stride) {
+        unsigned x[SCITEMS], sv[SCITEMS], nx[SCITEMS];
+        signed char r[SCITEMS];
+#pragma unroll
+        for (int j = 0; j < SCITEMS; ++j) {
+            long long i = i0 + (long long)j * blockDim.x;
+            x[j] = i < ns ? key[i] : n;
+            sv[j] = i < ns ? val[i] : 0u;
+            nx[j] = (i + 1 < ns) ? key[i + 1] : n;
+        }
+#pragma unroll
+        for (int j = 0; j < SCITEMS; ++j) r[j] = x[j] < n ? role[sv[j] >> 1] : (signed char)-1;
+#pragma unroll
+        for (int j = 0; j < SCITEMS; ++j) {
+            long long i = i0 + (long long)j * blockDim.x;
+            if (i >= ns || x[j] >= n) continue;
+            const int k = (int)(sv[j] >> 1);
+            if (r[j] >= 0 && r[j] != (signed char)(sv[j] & 1)) parent[k] = lastw[i];  // source
+            if (i == ns - 1 || nx[j] != x[j]) finalw[x[j]] = lastw[i];
+        }
     }
 }
 
