@@ -1689,7 +1689,10 @@ struct Tree {
         }
     }
     bool force_flat = false;  // node-sharded runs always walk the flat tree
-    bool flat() const { return force_flat || getenv("CVZ_BH_BINARY") == nullptr; }
+    bool flat() const {
+        static const bool binary = getenv("CVZ_BH_BINARY") != nullptr;
+        return force_flat || !binary;
+    }
     // reference cell numbering of the current tree (see cell_entries_kernel)
     void build_ids(cudaStream_t s) {
         if (!idslot) {
