@@ -111,23 +111,51 @@ __global__ void __launch_bounds__(CBLOCK) compact_edges_kernel(
             }
         }
     }
-    int total;
-    int off = block_exclusive_scan<CBLOCK>(cnt, s_warp, total);
-    unsigned long long prefix = tile_prefix(st, tile, (unsigned long long)total, &s_prefix);
-    // Items are strided by CBLOCK inside the tile, so a thread's kept items
-    // are not contiguous in stream order: recompute a per-slot ordinal.
-    // Rank of (j, tid) in tile order = sum over j' < j of all kept + rank in slot j.
-    // Do it slot-by-slot with a block scan per slot (CITEMS scans).
-    __syncthreads();
-    (void)off;
-    long long run = 0;
+    // warp ballots -> per (item, warp) counts -> one scan by warp 0: two
+    // block barriers per tile instead of one block scan per item slot
+    constexpr int NW = CBLOCK / 32;
+    __shared__ unsigned s_cnt[CITEMS * NW];
+    __shared__ unsigned s_total;
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    unsigned bal[CITEMS];
 #pragma unroll
     for (int j = 0; j < CITEMS; ++j) {
-        int tot_j;
-        int o = block_exclusive_scan<CBLOCK>(keep[j] ? 1 : 0, s_warp, tot_j);
-        if (keep[j]) out[prefix + run + o] = e[j];
-        run += tot_j;
+        bal[j] = __ballot_sync(0xffffffffu, keep[j]);
+        if (lane == 0) s_cnt[j * NW + wid] = __popc(bal[j]);
     }
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan of the CITEMS * NW counts, PER per lane
+        constexpr int PER = CITEMS * NW / 32;
+        static_assert(PER * 32 == CITEMS * NW, "scan layout");
+        unsigned a[PER], v = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            a[q] = s_cnt[PER * lane + q];
+            v += a[q];
+        }
+        unsigned x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        unsigned r = x - v;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            s_cnt[PER * lane + q] = r;
+            r += a[q];
+        }
+        if (lane == 31) s_total = x;
+    }
+    __syncthreads();
+    const unsigned total = s_total;
+    (void)cnt;
+    (void)s_warp;
+    unsigned long long prefix = tile_prefix(st, tile, (unsigned long long)total, &s_prefix);
+    const unsigned lt = (1u << lane) - 1;
+#pragma unroll
+    for (int j = 0; j < CITEMS; ++j)
+        if (keep[j]) out[prefix + s_cnt[j * NW + wid] + __popc(bal[j] & lt)] = e[j];
     // max + range flag
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane_id() == 0) s_max[threadIdx.x >> 5] = mx;

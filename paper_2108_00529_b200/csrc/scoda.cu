@@ -698,7 +698,7 @@ __global__ void compose_kernel(long long n, const long long *__restrict__ rep,
 }
 
 // stable relabel + drop-intra compaction (single pass, decoupled look-back)
-constexpr int RITEMS = 16;
+constexpr int RITEMS = 8;
 constexpr int RTILE = TB * RITEMS;
 
 constexpr long long SAT_BIT = 1LL << 62;
