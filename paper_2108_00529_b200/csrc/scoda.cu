@@ -43,9 +43,6 @@ constexpr int TB = 256;
 // fast mode: edges in flight <= m / FAST_WINDOW_DIV
 constexpr long long FAST_WINDOW_DIV = 128;
 
-struct MaxOp {
-    __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
-};
 
 __global__ void gather_edges_kernel(const int2 *__restrict__ e, const long long *__restrict__ order,
                                     long long m, int2 *__restrict__ out) {
@@ -160,7 +157,6 @@ __global__ void slot_counter_kernel(const unsigned *__restrict__ key,
                                     const int *__restrict__ seg_start,
                                     const long long *__restrict__ d0, long long T,
                                     CT *__restrict__ cval) {
-    const CT big = (CT)(T + 1);  // > T: marks sentinel slots inactive
     const long long stride = (long long)gridDim.x * blockDim.x * SCITEMS;
     for (long long i0 = (long long)blockIdx.x * blockDim.x * SCITEMS + threadIdx.x; i0 < ns;
          i0 += stride) {
@@ -182,13 +178,10 @@ __global__ void slot_counter_kernel(const unsigned *__restrict__ key,
         for (int j = 0; j < SCITEMS; ++j) {
             long long i = i0 + (long long)j * blockDim.x;
             if (i >= ns) continue;
-            if (x[j] >= n) {
-                cval[sv[j]] = big;
-                continue;
-            }
+            if (x[j] >= n) continue;  // sentinel slot: T + 1 prefill
             long long r = i - st[j] + 1;
-            long long c = min(d[j] + r, T + 1);  // d <= T here (larger seeds were dropped)
-            cval[sv[j]] = (CT)c;
+            long long c = d[j] + r;  // d <= T here (larger seeds were dropped)
+            if (c <= T) cval[sv[j]] = (CT)c;  // saturated slots keep the T + 1 prefill
         }
     }
 }
@@ -214,46 +207,52 @@ __global__ void edge_role_kernel(const int2 *__restrict__ E, long long m,
     }
 }
 
-// write-slot indicator: k if slot i (sorted) is the TARGET of event k
-struct WriteVal {
-    const unsigned *key, *val;
-    const signed char *role;
-    unsigned n;
-    __device__ __forceinline__ int operator()(int i) const {
-        unsigned x = key[i];
-        if (x >= n) return -1;
-        unsigned s = val[i];
-        int k = (int)(s >> 1);
-        return role[k] == (signed char)(s & 1) ? k : -1;
-    }
-};
-
-__global__ void parents_kernel(const unsigned *__restrict__ key, const unsigned *__restrict__ val,
-                               long long ns, unsigned n, const signed char *__restrict__ role,
-                               const int *__restrict__ lastw, int *__restrict__ parent,
-                               int *__restrict__ finalw) {
-    // 4 slots per thread, role[] gathers issued together (latency-bound)
-    const long long stride = (long long)gridDim.x * blockDim.x * SCITEMS;
-    for (long long i0 = (long long)blockIdx.x * blockDim.x * SCITEMS + threadIdx.x; i0 < ns;
-         i0 += stride) {
-        unsigned x[SCITEMS], sv[SCITEMS], nx[SCITEMS];
-        signed char r[SCITEMS];
-#pragma unroll
-        for (int j = 0; j < SCITEMS; ++j) {
-            long long i = i0 + (long long)j * blockDim.x;
-            x[j] = i < ns ? key[i] : n;
-            sv[j] = i < ns ? val[i] : 0u;
-            nx[j] = (i + 1 < ns) ? key[i + 1] : n;
+// Parents without a segmented scan.  Writes to node x happen only at its
+// active slots -- the first b = T - d0(x) of its segment (a later slot's
+// post-increment counter exceeds T) -- and the sorted segment lists them in
+// stream order.  So the last write before an active source slot i is found
+// by scanning back at most b - 1 slots, and x's final write among its (at
+// most b) active slots; every other slot does nothing.  Same results as the
+// inclusive "last write so far" scan over all slots it replaces.
+__global__ void direct_parents_kernel(const unsigned *__restrict__ key,
+                                      const unsigned *__restrict__ val, long long ns, unsigned n,
+                                      const int *__restrict__ seg_start,
+                                      const int *__restrict__ seg_end,
+                                      const long long *__restrict__ d0, long long T,
+                                      const signed char *__restrict__ role,
+                                      int *__restrict__ parent, int *__restrict__ finalw) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ns;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned x = key[i];
+        if (x >= n) continue;
+        const int st = seg_start[x];
+        const long long b = T - (d0 ? d0[x] : 0);  // active slots of x
+        if (i - st >= b) continue;
+        const unsigned s = val[i];
+        const int k = (int)(s >> 1);
+        const signed char ro = role[k];
+        if (ro >= 0 && ro != (signed char)(s & 1)) {  // event k reads x's label here
+            int p = -1;
+            for (long long j = i - 1; j >= st; --j) {
+                const unsigned sj = val[j];
+                if (role[sj >> 1] == (signed char)(sj & 1)) {
+                    p = (int)(sj >> 1);
+                    break;
+                }
+            }
+            parent[k] = p;
         }
-#pragma unroll
-        for (int j = 0; j < SCITEMS; ++j) r[j] = x[j] < n ? role[sv[j] >> 1] : (signed char)-1;
-#pragma unroll
-        for (int j = 0; j < SCITEMS; ++j) {
-            long long i = i0 + (long long)j * blockDim.x;
-            if (i >= ns || x[j] >= n) continue;
-            const int k = (int)(sv[j] >> 1);
-            if (r[j] >= 0 && r[j] != (signed char)(sv[j] & 1)) parent[k] = lastw[i];  // source
-            if (i == ns - 1 || nx[j] != x[j]) finalw[x[j]] = lastw[i];
+        const long long last_active = min((long long)seg_end[x], (long long)st + b) - 1;
+        if (i == last_active) {  // x's final label comes from its last write
+            int fw = -1;
+            for (long long j = i; j >= st; --j) {
+                const unsigned sj = val[j];
+                if (role[sj >> 1] == (signed char)(sj & 1)) {
+                    fw = (int)(sj >> 1);
+                    break;
+                }
+            }
+            finalw[x] = fw;
         }
     }
 }
@@ -878,23 +877,11 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
         auto *role = sc.alloc<signed char>(m);
         CVZ_LAUNCH(edge_role_kernel<CT>, grid_for(m, TB, 1, 16), TB, 0, s, E, m, cval, T, tie,
                    role);
-        // 4. segmented "last write so far" over the node-sorted slots
-        int *lastw = sc.alloc<int>(ns);
-        if (ns > 0) {
-            WriteVal wv{skeys, svals, role, (unsigned)n};
-            auto vin = thrust::make_transform_iterator(thrust::counting_iterator<int>(0), wv);
-            size_t tb = 0;
-            CVZ_CUDA(cub::DeviceScan::InclusiveScanByKey(nullptr, tb, skeys, vin, lastw, MaxOp(),
-                                                         (int)ns, cub::Equality(), s));
-            void *tmp = sc.alloc<char>(tb);
-            CVZ_REGION("cub_scan_by_key:scoda_lastw", s);
-            CVZ_CUDA(cub::DeviceScan::InclusiveScanByKey(tmp, tb, skeys, vin, lastw, MaxOp(),
-                                                         (int)ns, cub::Equality(), s));
-            count_launches(2);
-        }
+        // 4. each event's parent = last earlier write to its source node
+        //    (bounded backward scan over the node's active slots)
         int *parent = sc.alloc<int>(m);
-        CVZ_LAUNCH(parents_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, svals, ns,
-                   (unsigned)n, role, lastw, parent, finalw);
+        CVZ_LAUNCH(direct_parents_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, svals, ns,
+                   (unsigned)n, seg_start, seg_end, d0p, T, role, parent, finalw);
         // 5. event values by pointer jumping (one cooperative launch)
         origin = sc.alloc<int>(m);
         int *ptr = sc.alloc<int>(m);
