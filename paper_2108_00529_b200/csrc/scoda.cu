@@ -44,6 +44,10 @@ constexpr int TB = 256;
 constexpr long long FAST_WINDOW_DIV = 128;
 
 
+struct MaxOp {
+    __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
+};
+
 __global__ void gather_edges_kernel(const int2 *__restrict__ e, const long long *__restrict__ order,
                                     long long m, int2 *__restrict__ out) {
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
@@ -206,6 +210,52 @@ __global__ void edge_role_kernel(const int2 *__restrict__ E, long long m,
         role[k] = r;
     }
 }
+
+// write-slot indicator: k if slot i (sorted) is the TARGET of event k
+struct WriteVal {
+    const unsigned *key, *val;
+    const signed char *role;
+    unsigned n;
+    __device__ __forceinline__ int operator()(int i) const {
+        unsigned x = key[i];
+        if (x >= n) return -1;
+        unsigned s = val[i];
+        int k = (int)(s >> 1);
+        return role[k] == (signed char)(s & 1) ? k : -1;
+    }
+};
+
+__global__ void parents_kernel(const unsigned *__restrict__ key, const unsigned *__restrict__ val,
+                               long long ns, unsigned n, const signed char *__restrict__ role,
+                               const int *__restrict__ lastw, int *__restrict__ parent,
+                               int *__restrict__ finalw) {
+    // 4 slots per thread, role[] gathers issued together (latency-bound)
+    const long long stride = (long long)gridDim.x * blockDim.x * SCITEMS;
+    for (long long i0 = (long long)blockIdx.x * blockDim.x * SCITEMS + threadIdx.x; i0 < ns;
+         i0 += stride) {
+        unsigned x[SCITEMS], sv[SCITEMS], nx[SCITEMS];
+        signed char r[SCITEMS];
+#pragma unroll
+        for (int j = 0; j < SCITEMS; ++j) {
+            long long i = i0 + (long long)j * blockDim.x;
+            x[j] = i < ns ? key[i] : n;
+            sv[j] = i < ns ? val[i] : 0u;
+            nx[j] = (i + 1 < ns) ? key[i + 1] : n;
+        }
+#pragma unroll
+        for (int j = 0; j < SCITEMS; ++j) r[j] = x[j] < n ? role[sv[j] >> 1] : (signed char)-1;
+#pragma unroll
+        for (int j = 0; j < SCITEMS; ++j) {
+            long long i = i0 + (long long)j * blockDim.x;
+            if (i >= ns || x[j] >= n) continue;
+            const int k = (int)(sv[j] >> 1);
+            if (r[j] >= 0 && r[j] != (signed char)(sv[j] & 1)) parent[k] = lastw[i];  // source
+            if (i == ns - 1 || nx[j] != x[j]) finalw[x[j]] = lastw[i];
+        }
+    }
+}
+
+constexpr long long DIRECT_PARENTS_MAX_T = 64;
 
 // Parents without a segmented scan.  Writes to node x happen only at its
 // active slots -- the first b = T - d0(x) of its segment (a later slot's
@@ -877,11 +927,32 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
         auto *role = sc.alloc<signed char>(m);
         CVZ_LAUNCH(edge_role_kernel<CT>, grid_for(m, TB, 1, 16), TB, 0, s, E, m, cval, T, tie,
                    role);
-        // 4. each event's parent = last earlier write to its source node
-        //    (bounded backward scan over the node's active slots)
+        // 4. each event's parent = last earlier write to its source node: a
+        //    bounded backward scan over the node's <= T active slots, or for
+        //    large thresholds (quadratic scans) a segmented "last write so
+        //    far" max-scan over all node-sorted slots
         int *parent = sc.alloc<int>(m);
-        CVZ_LAUNCH(direct_parents_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, svals, ns,
-                   (unsigned)n, seg_start, seg_end, d0p, T, role, parent, finalw);
+        if (T <= DIRECT_PARENTS_MAX_T) {
+            CVZ_LAUNCH(direct_parents_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, svals, ns,
+                       (unsigned)n, seg_start, seg_end, d0p, T, role, parent, finalw);
+        } else {
+            int *lastw = sc.alloc<int>(ns);
+            if (ns > 0) {
+                WriteVal wv{skeys, svals, role, (unsigned)n};
+                auto vin = thrust::make_transform_iterator(thrust::counting_iterator<int>(0), wv);
+                size_t tb = 0;
+                CVZ_CUDA(cub::DeviceScan::InclusiveScanByKey(nullptr, tb, skeys, vin, lastw,
+                                                             MaxOp(), (int)ns, cub::Equality(),
+                                                             s));
+                void *tmp = sc.alloc<char>(tb);
+                CVZ_REGION("cub_scan_by_key:scoda_lastw", s);
+                CVZ_CUDA(cub::DeviceScan::InclusiveScanByKey(tmp, tb, skeys, vin, lastw, MaxOp(),
+                                                             (int)ns, cub::Equality(), s));
+                count_launches(2);
+            }
+            CVZ_LAUNCH(parents_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, svals, ns,
+                       (unsigned)n, role, lastw, parent, finalw);
+        }
         // 5. event values by pointer jumping (one cooperative launch)
         origin = sc.alloc<int>(m);
         int *ptr = sc.alloc<int>(m);

@@ -154,6 +154,23 @@ def test_detect_interleaved_orders_bit_exact(cv, orc):
         assert np.array_equal(a.label, ref[0])
 
 
+@pytest.mark.parametrize("base", [8, 40, 100, 300])
+def test_detect_thresholds_both_parent_paths(cv, orc, base):
+    """Dense graph, thresholds below and above DIRECT_PARENTS_MAX_T (64): the
+    bounded backward scan and the segmented max-scan give the reference's
+    labels, counters and history bit for bit."""
+    from paper_2108_00529_b200 import synth
+    e = synth.planted_partition(600, 90000, 6, seed=9)
+    g = cv.from_edge_array(e)
+    n, ee, deg = orc.from_edge_array(e)
+    ref = orc.detect_communities(n, ee, deg, base, 10, 0, workers=1)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+    assert np.array_equal(a.label, ref[0]) and np.array_equal(a.counter_degree, ref[1])
+    assert len(a.round_history) == len(ref[2])
+    for x, y in zip(a.round_history, ref[2]):
+        assert np.array_equal(x, y)
+
+
 def test_reference_community_kats(cv):
     # /root/reference/pkg/tests/test_community.py:80-153
     g = cv.from_edge_array(np.array([[0, 1]]))
