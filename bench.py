@@ -557,3 +557,10 @@ def main():
 
 if __name__ == "__main__":
     main()
+    try:  # clean NCCL/gloo shutdown on every rank (torchrun runs)
+        import torch.distributed as _dist
+        if _dist.is_available() and _dist.is_initialized():
+            _dist.barrier()
+            _dist.destroy_process_group()
+    except Exception:  # noqa: BLE001 -- shutdown must not turn a result into a failure
+        pass
