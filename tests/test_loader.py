@@ -196,3 +196,28 @@ def test_run_pipeline_end_to_end(tmp_path):
     with pytest.raises(cv.PipelineStageError, match="parse"):
         cv.run_pipeline(cv.PipelineConfig(input=str(tmp_path / "missing.txt"),
                                           outdir=str(out)))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_run_ablation_rows(tmp_path):
+    """C/cli.py:221-269 sweep: one row per setting, detection bit-exact vs the
+    oracle at every threshold, TSV written with the reference's columns."""
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import synth
+    e = synth.planted_partition(2000, 20000, 20, seed=8)
+    path = tmp_path / "g.txt"
+    path.write_text("\n".join(f"{a} {b}" for a, b in e) + "\n")
+    cfg = cv.PipelineConfig(input=str(path), outdir=str(tmp_path), workers=1)
+    rows = cv.run_ablation(cfg, "threshold", str(tmp_path / "abl.tsv"))
+    n, ee, deg = orc.parse_edge_list(path.read_text())
+    for r in rows:
+        lab, _, _ = orc.detect_communities(n, ee, deg, r["value"], 10, 0, workers=1)
+        assert r["communities"] == len(np.unique(lab))
+        assert abs(r["modularity"] - orc.modularity(ee, deg, lab)) <= 1e-9
+        assert r["mean_weight_overshoot"] >= 0  # count-min never undercounts
+    head = (tmp_path / "abl.tsv").read_text().splitlines()[0].split("\t")
+    assert head == ["axis", "value", "communities", "supernodes", "superedges", "modularity",
+                    "mean_weight_overshoot", "detect_ms"]
+    with pytest.raises(ValueError):
+        cv.run_ablation(cfg, "zoom")
