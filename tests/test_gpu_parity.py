@@ -644,3 +644,56 @@ def test_long_layout_final_stress_within_2pct(cv, orc):
     ref = _stress(pos, sg.edges, ew)
     assert np.all(np.abs(ours - ref) <= 0.02 * np.abs(ref)), (ours, ref)
     assert abs(res.displacement[-1] - disp[-1]) <= 0.02 * max(disp[-1], 1e-12) + 1e-9
+
+
+def _pipeline_vs_oracle(cv, orc, e, node_count=None, iters=3, check_layout=True):
+    g = cv.from_edge_array(e, node_count)
+    n, ee, deg = orc.from_edge_array(np.asarray(e, np.int64).reshape(-1, 2), node_count)
+    assert g.node_count == n and np.array_equal(g.edges, ee) and np.array_equal(g.degree, deg)
+    base = orc.degree_stats(deg)[0] if len(ee) else 1
+    lab, cnt, hist = orc.detect_communities(n, ee, deg, base, 10, 0, workers=1)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+    assert np.array_equal(a.label, lab) and np.array_equal(a.counter_degree, cnt)
+    s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    cv.accumulate_sizes(s, a, g)
+    sg = cv.contract(g, a, s)
+    A, B = orc.sketch_params(4, 0)
+    t = np.zeros((4, orc.default_cols(len(ee))), np.int64)
+    orc.sketch_add_many(t, A, B, lab, deg)
+    k, se, w, mult, comm = orc.contract(ee, lab, t, A, B)
+    assert sg.node_count == k and np.array_equal(sg.edges.reshape(-1, 2), se.reshape(-1, 2))
+    assert np.array_equal(sg.weight, w) and np.array_equal(sg.multiplicity, mult)
+    res = cv.layout(sg, cv.LayoutParams(iterations=iters))
+    assert res.positions.shape == (k, 2) and np.all(np.isfinite(res.positions))
+    if k > 1 and check_layout:
+        mass, ew = orc.masses_supergraph(w, mult)
+        pos, _ = orc.layout(k, mass, se.reshape(-1, 2), ew, iterations=iters)
+        diam = max(np.hypot(*(pos.max(0) - pos.min(0))), 1e-12)
+        assert np.max(np.abs(res.positions - pos)) <= 1e-7 * diam
+    return g, a, sg
+
+
+def test_pipeline_edge_cases(cv, orc):
+    """Degenerate inputs through the whole path, each against the oracle:
+    a single edge, duplicates only, isolated nodes (node_count beyond the max
+    id: isolated supernodes keep weight 0, layout mass clamps to 1), a
+    one-community graph (no superedges, 1-node layout), sparse large ids,
+    and a star (one hub saturating at T + 1)."""
+    _pipeline_vs_oracle(cv, orc, np.array([[0, 1]]))
+    _pipeline_vs_oracle(cv, orc, np.array([[2, 5]] * 7))
+    g, a, sg = _pipeline_vs_oracle(cv, orc, np.array([[0, 1], [1, 2], [2, 0], [3, 4]]),
+                                   node_count=9)
+    assert np.sum(sg.weight == 0) >= 1
+    _pipeline_vs_oracle(cv, orc, np.array([[i, j] for i in range(6) for j in range(i + 1, 6)]))
+    rng = np.random.default_rng(4)
+    ids = rng.choice(1 << 24, size=300, replace=False)
+    # (millions of isolated supernodes: integer stages vs the oracle, layout
+    # only checked finite -- the oracle's O(n) per-iteration tree is slow)
+    _pipeline_vs_oracle(cv, orc, ids[rng.integers(0, 300, size=(2000, 2))], check_layout=False)
+    star = np.array([[0, i] for i in range(1, 400)] + [[i, i + 1] for i in range(1, 399, 2)])
+    _pipeline_vs_oracle(cv, orc, star)
+    # only self-loops: no edges left (C/graph.py:117-118) -> detection refuses
+    g = cv.from_edge_array(np.array([[3, 3], [1, 1]]), node_count=4)
+    assert g.edge_count == 0 and g.node_count == 4 and g.degree.tolist() == [0, 0, 0, 0]
+    with pytest.raises(ValueError):
+        cv.detect_communities(g, cv.ThresholdSchedule(base=2))
