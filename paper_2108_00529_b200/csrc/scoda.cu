@@ -1002,7 +1002,10 @@ void scoda_pass_dev(const int2 *E, long long m, long long n, long long T, int ti
         // reference's own parallel schedules (C/community.py:164-195) only
         // while the edges in flight are a small fraction of the stream
         // (DESIGN.md "fast mode"); at C4 scale this is full occupancy anyway.
-        long long window = std::max(256LL, std::min(m / FAST_WINDOW_DIV, 2048LL * num_sms() * FU));
+        static const long long wdiv =
+            getenv("CVZ_FAST_WINDOW_DIV") ? std::max(1LL, atoll(getenv("CVZ_FAST_WINDOW_DIV")))
+                                          : FAST_WINDOW_DIV;
+        long long window = std::max(256LL, std::min(m / wdiv, 2048LL * num_sms() * FU));
         unsigned blocks = (unsigned)((window / FU + TB - 1) / TB);
         CVZ_LAUNCH(fast_pass_kernel, blocks, TB, 0, s, E, m,
                    reinterpret_cast<const long long *>(d0), T, tie, cnt,
