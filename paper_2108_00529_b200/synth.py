@@ -102,7 +102,7 @@ def rmat_counter(scale: int, start: int, count: int, seed: int = 0,
     int32 array -- the host twin used by the tests."""
     a, b, c, _ = abcd
     k = np.arange(start, start + count, dtype=np.uint64)
-    base = np.uint64(seed) * _PHI
+    base = np.uint64((int(seed) * 0x9E3779B97F4A7C15) % (1 << 64))
     u = np.zeros(count, dtype=np.int64)
     v = np.zeros(count, dtype=np.int64)
     with np.errstate(over="ignore"):

@@ -151,10 +151,17 @@ def _gpu_worker(rank, world, port, out_dir, iters):
     p = cv.LayoutParams(iterations=iters)
     r_sup = layout_sharded(sup, p, comm)
     r_full = layout_sharded(g, cv.LayoutParams(iterations=max(2, iters // 4)), comm)
+    # exact repulsion (theta = 0) and coincident starting points (reference
+    # cell-numbered jitter rerun) on the node-sharded path
+    r_exact = layout_sharded(sup, cv.LayoutParams(iterations=5, theta=0.0), comm)
+    p0 = np.repeat(np.random.default_rng(1).uniform(-3, 3, (sup.node_count // 4 + 1, 2)), 4,
+                   axis=0)[:sup.node_count]
+    r_coin = layout_sharded(sup, cv.LayoutParams(iterations=5), comm, positions=p0)
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), degree=sg.degree, edges=g.edges,
              m=sg.edge_count, table=s.table, labels=labels.cpu().numpy(),
              sup_pos=r_sup.positions, sup_disp=r_sup.displacement,
-             full_pos=r_full.positions, full_disp=r_full.displacement)
+             full_pos=r_full.positions, full_disp=r_full.displacement,
+             exact_pos=r_exact.positions, coin_pos=r_coin.positions, p0=p0)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -196,6 +203,12 @@ def test_sharded_matches_single_gpu():
         np.testing.assert_allclose(r["sup_disp"], ref_sup.displacement, rtol=1e-6, atol=1e-9)
     assert np.array_equal(r0["sup_pos"], r1["sup_pos"])
     assert np.array_equal(r0["full_pos"], r1["full_pos"])
+    ref_exact = cv.layout(sup, cv.LayoutParams(iterations=5, theta=0.0))
+    ref_coin = cv.layout(sup, cv.LayoutParams(iterations=5), positions=r0["p0"])
+    for key, ref in (("exact_pos", ref_exact), ("coin_pos", ref_coin)):
+        diam = np.hypot(*(ref.positions.max(0) - ref.positions.min(0)))
+        for r in (r0, r1):
+            assert np.max(np.abs(r[key] - ref.positions)) <= 1e-7 * diam, key
 
 
 @pytest.mark.gpu
