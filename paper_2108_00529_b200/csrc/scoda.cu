@@ -25,6 +25,7 @@
 // node sees a fixed point; nodes that never do sit on/above a >=2-cycle and
 // get a min-doubling pass over the (closed) set of such nodes.
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -132,6 +133,31 @@ __global__ void __launch_bounds__(TB) slot_keys_kernel(
         }
     }
     if (threadIdx.x == 0 && tile == num_tiles - 1) *d_count = prefix + total;
+}
+
+// First-round slot keys: slot 2k = u, 2k+1 = v (sentinel n for the second
+// slot of a self-loop: it is bumped once, C/community.py:104-109), values =
+// slot ids.  Two edges per 128-bit load, two 128-bit stores per array.
+__global__ void slot_keys_direct_kernel(const int4 *__restrict__ E2, const int2 *__restrict__ E,
+                                        long long m, unsigned n, unsigned *__restrict__ keys,
+                                        unsigned *__restrict__ vals) {
+    const long long pairs = m / 2;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int4 p = __ldcs(E2 + i);  // edges 2i, 2i+1
+        const unsigned s0 = (unsigned)(4 * i);
+        reinterpret_cast<uint4 *>(keys)[i] =
+            make_uint4((unsigned)p.x, p.x == p.y ? n : (unsigned)p.y, (unsigned)p.z,
+                       p.z == p.w ? n : (unsigned)p.w);
+        reinterpret_cast<uint4 *>(vals)[i] = make_uint4(s0, s0 + 1, s0 + 2, s0 + 3);
+    }
+    if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int2 p = E[m - 1];
+        keys[2 * (m - 1)] = (unsigned)p.x;
+        keys[2 * (m - 1) + 1] = p.x == p.y ? n : (unsigned)p.y;
+        vals[2 * (m - 1)] = (unsigned)(2 * (m - 1));
+        vals[2 * (m - 1) + 1] = (unsigned)(2 * (m - 1) + 1);
+    }
 }
 
 template <class CT>
@@ -896,18 +922,28 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
     if (m > 0) {
         // 1. live slots in stream order (dead ones dropped, see slot_keys_kernel)
         auto *keys = sc.alloc<unsigned>(ns_all), *vals = sc.alloc<unsigned>(ns_all);
-        unsigned tiles = (unsigned)((m + STILE - 1) / STILE);
-        auto *status = sc.alloc<unsigned long long>(tiles);
-        auto *ctr = sc.alloc<unsigned>(1);
-        auto *dcount = sc.alloc<unsigned long long>(1);
-        CVZ_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * tiles, s));
-        CVZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
-        CVZ_LAUNCH(slot_keys_kernel, tiles, TB, 0, s, E, m, d0p, T, keys, vals,
-                   LookbackState{status, ctr}, dcount, tiles);
-        unsigned long long hns = 0;
-        CVZ_CUDA(cudaMemcpyAsync(&hns, dcount, sizeof(hns), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
-        const long long ns = (long long)hns;
+        long long ns;
+        if (!d0p && (reinterpret_cast<uintptr_t>(E) & 15) == 0) {
+            // no seeds (first round): every slot is live except a self-loop's
+            // second one, which gets the sentinel key n instead of being
+            // dropped -- a plain streaming pass, no compaction
+            ns = ns_all;
+            CVZ_LAUNCH(slot_keys_direct_kernel, grid_for(m, TB, 2, 16), TB, 0, s,
+                       reinterpret_cast<const int4 *>(E), E, m, (unsigned)n, keys, vals);
+        } else {
+            unsigned tiles = (unsigned)((m + STILE - 1) / STILE);
+            auto *status = sc.alloc<unsigned long long>(tiles);
+            auto *ctr = sc.alloc<unsigned>(1);
+            auto *dcount = sc.alloc<unsigned long long>(1);
+            CVZ_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * tiles, s));
+            CVZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+            CVZ_LAUNCH(slot_keys_kernel, tiles, TB, 0, s, E, m, d0p, T, keys, vals,
+                       LookbackState{status, ctr}, dcount, tiles);
+            unsigned long long hns = 0;
+            CVZ_CUDA(cudaMemcpyAsync(&hns, dcount, sizeof(hns), cudaMemcpyDeviceToHost, s));
+            CVZ_CUDA(cudaStreamSynchronize(s));
+            ns = (long long)hns;
+        }
         // 2. stable sort by node: each node's slots in stream order
         auto *skeys = sc.alloc<unsigned>(ns), *svals = sc.alloc<unsigned>(ns);
         if (ns > 0)
