@@ -261,15 +261,17 @@ void superedges(const int2 *e, long long m, const int *dense, long long k, int B
         res->mult = device_alloc<int64_t>(0, s);
         return;
     }
-    K *sorted = sc.alloc<K>(c);
+    // keys are scratch: sort in place over a DoubleBuffer (no copy pass)
+    cub::DoubleBuffer<K> dk(keys, sc.alloc<K>(c));
     size_t tb = 0;
-    CVZ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, (int)c, 0, 2 * B, s));
+    CVZ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, dk, (int)c, 0, 2 * B, s));
     void *tmp = sc.alloc<char>(tb);
     {
         CVZ_REGION("cub_sort:contract_pairs", s);
-        CVZ_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, (int)c, 0, 2 * B, s));
+        CVZ_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, dk, (int)c, 0, 2 * B, s));
     }
     count_launches(1 + (2 * B + 7) / 8);
+    K *sorted = dk.Current();
     K *uniq = sc.alloc<K>(c);
     int *counts = sc.alloc<int>(c);
     auto *nruns = sc.alloc<long long>(1);

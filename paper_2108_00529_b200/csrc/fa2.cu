@@ -1838,16 +1838,17 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
         CVZ_LAUNCH(half_edges_kernel, grid_for(m, FB, 1, 8), FB, 0, s, e, m, key, val, cnt);
         int bits = 1;
         while (bits < 32 && (1LL << bits) < n) ++bits;
+        // scratch in / out: sort over DoubleBuffers (no copy pass)
+        cub::DoubleBuffer<unsigned> dk(key, skey), dv(val, sval);
         size_t tb = 0;
-        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, skey, val, sval, (int)nh, 0,
-                                                 bits, s));
+        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)nh, 0, bits, s));
         void *tmp = sc.alloc<char>(tb);
         {
             CVZ_REGION("cub_sort:csr", s);
-            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, skey, val, sval, (int)nh, 0, bits,
-                                                     s));
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)nh, 0, bits, s));
         }
         count_launches(1 + (bits + 7) / 8);
+        sval = dv.Current();
         CVZ_LAUNCH(csr_fill_kernel, grid_for(nh, FB, 1, 8), FB, 0, s, e, sval, nh, weight, sign,
                    c.col, c.w);
     }

@@ -111,16 +111,19 @@ int cvz_first_seen_remap(const int64_t *ext, int64_t count, int32_t *dense, int6
         auto *val = sc.alloc<unsigned>(count), *sval = sc.alloc<unsigned>(count);
         CVZ_LAUNCH(remap_keys_kernel, grid_for(count, RB, 1, 8), RB, 0, s, x, (long long)count, mm,
                    key, val);
+        // scratch in / out: sort over DoubleBuffers (no copy pass)
+        cub::DoubleBuffer<unsigned long long> dk(key, skey);
+        cub::DoubleBuffer<unsigned> dv(val, sval);
         size_t tb = 0;
-        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, skey, val, sval, (int)count, 0,
-                                                 bits, s));
+        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)count, 0, bits, s));
         void *tmp = sc.alloc<char>(tb);
         {
             CVZ_REGION("cub_sort:remap", s);
-            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, skey, val, sval, (int)count, 0,
-                                                     bits, s));
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)count, 0, bits, s));
             count_launches(1 + (bits + 7) / 8);
         }
+        skey = dk.Current();
+        sval = dv.Current();
         auto *hidx = sc.alloc<unsigned>(count), *first = sc.alloc<unsigned>(count);
         auto *rank = sc.alloc<unsigned>(count);
         CVZ_CUDA(cudaMemsetAsync(first, 0, sizeof(unsigned) * count, s));

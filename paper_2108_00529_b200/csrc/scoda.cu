@@ -885,17 +885,24 @@ __global__ void __launch_bounds__(TB) relabel_compact_kernel(
     if (threadIdx.x == 0 && tile == num_tiles - 1) *d_count = prefix + total;
 }
 
+// Stable radix sort of (key, value) pairs in place over two buffer pairs
+// (CUB DoubleBuffer: no extra copy pass -- 1.16 vs 1.76 ms for 65M pairs on
+// B200).  Returns with *k / *v pointing at the sorted data.
 template <class T>
-void cub_sort_pairs(const unsigned *kin, unsigned *kout, const T *vin, T *vout, long long ns,
-                    int end_bit, Scratch &sc, cudaStream_t s) {
+void cub_sort_pairs_db(unsigned *&k, unsigned *kalt, T *&v, T *valt, long long ns, int end_bit,
+                       Scratch &sc, cudaStream_t s) {
+    cub::DoubleBuffer<unsigned> dk(k, kalt);
+    cub::DoubleBuffer<T> dv(v, valt);
     size_t tb = 0;
-    CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, (int)ns, 0,
-                                             end_bit, s));
+    CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)ns, 0, end_bit, s));
     void *tmp = sc.alloc<char>(tb);
-    CVZ_REGION("cub_sort:scoda_slots", s);
-    CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, (int)ns, 0, end_bit,
-                                             s));
+    {
+        CVZ_REGION("cub_sort:scoda_slots", s);
+        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)ns, 0, end_bit, s));
+    }
     count_launches(1 + (end_bit + 7) / 8);
+    k = dk.Current();
+    v = dv.Current();
 }
 
 int bits_for_value(unsigned long long v) {  // bits to hold 0..v
@@ -945,10 +952,10 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
             ns = (long long)hns;
         }
         // 2. stable sort by node: each node's slots in stream order
-        auto *skeys = sc.alloc<unsigned>(ns), *svals = sc.alloc<unsigned>(ns);
+        unsigned *skeys = keys, *svals = vals;
         if (ns > 0)
-            cub_sort_pairs(keys, skeys, vals, svals, ns, bits_for_value((unsigned long long)n), sc,
-                           s);
+            cub_sort_pairs_db(skeys, sc.alloc<unsigned>(ns), svals, sc.alloc<unsigned>(ns), ns,
+                              bits_for_value((unsigned long long)n), sc, s);
         CVZ_LAUNCH(seg_bounds_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, ns, (unsigned)n,
                    seg_start, seg_end);
         // 3. post-increment counters (dead slots: T + 1)
