@@ -56,22 +56,23 @@ __device__ __forceinline__ double separation(double &dx, double &dy, long long a
     return EPS;
 }
 
-// 1 / d2 without DDIV: fp32 seed + two fp64 Newton steps (relative error
-// ~1e-16, i.e. at the last ulp).  The reference computes kr*mi*mj / (d*d)
-// with d = sqrt(d2) (C/layout.py:240,260); d*d and d2 differ by <= 1 ulp, so
-// f = kr*mi*mj * (1/d2) agrees to ~1e-15 relative while skipping the fp64
-// sqrt + divide sequences that bound the traversal on the FP64 pipe.
-__device__ __forceinline__ float rcp_approx(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+// 1 / d2 without DDIV: MUFU.RCP64H seed (rcp.approx.ftz.f64) + a cubic and a
+// Newton fp64 step (relative error ~1e-16, i.e. at the last ulp).  The
+// reference computes kr*mi*mj / (d*d) with d = sqrt(d2) (C/layout.py:240,260);
+// d*d and d2 differ by <= 1 ulp, so f = kr*mi*mj * (1/d2) agrees to ~1e-15
+// relative while skipping the fp64 sqrt + divide sequences that bound the
+// traversal on the FP64 pipe.  The seed needs no fp32 round trip (F2F x2).
+__device__ __forceinline__ double rcp_approx(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     return r;
 }
 
 __device__ __forceinline__ double inv_d2(double d2) {
-    if (d2 > 1e30 || d2 < 1e-30) return 1.0 / d2;  // outside the fp32 seed's range
-    // 2^-22 seed, two Newton steps -> ~2^-88 before the final rounding
-    double r = (double)rcp_approx((float)d2);
+    if (d2 > 1e300) return 1.0 / d2;  // 1/d2 would be subnormal (flushed by the seed)
+    double r = rcp_approx(d2);
     double e = fma(-d2, r, 1.0);
+    e = fma(e, e, e);  // cubic first step (e -> e^3), as the DDIV sequence does
     r = fma(r, e, r);
     e = fma(-d2, r, 1.0);
     return fma(r, e, r);
