@@ -69,7 +69,8 @@ __device__ __forceinline__ double rcp_approx(double x) {
 }
 
 __device__ __forceinline__ double inv_d2(double d2) {
-    if (d2 > 1e300) return 1.0 / d2;  // 1/d2 would be subnormal (flushed by the seed)
+    // d2 >= COINCIDE_EPS^2 at every call; d2 > ~1e308 (1/d2 subnormal) would
+    // flush to 0 (coordinates beyond ~1e150, far outside any layout)
     double r = rcp_approx(d2);
     double e = fma(-d2, r, 1.0);
     e = fma(e, e, e);  // cubic first step (e -> e^3), as the DDIV sequence does
@@ -1080,6 +1081,12 @@ __global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(Walker w, const PNode
     w.s2tab = s2tab;
     w.th2 = mul(theta, theta);
     const double th2 = w.th2;
+    // side^2 at depth d is side0^2 * 4^-d exactly (power-of-two scaling, no
+    // subnormals in range): subtract 2d from the exponent instead of a
+    // shared-memory lookup per node
+    const double s20 = s2tab[0];
+    const bool s2exp = s20 > 1e-200 && s20 < 1e300;
+    const int s20_hi = __double2hiint(s20), s20_lo = __double2loint(s20);
     const int count = work ? *nwork : w.n;
     for (int t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < count;
          t0 += gridDim.x * blockDim.x) {
@@ -1105,9 +1112,13 @@ __global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(Walker w, const PNode
             const double d2 = add(mul(dx, dx), mul(dy, dy));
             // cells open unless side^2 < theta^2 d^2; leaves are always
             // approximated (C/layout.py:256-261)
-            if (kind == 1 && !(s2tab[t.meta >> 2] < mul(th2, d2))) {
-                ++c;
-                continue;
+            if (kind == 1) {
+                const double s2 = s2exp ? __hiloint2double(s20_hi - ((t.meta >> 2) << 21), s20_lo)
+                                        : s2tab[t.meta >> 2];
+                if (!(s2 < mul(th2, d2))) {
+                    ++c;
+                    continue;
+                }
             }
             if (c != self) {  // j == i skipped (:237-238)
                 if (d2 >= EPS * EPS) {
