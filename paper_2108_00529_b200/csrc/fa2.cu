@@ -1070,17 +1070,19 @@ __device__ __forceinline__ double2 aggregate_add(const Walker w, const PNode t, 
 template <int MINB>
 __global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(Walker w, const PNode *__restrict__ pn,
                                                      const unsigned *__restrict__ cle, double kr,
-                                                     double theta, double2 *__restrict__ out,
+                                                     double th2, double eps2,
+                                                     double2 *__restrict__ out,
                                                      const long long *__restrict__ bad,
                                                      const int *__restrict__ work,
                                                      const int *__restrict__ nwork) {
+    // th2 = theta * theta and eps2 = COINCIDE_EPS^2 come in as launch
+    // parameters so the hot loop reads them as constant-bank operands
     griddep_wait();
     if (bad && *bad) return;
     __shared__ double s2tab[MAX_DEPTH];
     side2_table(s2tab, w.cr.bbox);
     w.s2tab = s2tab;
-    w.th2 = mul(theta, theta);
-    const double th2 = w.th2;
+    w.th2 = th2;
     // side^2 at depth d is side0^2 * 4^-d exactly (power-of-two scaling, no
     // subnormals in range): subtract 2d from the exponent instead of a
     // shared-memory lookup per node
@@ -1120,17 +1122,16 @@ __global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(Walker w, const PNode
                     continue;
                 }
             }
-            if (c != self) {  // j == i skipped (:237-238)
-                if (d2 >= EPS * EPS) {
-                    const double f = mul(mul(kmi, t.m), inv_d2(d2));
-                    fx = add(fx, mul(f, dx));
-                    fy = add(fy, mul(f, dy));
-                } else {
-                    double2 r = jitter_add(w.bodies, w.n, w.aux, w.cr, th2, c, kind, i, kmi, t.m,
-                                           dx, dy, d2, false, fx, fy);
-                    fx = r.x;
-                    fy = r.y;
-                }
+            if (d2 >= eps2) {
+                const double f = mul(mul(kmi, t.m), inv_d2(d2));
+                fx = add(fx, mul(f, dx));
+                fy = add(fy, mul(f, dy));
+            } else if (c != self) {  // j == i skipped (:237-238); a leaf stores its
+                                     // body's exact position, so self has d2 == 0
+                double2 r = jitter_add(w.bodies, w.n, w.aux, w.cr, th2, c, kind, i, kmi, t.m, dx,
+                                       dy, d2, false, fx, fy);
+                fx = r.x;
+                fy = r.y;
             }
             c = t.skip;
         }
@@ -1763,8 +1764,8 @@ struct Tree {
             CVZ_LAUNCH(bh_warp_kernel<B>, persist_blocks(bh_warp_kernel<B>), FB, 0, s, w, pn, \
                        pcle, kr, theta, out, bad, work, nwork, wctr);                         \
         else                                                                                  \
-            CVZ_LAUNCH_PDL(bh_flat_kernel<B>, blocks_for(n, FB), FB, 0, s, w, pn, pcle, kr, theta,\
-                       out, bad, work, nwork);                                                \
+            CVZ_LAUNCH_PDL(bh_flat_kernel<B>, blocks_for(n, FB), FB, 0, s, w, pn, pcle, kr,       \
+                           theta * theta, EPS * EPS, out, bad, work, nwork);                  \
     } while (0)
             if (minb >= 6)
                 CVZ_BH_FLAT(6);
