@@ -1065,8 +1065,8 @@ __device__ __forceinline__ double2 aggregate_add(const Walker w, const PNode t, 
 }
 
 // per-thread walk: one body per thread, bodies in key order
-template <int MINB>
-__global__ void __launch_bounds__(FB, MINB) bh_flat_kernel(Walker w, const PNode *__restrict__ pn,
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) bh_flat_kernel(Walker w, const PNode *__restrict__ pn,
                                                      const unsigned *__restrict__ cle, double kr,
                                                      double th2, double eps2,
                                                      double2 *__restrict__ out,
@@ -1749,6 +1749,7 @@ struct Tree {
         CellRef cr{delta, pdelta, ids ? idslot : nullptr, jflag, bbox};
         if (flat()) {
             static const int minb = getenv("CVZ_BH_MINB") ? atoi(getenv("CVZ_BH_MINB")) : 5;
+            static const int bnt = getenv("CVZ_BH_NT") ? atoi(getenv("CVZ_BH_NT")) : 256;
 // per-thread walk by default; CVZ_BH_WARP=1 forces the warp-cooperative
             // walk, CVZ_BH_WARP=auto picks it for large n (clustered full graphs)
             static const char *wenv = getenv("CVZ_BH_WARP");
@@ -1762,15 +1763,26 @@ struct Tree {
             CVZ_LAUNCH(bh_warp_kernel<B>, persist_blocks(bh_warp_kernel<B>), FB, 0, s, w, pn, \
                        pcle, kr, theta, out, bad, work, nwork, wctr);                         \
         else                                                                                  \
-            CVZ_LAUNCH_PDL(bh_flat_kernel<B>, blocks_for(n, FB), FB, 0, s, w, pn, pcle, kr,       \
-                           theta * theta, EPS * EPS, out, bad, work, nwork);                  \
+            ::cvz::pdl_launch(NT == FB ? "bh_flat_kernel<" #B ">" : "bh_flat_kernel<NT," #B ">", \
+                              bh_flat_kernel<NT, B>, dim3(blocks_for(n, NT)), dim3(NT), 0, s, \
+                              w, pn, pcle, kr, theta * theta, EPS * EPS, out, bad, work,     \
+                              nwork);                                                        \
     } while (0)
-            if (minb >= 6)
-                CVZ_BH_FLAT(6);
-            else if (minb == 5)
-                CVZ_BH_FLAT(5);
-            else
-                CVZ_BH_FLAT(4);
+            if (bnt == 64) {
+                constexpr int NT = 64;
+                CVZ_BH_FLAT(20);
+            } else if (bnt == 128) {
+                constexpr int NT = 128;
+                CVZ_BH_FLAT(10);
+            } else {
+                constexpr int NT = FB;
+                if (minb >= 6)
+                    CVZ_BH_FLAT(6);
+                else if (minb == 5)
+                    CVZ_BH_FLAT(5);
+                else
+                    CVZ_BH_FLAT(4);
+            }
 #undef CVZ_BH_FLAT
         }
         else
