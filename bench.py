@@ -195,14 +195,14 @@ def kernel_bytes(name, st):
         # per body: Body (x, y, m, id) 32 B read + force 16 B write;
         # per tree node: TNode 48 B read once
         "bh_kernel": k * (32 + 16) + (k - 1) * 48,
-        # flat walk: per body 32 B read + 16 B force write; flat node array of
-        # k leaves + <= k-1 cells, FNode 48 B each, read once
-        "bh_flat_kernel<4>": k * (32 + 16) + (2 * k - 1) * 48,
-        "bh_flat_kernel<5>": k * (32 + 16) + (2 * k - 1) * 48,
-        "bh_flat_kernel<6>": k * (32 + 16) + (2 * k - 1) * 48,
-        # pos 16 + repulsion 16 + mass 8 + prev 16 + rowptr 8 + force 16 + swing 8
-        # per node; col 4 + weight 8 per half-edge
-        "forces_kernel": k * 88 + 2 * se * 12,
+        # flat walk: per body 32 B read + 16 B force write; preorder node
+        # array of k leaves + <= k-1 cells, PNode 32 B each, read once
+        "bh_flat_kernel<4>": k * (32 + 16) + (2 * k - 1) * 32,
+        "bh_flat_kernel<5>": k * (32 + 16) + (2 * k - 1) * 32,
+        "bh_flat_kernel<6>": k * (32 + 16) + (2 * k - 1) * 32,
+        # reads pos 16 + repulsion 16 + heavy index 4 + springs 16 + mass 8 +
+        # prev 16, writes force 16 + swing 8, per node
+        "forces_kernel": k * 100,
         # swing 8 + force 16 + pos r/w 32 + prev 16 per node
         "update_kernel": k * 72,
         # 1 ms graph replays excluded; per round bytes are in community_pass
@@ -236,10 +236,10 @@ def roofline(prof, st, peak_gbs):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
     if name.startswith("bh_"):
         # the tree walk is not HBM-bound: its node array is L1/L2-resident and
-        # every visit is a dependent fp64 chain (profiles/r1c_ncu_full_c4.md)
-        roof["limiter"] = ("fp64 issue/latency-bound tree walk, not HBM: ncu shows DRAM "
-                           "~1% of peak, L1 hit ~95%, FP64 pipe ~34%, issue active ~64%; "
-                           "bytes are the compulsory body + tree reads")
+        # every visit is a dependent fp64 chain (profiles/r1g_ncu_full_c4_fa2.md)
+        roof["limiter"] = ("issue-bound tree walk, not HBM: ncu shows DRAM ~1% of peak, "
+                           "L1 hit ~96% (~15 distinct nodes per warp load), FP64 pipe ~37%, "
+                           "issue active ~59%; bytes are the compulsory body + tree reads")
     return roof, top
 
 
