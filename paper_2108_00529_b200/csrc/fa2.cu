@@ -1302,7 +1302,27 @@ __global__ void __launch_bounds__(FB) springs_heavy_kernel(
         int u = heavy[w];
         double2 pu = pos[u];
         double fx = 0.0, fy = 0.0;
-        for (long long j = rowptr[u] + lane; j < rowptr[u + 1]; j += 32) {
+        const long long end = rowptr[u + 1];
+        long long j = rowptr[u] + lane;
+        // four lane-strided terms per step: loads batched ahead of the
+        // (unchanged, in-order) accumulation, so the col -> pos chains overlap
+        for (; j + 96 < end; j += 128) {
+            int v[4];
+            double c[4];
+            double2 pv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = col[j + 32 * q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[q] = cw[j + 32 * q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pv[q] = pos[v[q]];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                fx = add(fx, mul(c[q], sub(pv[q].x, pu.x)));
+                fy = add(fy, mul(c[q], sub(pv[q].y, pu.y)));
+            }
+        }
+        for (; j < end; j += 32) {
             double2 pv = pos[col[j]];
             double c = cw[j];
             fx = add(fx, mul(c, sub(pv.x, pu.x)));
