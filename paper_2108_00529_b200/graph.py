@@ -165,10 +165,72 @@ def parse_edge_list(text) -> Graph:
     return _parse_lines([ln.decode() if isinstance(ln, bytes) else ln for ln in text])
 
 
+# Binary edge cache (SPEC.md:77 permits "magic bytes, version, node_count,
+# edge array").  Little-endian: 8-byte magic, u32
+# version, u32 flags (bit 0: int64 ids), i64 node_count, i64 edge_count, then
+# the (edge_count, 2) dense-id edge array in stream order (self-loops already
+# dropped).  Reading it skips tokenising and remapping altogether.
+CACHE_MAGIC = b"CVZEDGE\0"
+CACHE_VERSION = 1
+_CACHE_HDR = 8 + 4 + 4 + 8 + 8
+
+
+def _write_cache_arrays(path, node_count: int, edges: np.ndarray) -> None:
+    edges = np.asarray(edges).reshape(-1, 2)
+    wide = bool(len(edges)) and int(edges.max()) >= 2**31
+    body = np.ascontiguousarray(edges, dtype="<i8" if wide else "<i4")
+    hdr = (CACHE_MAGIC + np.array([CACHE_VERSION, int(wide)], "<u4").tobytes()
+           + np.array([node_count, len(body)], "<i8").tobytes())
+    with open(path, "wb") as fh:
+        fh.write(hdr)
+        body.tofile(fh)
+
+
+def _read_cache_arrays(path):
+    """-> (node_count, (m, 2) int32/int64 edges); ParseError on a bad file."""
+    with open(path, "rb") as fh:
+        hdr = fh.read(_CACHE_HDR)
+        if len(hdr) < _CACHE_HDR or hdr[:8] != CACHE_MAGIC:
+            raise ParseError("not a commviz edge cache")
+        version, flags = (int(v) for v in np.frombuffer(hdr[8:16], "<u4"))
+        n, m = (int(v) for v in np.frombuffer(hdr[16:32], "<i8"))
+        if version != CACHE_VERSION:
+            raise ParseError(f"edge cache version {version} (expected {CACHE_VERSION})")
+        if n < 0 or m < 0:
+            raise ParseError("edge cache: negative sizes")
+        dt = np.dtype("<i8" if flags & 1 else "<i4")
+        body = np.fromfile(fh, dtype=dt, count=2 * m)
+    if body.size != 2 * m:
+        raise ParseError(f"edge cache truncated: {body.size // 2} of {m} edges")
+    edges = body.reshape(m, 2)
+    if m and (int(edges.min()) < 0 or int(edges.max()) >= n):
+        raise ParseError("edge cache: id outside [0, node_count)")
+    return n, edges
+
+
+def write_edge_cache(g: Graph, path) -> None:
+    """Write `g` (dense ids, stream order) as a binary edge cache that
+    `load_edge_list` reads back without parsing."""
+    _write_cache_arrays(path, g.node_count, g.edges)
+
+
+def read_edge_cache(path) -> Graph:
+    """Binary edge cache -> Graph (same node count, edges and degrees as the
+    graph that was written); the edges go straight to the GPU ingest."""
+    n, edges = _read_cache_arrays(path)
+    if len(edges) == 0:
+        raise ParseError("no edges")  # as for text (C/graph.py:86)
+    return from_edge_array(edges, node_count=n)
+
+
 def load_edge_list(path) -> Graph:
     """C/graph.py:95-97 (file bytes straight to the native tokenizer; a
-    non-ASCII file is decoded as utf-8 text exactly like the reference)."""
+    non-ASCII file is decoded as utf-8 text exactly like the reference).  A
+    binary edge cache (`write_edge_cache`) is recognised by its magic."""
     with open(path, "rb") as fh:
+        if fh.read(len(CACHE_MAGIC)) == CACHE_MAGIC:
+            return read_edge_cache(path)
+        fh.seek(0)
         data = fh.read()
     if data.isascii():
         g = _parse_native(data)

@@ -127,6 +127,53 @@ def test_tokenizer_edge_cases():
         assert gerr[1] == 3, text
 
 
+def test_edge_cache_format_round_trip(tmp_path):
+    """Binary edge cache: header + array round trip, int64
+    widening for ids >= 2^31, and the ParseErrors of a bad file (host only)."""
+    from paper_2108_00529_b200 import graph as G
+    rng = np.random.default_rng(3)
+    e = rng.integers(0, 1000, size=(5000, 2))
+    p = tmp_path / "g.cvzb"
+    G._write_cache_arrays(p, 1200, e)
+    n, back = G._read_cache_arrays(p)
+    assert n == 1200 and back.dtype == np.dtype("<i4") and np.array_equal(back, e)
+    assert p.stat().st_size == G._CACHE_HDR + e.size * 4
+    wide = np.array([[0, 2**33], [5, 7]])
+    G._write_cache_arrays(p, 2**33 + 1, wide)
+    n, back = G._read_cache_arrays(p)
+    assert n == 2**33 + 1 and back.dtype == np.dtype("<i8") and np.array_equal(back, wide)
+    raw = p.read_bytes()
+    for bad, msg in ((b"NOTCACHE" + raw[8:], "not a commviz edge cache"),
+                     (raw[:-8], "truncated"),
+                     (raw[:8] + b"\x02" + raw[9:], "version 2"),
+                     (raw[:8], "not a commviz edge cache")):
+        p.write_bytes(bad)
+        with pytest.raises(G.ParseError, match=msg):
+            G._read_cache_arrays(p)
+    G._write_cache_arrays(p, 3, np.array([[0, 5]]))
+    with pytest.raises(G.ParseError, match="outside"):
+        G._read_cache_arrays(p)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_edge_cache_load_matches_text(tmp_path):
+    import paper_2108_00529_b200 as cv
+    rng = np.random.default_rng(11)
+    text = random_text(rng, lines=4000)
+    g = cv.parse_edge_list(text)
+    p = tmp_path / "g.cvzb"
+    cv.write_edge_cache(g, p)
+    for h in (cv.load_edge_list(str(p)), cv.read_edge_cache(p)):
+        assert h.node_count == g.node_count
+        assert np.array_equal(h.edges, g.edges) and np.array_equal(h.degree, g.degree)
+    # isolated trailing ids survive (node_count comes from the header)
+    g2 = cv.from_edge_array(np.array([[0, 1], [1, 2]]), node_count=10)
+    cv.write_edge_cache(g2, p)
+    h = cv.load_edge_list(str(p))
+    assert h.node_count == 10 and h.degree.tolist() == [1, 2, 1] + [0] * 7
+
+
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
 def test_parse_edge_list_matches_oracle(tmp_path):
