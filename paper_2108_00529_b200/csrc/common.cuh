@@ -117,15 +117,17 @@ void pdl_launch(const char *name, void (*kernel)(KArgs...), dim3 grid, dim3 bloc
 
 // Cooperative launch (grid-wide barriers inside the kernel): the grid is the
 // number of CTAs that can be co-resident on all SMs.
+// `max_grid` > 0 caps the grid (kernels whose work is a known number of CTAs).
 template <class... KArgs, class... Args>
-void coop_launch(const char *name, void (*kernel)(KArgs...), int block, cudaStream_t s,
-                 Args... args) {
+void coop_launch_n(const char *name, void (*kernel)(KArgs...), unsigned max_grid, int block,
+                   cudaStream_t s, Args... args) {
     int per_sm = 0;
     CVZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0));
     int dev = 0, sms = 0;
     CVZ_CUDA(cudaGetDevice(&dev));
     CVZ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     dim3 grid((unsigned)(per_sm > 0 ? per_sm : 1) * (unsigned)sms);
+    if (max_grid > 0 && max_grid < grid.x) grid.x = max_grid;
     // arguments converted to the kernel's exact parameter types first
     std::tuple<typename std::decay<KArgs>::type...> typed(args...);
     void *argv[sizeof...(KArgs) > 0 ? sizeof...(KArgs) : 1];
@@ -138,8 +140,15 @@ void coop_launch(const char *name, void (*kernel)(KArgs...), int block, cudaStre
                                          argv, 0, s));
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
+template <class... KArgs, class... Args>
+void coop_launch(const char *name, void (*kernel)(KArgs...), int block, cudaStream_t s,
+                 Args... args) {
+    coop_launch_n(name, kernel, 0u, block, s, args...);
+}
 #define CVZ_COOP(kernel, block, stream, ...) \
     ::cvz::coop_launch(#kernel, kernel, (block), (stream), __VA_ARGS__)
+#define CVZ_COOP_N(kernel, max_grid, block, stream, ...) \
+    ::cvz::coop_launch_n(#kernel, kernel, (max_grid), (block), (stream), __VA_ARGS__)
 
 // Time a library primitive (CUB) under `name` (same rules as CVZ_LAUNCH).
 #define CVZ_REGION(name, stream) ::cvz::ProfScope _cvz_region(name, (stream))

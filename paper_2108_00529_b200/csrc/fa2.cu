@@ -25,6 +25,7 @@
 // swing, last block -> global speed] [update, clamp, disp max, bbox, last
 // block -> next bbox].  The whole iteration is captured once into a CUDA
 // graph and replayed `iterations` times; all scalars live on the device.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -1595,6 +1596,129 @@ unsigned persist_blocks(K kernel) {
 // ---------------------------------------------------------------------------
 // Tree workspace: everything one repulsion evaluation needs, preallocated so
 // an iteration can be captured in a CUDA graph.
+// ---- small-n tree-key sort ------------------------------------------------
+// Stable LSD radix sort of (klo, idx) pairs by bits [0, end_bit) in ONE
+// cooperative launch: 8-bit digits, one 2048-key tile per CTA, per pass
+//   tile -> smem digit histogram -> global [tile][digit] table -> grid sync
+//   -> every CTA scans the table for its own offsets -> block radix sort of
+//   the tile by the digit (stable) -> scatter -> grid sync.
+// Replaces CUB's onesweep (histogram + scan + memset + pass kernels, ~20 us
+// of fixed cost per pass at supergraph sizes) for n <= grid * 2048.
+// Passes ping-pong between `out` and `alt` so the last lands in `out`;
+// `in` is never written.  Result is identical to any stable sort.
+constexpr int TS_THREADS = 256;
+constexpr int TS_ITEMS = 8;
+constexpr int TS_TILE = TS_THREADS * TS_ITEMS;
+
+__global__ void __launch_bounds__(TS_THREADS) tree_sort_coop_kernel(
+    const unsigned *kin, const unsigned *vin, unsigned *kout,
+    unsigned *vout, unsigned *kalt, unsigned *valt, unsigned *hist, unsigned *prefix, int n,
+    int end_bit) {
+    namespace cg = cooperative_groups;
+    using Sort = cub::BlockRadixSort<unsigned, TS_THREADS, TS_ITEMS, unsigned>;
+    using Scan = cub::BlockScan<unsigned, TS_THREADS>;
+    __shared__ union {
+        typename Sort::TempStorage sort;
+        typename Scan::TempStorage scan;
+    } tmp;
+    __shared__ unsigned cnt[256], lstart[256], goff[256];
+    cg::grid_group grid = cg::this_grid();
+    griddep_wait();
+    const int tiles = (n + TS_TILE - 1) / TS_TILE;
+    const int c = blockIdx.x;
+    const int t = threadIdx.x;
+    const int base = c * TS_TILE;
+    const int count = c < tiles ? min(TS_TILE, n - base) : 0;
+    const int passes = (end_bit + 7) / 8;
+    const unsigned *ks = kin, *vs = vin;
+    for (int pass = 0; pass < passes; ++pass) {
+        const bool to_out = ((passes - 1 - pass) & 1) == 0;
+        unsigned *kd = to_out ? kout : kalt, *vd = to_out ? vout : valt;
+        const int b0 = 8 * pass, b1 = min(end_bit, b0 + 8);
+        const unsigned mask = (1u << (b1 - b0)) - 1u;
+        unsigned key[TS_ITEMS], val[TS_ITEMS];
+        cnt[t] = 0;
+        __syncthreads();
+        if (c < tiles) {
+#pragma unroll
+            for (int q = 0; q < TS_ITEMS; ++q) {
+                const int j = t * TS_ITEMS + q;  // blocked arrangement
+                if (j < count) {
+                    key[q] = __ldcg(ks + base + j);  // L2: written by other CTAs
+                    val[q] = __ldcg(vs + base + j);
+                    atomicAdd(&cnt[(key[q] >> b0) & mask], 1u);
+                } else {
+                    key[q] = 0xffffffffu;  // pads sort after every real key
+                    val[q] = 0u;
+                }
+            }
+        }
+        __syncthreads();
+        if (c < tiles) hist[(size_t)c * 256 + t] = cnt[t];
+        grid.sync();
+        // per digit, an exclusive scan over tiles (CTA g takes digits g,
+        // g + grid, ...): one L2 round trip per digit instead of a
+        // tiles-long dependent chain in every CTA
+        for (int d = c; d < 256; d += gridDim.x) {
+            unsigned run = 0;
+            for (int c0 = 0; c0 < tiles; c0 += TS_THREADS) {
+                const int cc = c0 + t;
+                const unsigned h = cc < tiles ? __ldcg(hist + (size_t)cc * 256 + d) : 0u;
+                unsigned ex, agg;
+                Scan(tmp.scan).ExclusiveSum(h, ex, agg);
+                __syncthreads();
+                if (cc < tiles) prefix[(size_t)cc * 256 + d] = run + ex;
+                run += agg;
+            }
+            if (t == 0) prefix[(size_t)tiles * 256 + d] = run;  // digit total
+        }
+        grid.sync();
+        if (c < tiles) {
+            const unsigned pre = __ldcg(prefix + (size_t)c * 256 + t);
+            const unsigned run = __ldcg(prefix + (size_t)tiles * 256 + t);
+            unsigned dbase;
+            Scan(tmp.scan).ExclusiveSum(run, dbase);
+            __syncthreads();
+            unsigned ls;
+            Scan(tmp.scan).ExclusiveSum(cnt[t], ls);
+            lstart[t] = ls;
+            goff[t] = dbase + pre;
+            __syncthreads();
+            Sort(tmp.sort).SortBlockedToStriped(key, val, b0, b1);
+#pragma unroll
+            for (int q = 0; q < TS_ITEMS; ++q) {
+                const int j = q * TS_THREADS + t;  // striped: sorted position
+                if (j < count) {
+                    const unsigned d = (key[q] >> b0) & mask;
+                    const unsigned dst = goff[d] + (unsigned)j - lstart[d];
+                    kd[dst] = key[q];
+                    vd[dst] = val[q];
+                }
+            }
+        }
+        if (pass + 1 < passes) grid.sync();
+        ks = kd;
+        vs = vd;
+    }
+}
+
+// Largest n the cooperative sort takes on this device (0 = unavailable).
+static int tree_sort_coop_cap() {
+    static int cap = -1;
+    if (cap < 0) {
+        int per_sm = 0, dev = 0, sms = 0, coop = 0;
+        CVZ_CUDA(cudaGetDevice(&dev));
+        CVZ_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        CVZ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CVZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tree_sort_coop_kernel,
+                                                               TS_THREADS, 0));
+        const char *e = getenv("CVZ_TREE_SORT");
+        const bool off = e && std::string(e) == "cub";
+        cap = (coop && !off) ? per_sm * sms * TS_TILE : 0;
+    }
+    return cap;
+}
+
 struct Tree {
     int n = 0;
     unsigned long long *khi, *khi3;
@@ -1629,6 +1753,8 @@ struct Tree {
     size_t etmp_sort = 0, etmp_scan = 0;
     void *tmp;
     size_t tmp_bytes;
+    unsigned *sort_alt = nullptr, *sort_hist = nullptr;  // cooperative small-n key sort
+    int tiles_ts = 0;
     void alloc(int n_, Scratch &sc) {
         n = n_;
         scr = &sc;
@@ -1667,6 +1793,11 @@ struct Tree {
         sy = sc.alloc<double>(ni);
         nodes = sc.alloc<TNode>(ni);
         tmp_bytes = sort_bytes<unsigned>(n, 32);
+        if (n <= tree_sort_coop_cap()) {
+            sort_alt = sc.alloc<unsigned>(2LL * n);
+            tiles_ts = (n + TS_TILE - 1) / TS_TILE;
+            sort_hist = sc.alloc<unsigned>((2 * (size_t)tiles_ts + 1) * 256);  // hist + prefix
+        }
         long_runs = sc.alloc<int>(n);
         nlong = sc.alloc<unsigned>(1);
         fix_k = sc.alloc<unsigned long long>(2LL * n);
@@ -1688,12 +1819,16 @@ struct Tree {
         size_t tb = tmp_bytes;
         // stable sort by the top 16 levels (4 radix passes), then the tie
         // fix-up orders bodies sharing a level-16 cell by the other 24 levels
-        {
+        if (sort_alt) {  // supergraph sizes: one cooperative launch
+            CVZ_COOP_N(tree_sort_coop_kernel, (unsigned)((n + TS_TILE - 1) / TS_TILE), TS_THREADS,
+                       s, klo, idx, klo2, idx2, sort_alt, sort_alt + n, sort_hist,
+                       sort_hist + tiles_ts * 256, n, 2 * top_digits);
+        } else {
             CVZ_REGION("cub_sort:tree_keys", s);
             CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, klo, klo2, idx, idx2, n, 0,
                                                      2 * top_digits, s));
+            count_launches(1 + (2 * top_digits + 7) / 8);
         }
-        count_launches(1 + (2 * top_digits + 7) / 8);
         CVZ_LAUNCH_PDL(tie_fixup_kernel, g, FB, 0, s, klo2, idx2, khi, n, long_runs, nlong);
         CVZ_LAUNCH_PDL(tie_fixup_long_kernel, num_sms(), 1024, 0, s, klo2, idx2, khi, n, long_runs,
                    nlong, fix_k, fix_i);
