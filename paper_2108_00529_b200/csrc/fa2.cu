@@ -440,12 +440,30 @@ __device__ DD3 block_scan_dd3(DD3 v, DD3 *warp_tot, DD3 &block_total) {
 
 // Gather the key-sorted bodies of one tile (bodies, 80-bit keys for karras)
 // and run the tile-local double-double prefix over them in the same CTA.
+// sorted 80-bit keys only (the split build: karras can start while the
+// bodies are gathered and prefix-summed on the main stream)
+__global__ void __launch_bounds__(FB) gather_keys_kernel(
+    const unsigned *__restrict__ idx, const unsigned *__restrict__ k32s,
+    const unsigned long long *__restrict__ krest, int n, unsigned long long *__restrict__ khi,
+    unsigned *__restrict__ klo, int top_digits) {
+    griddep_wait();
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        const unsigned long long r = krest[idx[p]];
+        khi[p] = ((unsigned long long)k32s[p] << (64 - 2 * top_digits)) | (r >> 16);
+        klo[p] = (unsigned)(r & 0xffffu) << 16;
+    }
+}
+
+__device__ __forceinline__ void dd_tiles_body(DD3 *__restrict__ tile_tot, int tiles);
+
+// khi == nullptr: keys already gathered (gather_keys_kernel); tile_ctr !=
+// nullptr: the last CTA to finish also scans the tile totals
 __global__ void __launch_bounds__(FB) gather_scan_kernel(
     const double2 *__restrict__ pos, const double *__restrict__ mass,
     const unsigned *__restrict__ idx, const unsigned *__restrict__ k32s,
     const unsigned long long *__restrict__ krest, int n, Body *__restrict__ bodies,
     unsigned long long *__restrict__ khi, unsigned *__restrict__ klo, DD3 *__restrict__ local,
-    DD3 *__restrict__ tile_tot, int top_digits) {
+    DD3 *__restrict__ tile_tot, int top_digits, unsigned *__restrict__ tile_ctr) {
     griddep_wait();
     __shared__ DD3 warp_tot[FB / 32];
     const long long base = (long long)blockIdx.x * TILE_DD + (long long)threadIdx.x * DD_ITEMS;
@@ -460,9 +478,11 @@ __global__ void __launch_bounds__(FB) gather_scan_kernel(
             double2 q = pos[i];
             double mi = mass[i];
             bodies[p] = Body{q.x, q.y, mi, (int)i, 0};
-            unsigned long long r = krest[i];
-            khi[p] = ((unsigned long long)k32s[p] << (64 - 2 * top_digits)) | (r >> 16);  // 0..31
-            klo[p] = (unsigned)(r & 0xffffu) << 16;                    // digits 32..39 on top
+            if (khi) {
+                unsigned long long r = krest[i];
+                khi[p] = ((unsigned long long)k32s[p] << (64 - 2 * top_digits)) | (r >> 16);
+                klo[p] = (unsigned)(r & 0xffffu) << 16;  // digits 32..39 on top
+            }
             v = DD3{DD{mi, 0.0}, DD{mul(mi, q.x), 0.0}, DD{mul(mi, q.y), 0.0}};
         }
         acc = dd3_add(acc, v);
@@ -487,6 +507,18 @@ __global__ void __launch_bounds__(FB) gather_scan_kernel(
         if (i < n) local[i] = dd3_add(excl, item[j]);
     }
     if (threadIdx.x == 0) tile_tot[blockIdx.x] = total;
+    if (tile_ctr) {  // last CTA scans the tile totals (threadfence-reduction pattern)
+        __shared__ bool last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(tile_ctr, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            dd_tiles_body(tile_tot, gridDim.x);
+            if (threadIdx.x == 0) *tile_ctr = 0u;  // ready for the next replay
+        }
+    }
 }
 
 // exclusive scan of the tile totals, one CTA
@@ -539,6 +571,19 @@ __global__ void __launch_bounds__(FB) karras_tiles_kernel(Keys K, int *__restric
     }
     karras_body(blockIdx.x, gridDim.x - 1, K, left, first, last, delta_out, parent_int,
                 parent_leaf, pdelta, rc_by_split);
+}
+
+__global__ void __launch_bounds__(FB) karras_only_kernel(Keys K, int *__restrict__ left,
+                                                         int *__restrict__ first,
+                                                         int *__restrict__ last,
+                                                         int *__restrict__ delta_out,
+                                                         int *__restrict__ parent_int,
+                                                         int *__restrict__ parent_leaf,
+                                                         int *__restrict__ pdelta,
+                                                         int *__restrict__ rc_by_split) {
+    griddep_wait();
+    karras_body(blockIdx.x, gridDim.x, K, left, first, last, delta_out, parent_int, parent_leaf,
+                pdelta, rc_by_split);
 }
 
 __global__ void node_sums_kernel(int n, const DD3 *__restrict__ local,
@@ -1742,6 +1787,7 @@ struct Tree {
     double *bbox = nullptr;
     unsigned *jflag = nullptr;
     unsigned *wctr = nullptr;  // work counter of the persistent BH walk
+    unsigned *tile_ctr = nullptr;  // last-CTA counter of gather_scan (split build)
     // reference cell numbering (allocated on first use)
     Scratch *scr = nullptr;
     int ne = 0;
@@ -1770,6 +1816,8 @@ struct Tree {
         jflag = sc.alloc<unsigned>(1);
         CVZ_CUDA(cudaMemsetAsync(jflag, 0, sizeof(unsigned), sc.stream()));
         wctr = sc.alloc<unsigned>(1);
+        tile_ctr = sc.alloc<unsigned>(1);
+        CVZ_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned), sc.stream()));
         khi = sc.alloc<unsigned long long>(n);
         khi3 = sc.alloc<unsigned long long>(n);
         klo = sc.alloc<unsigned>(n);
@@ -1805,7 +1853,11 @@ struct Tree {
         tmp = sc.alloc<char>(tmp_bytes);
     }
     // build from pos + bbox (bbox already on device)
-    void build(const double2 *pos, const double *mass, const double *bbox_, cudaStream_t s) {
+    // aux != nullptr: karras runs on `aux` while the bodies are gathered and
+    // prefix-summed on `s` (fork ev_a, join ev_b; both captured into the graph)
+    void build(const double2 *pos, const double *mass, const double *bbox_, cudaStream_t s,
+               cudaStream_t aux = nullptr, cudaEvent_t ev_a = nullptr,
+               cudaEvent_t ev_b = nullptr) {
         bbox = const_cast<double *>(bbox_);
         unsigned g = grid_for(n, FB, 1, 8);
         // radix-sorted levels: 12 (3 passes) measured best for supergraph-sized
@@ -1833,15 +1885,32 @@ struct Tree {
         CVZ_LAUNCH_PDL(tie_fixup_long_kernel, num_sms(), 1024, 0, s, klo2, idx2, khi, n, long_runs,
                    nlong, fix_k, fix_i);
         const int tiles = (n + TILE_DD - 1) / TILE_DD;
-        CVZ_LAUNCH_PDL(gather_scan_kernel, tiles, FB, 0, s, pos, mass, idx2, klo2, khi, n, bodies,
-                       khi3, klo3, prefix, tile_tot, top_digits);
         Keys K{khi3, klo3, n};
-        CVZ_LAUNCH_PDL(karras_tiles_kernel, grid_for(n - 1, FB, 1, 8) + 1, FB, 0, s, K, left,
-                       first, last, delta, parent_int, parent_leaf, pdelta, rc_by_split, tile_tot,
-                       tiles);
-        CVZ_LAUNCH_PDL(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix, tile_tot,
+        if (aux) {
+            CVZ_LAUNCH_PDL(gather_keys_kernel, g, FB, 0, s, idx2, klo2, khi, n, khi3, klo3,
+                           top_digits);
+            CVZ_CUDA(cudaEventRecord(ev_a, s));
+            CVZ_CUDA(cudaStreamWaitEvent(aux, ev_a, 0));
+            CVZ_LAUNCH(karras_only_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, aux, K, left, first,
+                       last, delta, parent_int, parent_leaf, pdelta, rc_by_split);
+            CVZ_CUDA(cudaEventRecord(ev_b, aux));
+            CVZ_LAUNCH(gather_scan_kernel, tiles, FB, 0, s, pos, mass, idx2, klo2, khi, n, bodies,
+                       (unsigned long long *)nullptr, (unsigned *)nullptr, prefix, tile_tot,
+                       top_digits, tile_ctr);
+            CVZ_CUDA(cudaStreamWaitEvent(s, ev_b, 0));
+            CVZ_LAUNCH(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix, tile_tot,
                        left, first, last, delta, pdelta, rc_by_split, bbox, smass, sx, sy, nodes,
                        flat() ? pcnt : nullptr);
+        } else {
+            CVZ_LAUNCH_PDL(gather_scan_kernel, tiles, FB, 0, s, pos, mass, idx2, klo2, khi, n,
+                           bodies, khi3, klo3, prefix, tile_tot, top_digits, (unsigned *)nullptr);
+            CVZ_LAUNCH_PDL(karras_tiles_kernel, grid_for(n - 1, FB, 1, 8) + 1, FB, 0, s, K, left,
+                           first, last, delta, parent_int, parent_leaf, pdelta, rc_by_split,
+                           tile_tot, tiles);
+            CVZ_LAUNCH_PDL(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix,
+                           tile_tot, left, first, last, delta, pdelta, rc_by_split, bbox, smass, sx,
+                           sy, nodes, flat() ? pcnt : nullptr);
+        }
         if (flat()) {
             {
                 CVZ_REGION("cub_scan:preorder", s);
@@ -2354,6 +2423,15 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                 cudaEventDestroy(b);
             }
         } side_guard{side, ev_fork, ev_join};
+        // karras of the tree build runs on a second side stream
+        cudaStream_t aux;
+        CVZ_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+        cudaEvent_t ev_ka, ev_kb;
+        CVZ_CUDA(cudaEventCreateWithFlags(&ev_ka, cudaEventDisableTiming));
+        CVZ_CUDA(cudaEventCreateWithFlags(&ev_kb, cudaEventDisableTiming));
+        SideGuard aux_guard{aux, ev_ka, ev_kb};
+        static const bool split_build = getenv("CVZ_TREE_SPLIT") == nullptr ||
+                                        std::string(getenv("CVZ_TREE_SPLIT")) != "0";
         auto one_iteration = [&](cudaStream_t st, bool ids) {
             CVZ_CUDA(cudaEventRecord(ev_fork, st));
             CVZ_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
@@ -2363,7 +2441,10 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                 CVZ_LAUNCH(exact_kernel, blocks_for(n, XT), XT, 0, st, p2, mass, N, P->repulsion,
                            frep, 0, N);
             } else {
-                tree.build(p2, mass, bbox, st);
+                if (split_build)
+                    tree.build(p2, mass, bbox, st, aux, ev_ka, ev_kb);
+                else
+                    tree.build(p2, mass, bbox, st);
                 if (ids) tree.build_ids(st);
                 tree.repulse(P->repulsion, P->theta, frep, badp, ids, st);
             }
