@@ -277,7 +277,7 @@ def run_ours(args, rank, ws):
         t1.record()
         torch.cuda.synchronize()
     launches = (_native.launch_count() - launches0) // args.steps
-    ms = t1.elapsed_time(t0) * -1 if False else t0.elapsed_time(t1)
+    ms = t0.elapsed_time(t1)
     ms_step = barrier_max(ms / args.steps, ws)
     barrier(ws)
     # per-stage breakdown of one extra plain step (CUDA events between the
@@ -288,6 +288,9 @@ def run_ours(args, rank, ws):
     st = stats[0]
     with _native.profile() as prof:
         pipeline(cv, dev)
+    # Barnes-Hut walk statistics from one more step with the instrumented
+    # walk variant (interactions beside the bytes)
+    _, bh_visits, bh_inter = _native.bh_stats(lambda: pipeline(cv, dev))
     # fast (racy) community mode, same graph: detect stage only
     g = cv.from_edge_array(dev)
     base = cv.degree_stats(g).mode_degree
@@ -320,6 +323,7 @@ def run_ours(args, rank, ws):
     h2d = host_np.nbytes
     d2h = pos.nbytes + lab.nbytes
     return dict(ms_step=ms_step, m_in=m_in, stage=st, launches=launches, clocks=clk.summary(),
+                bh_visits=bh_visits / ITERS, bh_inter=bh_inter / ITERS,
                 e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, prof=prof.kernels, fast=fast)
 
 
@@ -507,6 +511,15 @@ def main():
     peak, _src = peak_hbm()
     roof, top = roofline(r["prof"], st, peak)
     roof["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs ({_src})"
+    if roof.get("kernel", "").startswith("bh_flat") and r.get("bh_inter"):
+        # per-iteration walk counts (instrumented step) over the timed walk:
+        # ~20 fp64 flops per accepted term (d, 1/d^2 seed + cubic step, f,
+        # f*d accumulate), ~6 per opened cell (d, d^2, theta^2 d^2 test)
+        sec = roof["launch_ms"] / 1e3
+        acc, vis = r["bh_inter"], r["bh_visits"]
+        roof["walk"] = {"node_visits_per_iter": vis, "interactions_per_iter": acc,
+                        "interactions_per_s": acc / sec,
+                        "fp64_gflops_est": (20 * acc + 6 * (vis - acc)) / sec / 1e9}
     try:  # DRAM bytes per launch from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             roof["traffic"] = json.load(fh).get(roof["kernel"])

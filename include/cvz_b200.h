@@ -57,6 +57,15 @@ int cvz_profile_begin(void);
 int cvz_profile_end(void);
 const char *cvz_profile_report(void);
 
+/* Barnes-Hut walk statistics ("report BH interactions").
+ * enable = 1 zeroes two device counters and makes every following per-thread
+ * walk launch the instrumented kernel variant, which adds its node visits and
+ * accepted interactions (force terms) to them; enable = 0 turns it off and
+ * writes {visits, interactions} to totals (may be NULL).  Synchronises the
+ * device.  Measurement only: the timed walk is never the counting variant.
+ * No reference counterpart. */
+int cvz_bh_stats(int enable, unsigned long long *totals);
+
 /* ---------------------------------------------------------------- graph */
 
 /* C/graph.py:114-122 from_edge_array (mask u==v keeping stream order) and

@@ -45,6 +45,7 @@ SIGNATURES = {
     "cvz_profile_begin": [],
     "cvz_profile_end": [],
     "cvz_profile_report": [],
+    "cvz_bh_stats": [_I32, _P],
     "cvz_edges_compact": [_P, _I32, _I64, _P, _P, _P, _I32, _P],
     "cvz_degree_count": [_P, _I64, _I64, _P, _P],
     "cvz_degree_stats": [_P, _I64, _P, _P],
@@ -120,6 +121,18 @@ def load():
 
 def launch_count() -> int:
     return int(load().cvz_launch_count())
+
+
+def bh_stats(fn):
+    """Run fn() with the instrumented BH walk; returns (result, visits,
+    interactions) summed over every walk launched inside (cvz_bh_stats)."""
+    check(load().cvz_bh_stats(1, None), "cvz_bh_stats")
+    tot = (ctypes.c_ulonglong * 2)()
+    try:
+        out = fn()
+    finally:
+        check(load().cvz_bh_stats(0, ctypes.cast(tot, ctypes.c_void_p)), "cvz_bh_stats")
+    return out, int(tot[0]), int(tot[1])
 
 
 class profile:

@@ -1111,14 +1111,18 @@ __device__ __forceinline__ double2 aggregate_add(const Walker w, const PNode t, 
 }
 
 // per-thread walk: one body per thread, bodies in key order
-template <int NT, int MINB>
+// COUNT: also tally node visits and accepted (force) terms into stats[0..1]
+// (cvz_bh_stats; an instrumentation variant, never the timed walk)
+template <int NT, int MINB, bool COUNT = false>
 __global__ void __launch_bounds__(NT, MINB) bh_flat_kernel(Walker w, const PNode *__restrict__ pn,
                                                      const unsigned *__restrict__ cle, double kr,
                                                      double th2, double eps2,
                                                      double2 *__restrict__ out,
                                                      const long long *__restrict__ bad,
                                                      const int *__restrict__ work,
-                                                     const int *__restrict__ nwork) {
+                                                     const int *__restrict__ nwork,
+                                                     unsigned long long *__restrict__ stats = nullptr) {
+    unsigned long long n_visit = 0, n_acc = 0;
     // th2 = theta * theta and eps2 = COINCIDE_EPS^2 come in as launch
     // parameters so the hot loop reads them as constant-bank operands
     griddep_wait();
@@ -1147,7 +1151,9 @@ __global__ void __launch_bounds__(NT, MINB) bh_flat_kernel(Walker w, const PNode
         while (c >= 0) {
             const PNode t = pn[c];
             const int kind = t.meta & 3;
+            if (COUNT) ++n_visit;
             if (kind == 2) {
+                if (COUNT) ++n_acc;
                 double2 r = aggregate_add(w, t, c, p, i, xi, yi, mi, kmi, fx, fy);
                 fx = r.x;
                 fy = r.y;
@@ -1167,10 +1173,12 @@ __global__ void __launch_bounds__(NT, MINB) bh_flat_kernel(Walker w, const PNode
                 }
             }
             if (d2 >= eps2) {
+                if (COUNT) ++n_acc;
                 const double f = mul(mul(kmi, t.m), inv_d2(d2));
                 fx = add(fx, mul(f, dx));
                 fy = add(fy, mul(f, dy));
-            } else if (c != self) {  // j == i skipped (:237-238); a leaf stores its
+            } else if (c != self) {
+                if (COUNT) ++n_acc;  // j == i skipped (:237-238); a leaf stores its
                                      // body's exact position, so self has d2 == 0
                 double2 r = jitter_add(w.bodies, w.n, w.aux, w.cr, th2, c, kind, i, kmi, t.m, dx,
                                        dy, d2, false, fx, fy);
@@ -1180,6 +1188,16 @@ __global__ void __launch_bounds__(NT, MINB) bh_flat_kernel(Walker w, const PNode
             c = t.skip;
         }
         out[i] = make_double2(fx, fy);
+    }
+    if (COUNT) {
+        for (int o = 16; o > 0; o >>= 1) {
+            n_visit += __shfl_xor_sync(0xffffffffu, n_visit, o);
+            n_acc += __shfl_xor_sync(0xffffffffu, n_acc, o);
+        }
+        if (lane_id() == 0) {
+            atomicAdd(stats, n_visit);
+            atomicAdd(stats + 1, n_acc);
+        }
     }
 }
 
@@ -1641,6 +1659,9 @@ unsigned persist_blocks(K kernel) {
 // ---------------------------------------------------------------------------
 // Tree workspace: everything one repulsion evaluation needs, preallocated so
 // an iteration can be captured in a CUDA graph.
+// device counters of the instrumented walk (nullptr = off; cvz_bh_stats)
+static unsigned long long *g_bh_stats = nullptr;
+
 // ---- small-n tree-key sort ------------------------------------------------
 // Stable LSD radix sort of (klo, idx) pairs by bits [0, end_bit) in ONE
 // cooperative launch: 8-bit digits, one 2048-key tile per CTA, per pass
@@ -1990,7 +2011,7 @@ struct Tree {
             ::cvz::pdl_launch(NT == FB ? "bh_flat_kernel<" #B ">" : "bh_flat_kernel<NT," #B ">", \
                               bh_flat_kernel<NT, B>, dim3(blocks_for(n, NT)), dim3(NT), 0, s, \
                               w, pn, pcle, kr, theta * theta, EPS * EPS, out, bad, work,     \
-                              nwork);                                                        \
+                              nwork, (unsigned long long *)nullptr);                         \
     } while (0)
             if (bnt == 64) {
                 constexpr int NT = 64;
@@ -1998,6 +2019,10 @@ struct Tree {
             } else if (bnt == 128) {
                 constexpr int NT = 128;
                 CVZ_BH_FLAT(10);
+            } else if (g_bh_stats && minb == 5) {  // instrumented walk (cvz_bh_stats)
+                ::cvz::pdl_launch("bh_flat_kernel<count>", bh_flat_kernel<FB, 5, true>,
+                                  dim3(blocks_for(n, FB)), dim3(FB), 0, s, w, pn, pcle, kr,
+                                  theta * theta, EPS * EPS, out, bad, work, nwork, g_bh_stats);
             } else {
                 constexpr int NT = FB;
                 if (minb >= 6)
@@ -2525,6 +2550,27 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                                             std::to_string(out.bad) +
                                             "; reduce speed or check input weights");
         CVZ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int cvz_bh_stats(int enable, unsigned long long *totals) {
+    return guard([&] {
+        CVZ_CUDA(cudaDeviceSynchronize());
+        if (enable) {
+            if (!g_bh_stats) CVZ_CUDA(cudaMalloc(&g_bh_stats, 2 * sizeof(unsigned long long)));
+            CVZ_CUDA(cudaMemset(g_bh_stats, 0, 2 * sizeof(unsigned long long)));
+        } else if (g_bh_stats) {
+            unsigned long long h[2];
+            CVZ_CUDA(cudaMemcpy(h, g_bh_stats, sizeof(h), cudaMemcpyDeviceToHost));
+            CVZ_CUDA(cudaFree(g_bh_stats));
+            g_bh_stats = nullptr;
+            if (totals) {
+                totals[0] = h[0];
+                totals[1] = h[1];
+            }
+        } else if (totals) {
+            totals[0] = totals[1] = 0;
+        }
     });
 }
 

@@ -441,6 +441,26 @@ def test_bh_vs_exact_properties(cv):
     assert errs[0].mean() > errs[1].mean() > errs[2].mean()
 
 
+def test_bh_walk_stats(cv):
+    """cvz_bh_stats: the instrumented walk returns the same forces and counts
+    n(n-1) interactions when no cell can be accepted."""
+    from paper_2108_00529_b200 import _native
+    rng = np.random.default_rng(5)
+    n = 5000
+    pos = rng.uniform(-100, 100, (n, 2))
+    mass = rng.uniform(1, 5, n)
+    plain = cv.repulsion_forces(pos, mass, 80.0, 0.5)
+    counted, vis, inter = _native.bh_stats(lambda: cv.repulsion_forces(pos, mass, 80.0, 0.5))
+    assert np.array_equal(plain, counted)
+    assert n <= inter <= vis
+    k = 500
+    _, vis2, inter2 = _native.bh_stats(
+        lambda: cv.repulsion_forces(pos[:k], mass[:k], 80.0, 1e-6))
+    assert inter2 == k * (k - 1) and vis2 > inter2
+    _, vis3, inter3 = _native.bh_stats(lambda: None)  # nothing launched
+    assert vis3 == inter3 == 0
+
+
 def test_bh_large_vs_oracle(cv, orc):
     rng = np.random.default_rng(11)
     n = 200_000
