@@ -333,6 +333,46 @@ __global__ void direct_parents_kernel(const unsigned *__restrict__ key,
     }
 }
 
+// Same results, one pass per node: the thread holding a segment's first
+// slot walks x's (<= b <= T) active slots forward, carrying the last write,
+// so each active slot's role is read once (the per-slot kernel above
+// rescans up to b - 1 predecessors for every reading slot).
+constexpr int DP_BATCH = 8;
+// One thread per node: seg_start[x] is only written for nodes that have
+// slots this round, so it is validated against the sorted keys (in range,
+// key[st] == x, key[st - 1] != x) before use.
+__global__ void node_parents_kernel(const unsigned *__restrict__ key,
+                                    const unsigned *__restrict__ val, long long ns, unsigned n,
+                                    const int *__restrict__ seg_start,
+                                    const int *__restrict__ seg_end,
+                                    const long long *__restrict__ d0, long long T,
+                                    const signed char *__restrict__ role,
+                                    int *__restrict__ parent, int *__restrict__ finalw) {
+    for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+        const long long i = seg_start[x];
+        if (i < 0 || i >= ns || key[i] != x || (i > 0 && key[i - 1] == x)) continue;
+        const long long b = T - (d0 ? d0[x] : 0);
+        const long long end = min((long long)seg_end[x], i + b);
+        if (end <= i) continue;
+        int last = -1;
+        for (long long j0 = i; j0 < end; j0 += DP_BATCH) {
+            unsigned sv[DP_BATCH];
+            signed char ro[DP_BATCH];
+#pragma unroll
+            for (int q = 0; q < DP_BATCH; ++q) sv[q] = j0 + q < end ? val[j0 + q] : 0u;
+#pragma unroll
+            for (int q = 0; q < DP_BATCH; ++q) ro[q] = j0 + q < end ? role[sv[q] >> 1] : -1;
+#pragma unroll
+            for (int q = 0; q < DP_BATCH; ++q) {
+                const signed char e = (signed char)(sv[q] & 1);
+                if (ro[q] >= 0 && ro[q] != e) parent[sv[q] >> 1] = last;  // event reads x
+                if (ro[q] == e) last = (int)(sv[q] >> 1);                 // event writes x
+            }
+        }
+        finalw[x] = last;
+    }
+}
+
 // events: origin[k] = node whose initial label event k carries (-1 pending)
 __global__ void events_init_kernel(const int2 *__restrict__ E, long long m,
                                    const signed char *__restrict__ role,
@@ -975,7 +1015,11 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
         //    large thresholds (quadratic scans) a segmented "last write so
         //    far" max-scan over all node-sorted slots
         int *parent = sc.alloc<int>(m);
-        if (T <= DIRECT_PARENTS_MAX_T) {
+        static const bool slot_parents = getenv("CVZ_PARENTS_SLOT") != nullptr;
+        if (T <= DIRECT_PARENTS_MAX_T && !slot_parents) {
+            CVZ_LAUNCH(node_parents_kernel, grid_for(n, TB, 1, 16), TB, 0, s, skeys, svals, ns,
+                       (unsigned)n, seg_start, seg_end, d0p, T, role, parent, finalw);
+        } else if (T <= DIRECT_PARENTS_MAX_T) {
             CVZ_LAUNCH(direct_parents_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, svals, ns,
                        (unsigned)n, seg_start, seg_end, d0p, T, role, parent, finalw);
         } else {
