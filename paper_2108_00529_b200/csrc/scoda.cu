@@ -167,14 +167,35 @@ __global__ void fill_kernel(CT *__restrict__ a, long long len, CT v) {
         a[i] = v;
 }
 
+// four sorted keys per thread (one 16-byte load; the neighbours across the
+// group edges come from two scalar loads that hit L1/L2)
 __global__ void seg_bounds_kernel(const unsigned *__restrict__ key, long long ns, unsigned n,
                                   int *__restrict__ seg_start, int *__restrict__ seg_end) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ns;
-         i += (long long)gridDim.x * blockDim.x) {
-        unsigned x = key[i];
-        if (x >= n) continue;
-        if (i == 0 || key[i - 1] != x) seg_start[x] = (int)i;
-        if (i == ns - 1 || key[i + 1] != x) seg_end[x] = (int)(i + 1);
+    const long long groups = (ns + 3) / 4;
+    for (long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x; gi < groups;
+         gi += (long long)gridDim.x * blockDim.x) {
+        const long long i0 = 4 * gi;
+        unsigned k[6];  // k[0] = key[i0 - 1], k[1..4] = key[i0..i0+3], k[5] = key[i0 + 4]
+        if (i0 + 4 <= ns) {
+            const uint4 v = reinterpret_cast<const uint4 *>(key)[gi];
+            k[1] = v.x;
+            k[2] = v.y;
+            k[3] = v.z;
+            k[4] = v.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) k[1 + q] = i0 + q < ns ? key[i0 + q] : 0xffffffffu;
+        }
+        k[0] = i0 > 0 ? key[i0 - 1] : 0xffffffffu;
+        k[5] = i0 + 4 < ns ? key[i0 + 4] : 0xffffffffu;
+#pragma unroll
+        for (int q = 1; q <= 4; ++q) {
+            const long long i = i0 + q - 1;
+            const unsigned x = k[q];
+            if (i >= ns || x >= n) continue;
+            if (i == 0 || k[q - 1] != x) seg_start[x] = (int)i;
+            if (i == ns - 1 || k[q + 1] != x) seg_end[x] = (int)(i + 1);
+        }
     }
 }
 
@@ -996,7 +1017,7 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
         if (ns > 0)
             cub_sort_pairs_db(skeys, sc.alloc<unsigned>(ns), svals, sc.alloc<unsigned>(ns), ns,
                               bits_for_value((unsigned long long)n), sc, s);
-        CVZ_LAUNCH(seg_bounds_kernel, grid_for(ns, TB, 1, 16), TB, 0, s, skeys, ns, (unsigned)n,
+        CVZ_LAUNCH(seg_bounds_kernel, grid_for((ns + 3) / 4, TB, 1, 16), TB, 0, s, skeys, ns, (unsigned)n,
                    seg_start, seg_end);
         // 3. post-increment counters (dead slots: T + 1)
         CT *cval = sc.alloc<CT>(ns_all);
