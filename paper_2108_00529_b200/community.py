@@ -257,6 +257,7 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
     a = CommunityAssignment(label=Dual(dev=node_lab), counter_degree=Dual(dev=deg),
                             round_history=_History(history))
     a.stream_edges = streamed
+    a._label.prefetch()  # the labels reach the host while later stages run
     return a
 
 
