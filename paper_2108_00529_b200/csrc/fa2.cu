@@ -1995,8 +1995,9 @@ struct Tree {
         if (flat()) {
             static const int minb = getenv("CVZ_BH_MINB") ? atoi(getenv("CVZ_BH_MINB")) : 5;
             static const int bnt = getenv("CVZ_BH_NT") ? atoi(getenv("CVZ_BH_NT")) : 256;
-// per-thread walk by default; CVZ_BH_WARP=1 forces the warp-cooperative
-            // walk, CVZ_BH_WARP=auto picks it for large n (clustered full graphs)
+            // per-thread walk by default (it beats the warp-cooperative walk on
+            // both supergraphs and full graphs); CVZ_BH_WARP=1 forces the warp
+            // walk, CVZ_BH_WARP=auto picks it for n >= 2^21
             static const char *wenv = getenv("CVZ_BH_WARP");
             const bool warp = wenv && (std::string(wenv) == "1" ||
                                        (std::string(wenv) == "auto" && n >= (1 << 21)));
