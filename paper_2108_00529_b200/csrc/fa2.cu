@@ -1207,8 +1207,8 @@ __global__ void __launch_bounds__(NT, MINB) bh_flat_kernel(Walker w, const PNode
 // c: after accepting c it resumes at c.skip (preorder: c's subtree is
 // [c, skip)).  The warp descends iff some active lane opens, so each lane
 // visits exactly its per-thread traversal in the same order (identical
-// sums).  Wins when a warp's bodies are tightly clustered (full-graph
-// layouts); persistent CTAs pull 32-body groups from a counter.
+// sums).  Meant for tightly clustered warps (measured slower than the
+// per-thread walk at C4, supergraph and full graph; CVZ_BH_WARP=1).
 template <int MINB>
 __global__ void __launch_bounds__(FB, MINB) bh_warp_kernel(Walker w, const PNode *__restrict__ pn,
                                                      const unsigned *__restrict__ cle, double kr,
