@@ -537,6 +537,10 @@ def main():
                    "parallelism": f"replicas x{ws}",
                    "l2": "inputs (262 MB edge list) larger than the 126 MB L2"},
         "community_pass_edges_per_s": st["m"] / (st["detect_ms"] / 1000.0),
+        # also the streamed edges summed over rounds per second
+        "community_pass_stream_edges_per_s": sum(st["m_r"]) / (st["detect_ms"] / 1000.0),
+        # sketch sizing + supergraph contraction, per input edge
+        "sketch_contract_edges_per_s": st["m"] / (st["contract_ms"] / 1000.0),
         "ms_per_fa2_iter": st["layout_ms"] / ITERS,
         "end_to_end_s": r["ms_step"] / 1000.0,
         "stage_ms": {k: st[k] for k in ("ingest_ms", "detect_ms", "contract_ms", "layout_ms")},
