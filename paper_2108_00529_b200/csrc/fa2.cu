@@ -1551,31 +1551,42 @@ __global__ void __launch_bounds__(FB) update_kernel(
         c = p.y;
         d = p.y;
     }
-    // block max |disp| (non-negative doubles order like their bit patterns)
+    // block max |disp| and bbox: min/max are order-free, so warp shuffles
+    // then one smem pass over the 8 warp results give the exact values
     __shared__ double sm[FB], s0[FB], s1[FB], s2[FB], s3[FB];
-    sm[threadIdx.x] = nrm;
-    s0[threadIdx.x] = a;
-    s1[threadIdx.x] = b;
-    s2[threadIdx.x] = c;
-    s3[threadIdx.x] = d;
     bool anybad = __syncthreads_or(!fin);
-    for (int o = FB / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) {
-            sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + o]);
-            s0[threadIdx.x] = fmin(s0[threadIdx.x], s0[threadIdx.x + o]);
-            s1[threadIdx.x] = fmax(s1[threadIdx.x], s1[threadIdx.x + o]);
-            s2[threadIdx.x] = fmin(s2[threadIdx.x], s2[threadIdx.x + o]);
-            s3[threadIdx.x] = fmax(s3[threadIdx.x], s3[threadIdx.x + o]);
-        }
-        __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) {
+        nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
+        a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+        c = fmin(c, __shfl_xor_sync(0xffffffffu, c, o));
+        d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
     }
+    __shared__ double wr[5][FB / 32];
+    const int wid = threadIdx.x >> 5;
+    if (lane_id() == 0) {
+        wr[0][wid] = nrm;
+        wr[1][wid] = a;
+        wr[2][wid] = b;
+        wr[3][wid] = c;
+        wr[4][wid] = d;
+    }
+    __syncthreads();
     __shared__ bool last;
     if (threadIdx.x == 0) {
-        bpart[5 * blockIdx.x + 0] = s0[0];
-        bpart[5 * blockIdx.x + 1] = s1[0];
-        bpart[5 * blockIdx.x + 2] = s2[0];
-        bpart[5 * blockIdx.x + 3] = s3[0];
-        bpart[5 * blockIdx.x + 4] = anybad ? -1.0 : sm[0];
+        double m0 = wr[0][0], m1 = wr[1][0], m2 = wr[2][0], m3 = wr[3][0], m4 = wr[4][0];
+        for (int w = 1; w < FB / 32; ++w) {
+            m0 = fmax(m0, wr[0][w]);
+            m1 = fmin(m1, wr[1][w]);
+            m2 = fmax(m2, wr[2][w]);
+            m3 = fmin(m3, wr[3][w]);
+            m4 = fmax(m4, wr[4][w]);
+        }
+        bpart[5 * blockIdx.x + 0] = m1;
+        bpart[5 * blockIdx.x + 1] = m2;
+        bpart[5 * blockIdx.x + 2] = m3;
+        bpart[5 * blockIdx.x + 3] = m4;
+        bpart[5 * blockIdx.x + 4] = anybad ? -1.0 : m0;
         __threadfence();
         last = atomicAdd(ctr, 1u) == gridDim.x - 1;
     }
