@@ -1459,22 +1459,27 @@ __global__ void __launch_bounds__(FB) forces_kernel(
         s_sw = sw;
         s_tr = mul(mu, tot) / 2.0;
     }
-    // deterministic block reduction
+    // deterministic block reduction: fixed butterfly within each warp, then
+    // the 8 warp sums in warp order
     __shared__ double a[FB], b[FB];
-    a[threadIdx.x] = s_sw;
-    b[threadIdx.x] = s_tr;
-    __syncthreads();
-    for (int o = FB / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) {
-            a[threadIdx.x] += a[threadIdx.x + o];
-            b[threadIdx.x] += b[threadIdx.x + o];
-        }
-        __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) {
+        s_sw += __shfl_xor_sync(0xffffffffu, s_sw, o);
+        s_tr += __shfl_xor_sync(0xffffffffu, s_tr, o);
     }
+    if (lane_id() == 0) {
+        a[threadIdx.x >> 5] = s_sw;
+        b[threadIdx.x >> 5] = s_tr;
+    }
+    __syncthreads();
     __shared__ bool last;
     if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = a[0];
-        part[2 * blockIdx.x + 1] = b[0];
+        double bs = a[0], bt = b[0];
+        for (int w = 1; w < FB / 32; ++w) {
+            bs += a[w];
+            bt += b[w];
+        }
+        part[2 * blockIdx.x] = bs;
+        part[2 * blockIdx.x + 1] = bt;
         __threadfence();
         last = atomicAdd(ctr, 1u) == gridDim.x - 1;
     }
