@@ -1298,17 +1298,25 @@ __global__ void __launch_bounds__(XT) exact_kernel(const double2 *__restrict__ p
 
 // ---- CSR for attraction ------------------------------------------------------
 __global__ void half_edges_kernel(const int2 *__restrict__ e, long long m,
-                                  unsigned *__restrict__ key, unsigned *__restrict__ val,
-                                  unsigned *__restrict__ cnt) {
+                                  unsigned *__restrict__ key, unsigned *__restrict__ val) {
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
          k += (long long)gridDim.x * blockDim.x) {
         int2 p = e[k];
-        key[2 * k] = (unsigned)p.x;
-        key[2 * k + 1] = (unsigned)p.y;
-        val[2 * k] = (unsigned)(2 * k);
-        val[2 * k + 1] = (unsigned)(2 * k + 1);
-        atomicAdd(cnt + p.x, 1u);
-        atomicAdd(cnt + p.y, 1u);
+        reinterpret_cast<uint2 *>(key)[k] = make_uint2((unsigned)p.x, (unsigned)p.y);
+        reinterpret_cast<uint2 *>(val)[k] = make_uint2((unsigned)(2 * k), (unsigned)(2 * k + 1));
+    }
+}
+
+// rowptr from the node-sorted half-edge keys (no per-node atomics: hub rows
+// serialised them): rows (skey[i-1], skey[i]] start at i, rows past the last
+// key at nh; every one of the n + 1 entries is written exactly once.
+__global__ void rowptr_kernel(const unsigned *__restrict__ skey, long long nh, long long n,
+                              long long *__restrict__ rowptr) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= nh;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long lo = i == 0 ? 0 : (long long)skey[i - 1] + 1;
+        const long long hi = i == nh ? n : (long long)skey[i];
+        for (long long x = lo; x <= hi; ++x) rowptr[x] = i;
     }
 }
 
@@ -2119,12 +2127,11 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
     c.rowptr = sc.alloc<long long>(n + 1);
     c.col = sc.alloc<int>(nh);
     c.w = sc.alloc<double>(nh);
-    unsigned *cnt = sc.alloc<unsigned>(n + 1);
-    CVZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (n + 1), s));
+    const unsigned *sorted_key = nullptr;
     if (m > 0) {
         unsigned *key = sc.alloc<unsigned>(nh), *val = sc.alloc<unsigned>(nh);
         unsigned *skey = sc.alloc<unsigned>(nh), *sval = sc.alloc<unsigned>(nh);
-        CVZ_LAUNCH(half_edges_kernel, grid_for(m, FB, 1, 8), FB, 0, s, e, m, key, val, cnt);
+        CVZ_LAUNCH(half_edges_kernel, grid_for(m, FB, 1, 8), FB, 0, s, e, m, key, val);
         int bits = 1;
         while (bits < 32 && (1LL << bits) < n) ++bits;
         // scratch in / out: sort over DoubleBuffers (no copy pass)
@@ -2138,15 +2145,12 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
         }
         count_launches(1 + (bits + 7) / 8);
         sval = dv.Current();
+        sorted_key = dk.Current();
         CVZ_LAUNCH(csr_fill_kernel, grid_for(nh, FB, 1, 8), FB, 0, s, e, sval, nh, weight, sign,
                    c.col, c.w);
     }
-    // rowptr = exclusive scan of counts (n+1 entries, last = 2m)
-    size_t tb2 = 0;
-    CVZ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, c.rowptr, (int)(n + 1), s));
-    void *tmp2 = sc.alloc<char>(tb2);
-    CVZ_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, tb2, cnt, c.rowptr, (int)(n + 1), s));
-    count_launches(2);
+    CVZ_LAUNCH(rowptr_kernel, grid_for(nh + 1, FB, 1, 8), FB, 0, s, sorted_key, m > 0 ? nh : 0,
+               n, c.rowptr);
     c.hidx = sc.alloc<int>(n);
     c.heavy = sc.alloc<int>(n);
     unsigned *nh_d = sc.alloc<unsigned>(1);
