@@ -588,6 +588,27 @@ def test_full_graph_layout_matches_oracle(cv, orc):
     assert np.max(np.abs(res.positions - pos)) <= 1e-7 * diam
 
 
+def test_layout_isolated_rows_match_oracle(cv, orc):
+    """CSR rows of isolated nodes at the start, middle and end of the id range
+    (the rowptr is derived from the sorted half-edge keys) and a hub row long
+    enough for the warp-summed springs path."""
+    rng = np.random.default_rng(9)
+    n = 3000
+    u = rng.integers(5, n - 5, 6000)
+    v = rng.integers(5, n - 5, 6000)
+    keep = (u != v) & (u != 1500) & (v != 1500)
+    hub = np.stack([np.full(200, 7), rng.integers(8, n - 5, 200)], 1)
+    e = np.concatenate([np.stack([u[keep], v[keep]], 1), hub])
+    e = e[(e[:, 0] != e[:, 1]) & (e[:, 0] != 1500) & (e[:, 1] != 1500)]
+    g = cv.from_edge_array(e, node_count=n)
+    assert g.degree[:5].sum() == 0 and g.degree[-5:].sum() == 0 and g.degree[1500] == 0
+    mass, ew = orc.masses_graph(g.degree, g.edge_count)
+    res = cv.layout(g, cv.LayoutParams(iterations=15, seed=4))
+    pos, _ = orc.layout(n, mass, g.edges, ew, iterations=15, seed=4)
+    diam = np.hypot(*(pos.max(0) - pos.min(0)))
+    assert np.max(np.abs(res.positions - pos)) <= 1e-7 * diam
+
+
 # ------------------------------------------------------------------- rng
 @pytest.mark.parametrize("n,seed", [(1, 0), (7, 3), (1000, 0), (318813, 0), (100003, 12345)])
 def test_device_init_positions_bit_exact(cv, orc, n, seed):
