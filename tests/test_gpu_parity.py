@@ -461,6 +461,18 @@ def test_bh_walk_stats(cv):
     assert vis3 == inter3 == 0
 
 
+@pytest.mark.parametrize("n", [2047, 2048, 2049, 6145])
+def test_bh_tile_boundaries_vs_oracle(cv, orc, n):
+    """Body counts around the cooperative tree-key sort's 2048-key tiles."""
+    rng = np.random.default_rng(n)
+    pos = np.concatenate([rng.normal(0, 5, (n // 2, 2)), rng.uniform(-90, 90, (n - n // 2, 2))])
+    mass = rng.integers(1, 9, n).astype(np.float64)
+    out = cv.repulsion_forces(pos, mass, 80.0, 0.7)
+    ref = orc.repulsion_forces(pos, mass, 80.0, 0.7)
+    rel = np.hypot(*(out - ref).T) / (np.hypot(*ref.T) + 1e-300)
+    assert rel.max() <= 1e-9
+
+
 def test_bh_large_vs_oracle(cv, orc):
     rng = np.random.default_rng(11)
     n = 200_000
