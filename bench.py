@@ -19,6 +19,7 @@ scaling); time = max over ranks.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -267,6 +268,10 @@ def run_ours(args, rank, ws):
     stats = []
     barrier(ws)
     launches0 = _native.launch_count()
+    # no cyclic-GC pause inside a timed region (the pipeline syncs with the
+    # host between stages, so a host stall would show up as device time)
+    gc.collect()
+    gc.disable()
     with Clocks(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -276,6 +281,7 @@ def run_ours(args, rank, ws):
             pipeline(cv, dev)
         t1.record()
         torch.cuda.synchronize()
+    gc.enable()
     launches = (_native.launch_count() - launches0) // args.steps
     ms = t0.elapsed_time(t1)
     ms_step = barrier_max(ms / args.steps, ws)
@@ -298,7 +304,11 @@ def run_ours(args, rank, ws):
         cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1, mode="fast")
     torch.cuda.synchronize()
     fms = []
+    gc.collect()
+    gc.disable()
+    fa = None
     for _ in range(max(3, args.steps)):  # per-call events: report the median call
+        fa = None  # release the previous result (its pinned label buffer) first
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record()
@@ -306,6 +316,7 @@ def run_ours(args, rank, ws):
         f1.record()
         torch.cuda.synchronize()
         fms.append(f0.elapsed_time(f1))
+    gc.enable()
     fast = dict(ms=float(np.median(fms)), ms_all=fms, rounds=len(fa.round_history),
                 m_r=list(fa.stream_edges), communities=fa.community_count)
     del g
@@ -315,10 +326,13 @@ def run_ours(args, rank, ws):
     for _ in range(max(1, args.warmup)):
         pos, lab = pipeline_e2e(cv, host_np)
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()
     e0 = time.perf_counter()
     for _ in range(args.steps):
         pos, lab = pipeline_e2e(cv, host_np)
     torch.cuda.synchronize()
+    gc.enable()
     e2e_ms = barrier_max((time.perf_counter() - e0) * 1000 / args.steps, ws)
     h2d = host_np.nbytes
     d2h = pos.nbytes + lab.nbytes
