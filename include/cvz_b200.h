@@ -174,14 +174,17 @@ int cvz_sketch_indices(const int64_t *hash_a, const int64_t *hash_b, int rows,
 
 /* C/sketch.py:71-86 sketch_add_many (C/supergraph.py:42-46 accumulate_sizes):
  * table[r, idx_r(key_j)] += amount_j with int64 wrap-around, then every
- * negative cell is set to INT64_MAX.  amounts must be >= 0 (validate != 0
+ * negative cell is set to INT64_MAX.  n_amounts is the length of amounts:
+ * k, or 1 to broadcast amounts[0] to every key (numpy's np.add.at
+ * broadcasting); anything else is CVZ_ERR_VALUE.  amounts must be >= 0 (validate != 0
  * checks first and returns CVZ_ERR_VALUE without touching the table; this
  * synchronises).  *d_saturated [dev] int32 is set to 1 if any cell wrapped.
  * Shared-memory-staged table when rows*cols fits, warp-aggregated global
  * atomics otherwise. */
 int cvz_sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *hash_a,
                    const int64_t *hash_b, const int64_t *keys, const int64_t *amounts,
-                   int64_t k, int validate, int32_t *d_saturated, void *stream);
+                   int64_t k, int64_t n_amounts, int validate, int32_t *d_saturated,
+                   void *stream);
 
 /* Sharded sketch building.  accumulate: delta[r, idx_r(key_j)]
  * += amount_j with u64 wrap-around and NO saturation (a rank-local delta

@@ -55,7 +55,7 @@ SIGNATURES = {
                          _P, _P, _P, _P, _P, ctypes.POINTER(_I64),
                          ctypes.POINTER(ctypes.c_int), _I64, ctypes.POINTER(_I64), _P],
     "cvz_sketch_indices": [_P, _P, _I32, _I64, _P, _I64, _P, _P],
-    "cvz_sketch_add": [_P, _I32, _I64, _P, _P, _P, _P, _I64, _I32, _P, _P],
+    "cvz_sketch_add": [_P, _I32, _I64, _P, _P, _P, _P, _I64, _I64, _I32, _P, _P],
     "cvz_sketch_estimate": [_P, _I32, _I64, _P, _P, _P, _I64, _P, _P],
     "cvz_contract": [_P, _I64, _P, _I64, _P, _I32, _I64, _P, _P,
                      ctypes.POINTER(_ContractResult), _P],

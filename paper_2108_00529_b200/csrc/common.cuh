@@ -12,6 +12,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <climits>
 #include <cstdlib>
 #include <tuple>
 #include <type_traits>
@@ -173,6 +174,35 @@ int guard(F &&f) {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+// A lazily computed per-device int (SM counts, occupancy, one-time function
+// attributes): one slot per device id, so a process that switches devices
+// never reuses another device's value.  Racing first calls compute the same
+// value, so a relaxed publish is enough.
+struct DeviceCache {
+    static constexpr int kMax = 64;
+    std::atomic<int> v[kMax];
+    DeviceCache() {
+        for (auto &x : v) x.store(INT_MIN, std::memory_order_relaxed);
+    }
+    template <class F>
+    int get(F &&compute) {
+        const int d = current_device();
+        if (d < 0 || d >= kMax) return compute();
+        int x = v[d].load(std::memory_order_acquire);
+        if (x == INT_MIN) {
+            x = compute();
+            v[d].store(x, std::memory_order_release);
+        }
+        return x;
+    }
+};
+
 void init_pool_once();
 
 // Stream-ordered scratch arena: every allocation is released (stream-ordered)
@@ -220,14 +250,12 @@ T *device_alloc(size_t n, cudaStream_t s) {
 }
 
 inline int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
+    static DeviceCache cache;
+    return cache.get([] {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device());
+        return sms > 0 ? sms : 148;
+    });
 }
 
 inline unsigned grid_for(long long work, int block, int per_thread = 1, int waves = 8) {

@@ -380,18 +380,28 @@ int cvz_contract(const int32_t *edges, int64_t m, const int64_t *labels, int64_t
         cudaStream_t s = as_stream(stream);
         Scratch sc(s);
         *res = cvz_contract_result{0, 0, nullptr, nullptr, nullptr, nullptr};
-        int *dense = sc.alloc<int>(n);
-        long long k = dense_ids(labels, n, dense, &res->comm_id, sc, s);
-        res->k = k;
-        res->weight = device_alloc<int64_t>(k, s);
-        sketch_estimate(table, rows, cols, hash_a, hash_b, res->comm_id, k, res->weight, s);
-        int B = bits_for(k);
-        auto *e = reinterpret_cast<const int2 *>(edges);
-        if (2 * B <= 32)
-            superedges<unsigned>(e, m, dense, k, B, sc, s, res);
-        else
-            superedges<unsigned long long>(e, m, dense, k, B, sc, s, res);
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        try {
+            int *dense = sc.alloc<int>(n);
+            long long k = dense_ids(labels, n, dense, &res->comm_id, sc, s);
+            res->k = k;
+            res->weight = device_alloc<int64_t>(k, s);
+            sketch_estimate(table, rows, cols, hash_a, hash_b, res->comm_id, k, res->weight, s);
+            int B = bits_for(k);
+            auto *e = reinterpret_cast<const int2 *>(edges);
+            if (2 * B <= 32)
+                superedges<unsigned>(e, m, dense, k, B, sc, s, res);
+            else
+                superedges<unsigned long long>(e, m, dense, k, B, sc, s, res);
+            CVZ_CUDA(cudaStreamSynchronize(s));
+        } catch (...) {
+            // the result buffers live outside the arena: release them here,
+            // the caller never sees a half-filled result
+            for (void *p : {(void *)res->comm_id, (void *)res->weight, (void *)res->se_edges,
+                            (void *)res->mult})
+                if (p) cudaFreeAsync(p, s);
+            *res = cvz_contract_result{0, 0, nullptr, nullptr, nullptr, nullptr};
+            throw;
+        }
     });
 }
 

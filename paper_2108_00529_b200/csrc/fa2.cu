@@ -1673,11 +1673,12 @@ size_t sort_bytes(int n, int bits) {
 // CTAs of a persistent kernel: all that fit at once on every SM.
 template <class K>
 unsigned persist_blocks(K kernel) {
-    static int per_sm = 0;
-    if (!per_sm) {
-        CVZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, FB, 0));
-        if (per_sm < 1) per_sm = 1;
-    }
+    static DeviceCache cache;
+    const int per_sm = cache.get([&] {
+        int b = 0;
+        CVZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, FB, 0));
+        return b < 1 ? 1 : b;
+    });
     return (unsigned)(per_sm * num_sms());
 }
 
@@ -1795,19 +1796,18 @@ __global__ void __launch_bounds__(TS_THREADS) tree_sort_coop_kernel(
 
 // Largest n the cooperative sort takes on this device (0 = unavailable).
 static int tree_sort_coop_cap() {
-    static int cap = -1;
-    if (cap < 0) {
-        int per_sm = 0, dev = 0, sms = 0, coop = 0;
-        CVZ_CUDA(cudaGetDevice(&dev));
+    static DeviceCache cache;
+    return cache.get([] {
+        int per_sm = 0, sms = 0, coop = 0;
+        const int dev = current_device();
         CVZ_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
         CVZ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         CVZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tree_sort_coop_kernel,
                                                                TS_THREADS, 0));
         const char *e = getenv("CVZ_TREE_SORT");
         const bool off = e && std::string(e) == "cub";
-        cap = (coop && !off) ? per_sm * sms * TS_TILE : 0;
-    }
-    return cap;
+        return (coop && !off) ? per_sm * sms * TS_TILE : 0;
+    });
 }
 
 struct Tree {

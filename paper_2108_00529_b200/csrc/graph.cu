@@ -51,17 +51,16 @@ void prof_record(const char *name, cudaEvent_t a, cudaEvent_t b) {
     g_prof_recs.push_back(ProfRec{name, a, b});
 }
 
-void init_pool_once() {
-    static bool done = false;
-    if (done) return;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done = true;
+void init_pool_once() {  // per device: the release threshold is a pool attribute
+    static DeviceCache done;
+    done.get([] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, current_device()) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        return 1;
+    });
 }
 
 namespace {

@@ -112,10 +112,11 @@ __global__ void add_direct_kernel(unsigned long long *__restrict__ table,
 // identical counters to the node-based form because it is integer addition).
 struct KeyAmounts {
     const long long *keys, *amounts;
+    long long astride;  // 1, or 0 to broadcast amounts[0] (np.add.at broadcasting)
     __device__ __forceinline__ void get(long long j, long long &key,
                                         unsigned long long &amt) const {
         key = keys[j];
-        amt = (unsigned long long)amounts[j];
+        amt = (unsigned long long)amounts[j * astride];
     }
 };
 struct EdgeLabels {
@@ -225,13 +226,13 @@ void sketch_accumulate(int64_t *table, int rows, int64_t cols, const int64_t *ha
     auto *pa = reinterpret_cast<const long long *>(ha);
     auto *pb = reinterpret_cast<const long long *>(hb);
     if (staged) {
-        static bool attr = false;
-        if (!attr) {
+        static DeviceCache attr;  // the attribute is per device
+        attr.get([] {
             CVZ_CUDA(cudaFuncSetAttribute(add_staged_kernel<Src>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)STAGED_MAX_BYTES));
-            attr = true;
-        }
+            return 1;
+        });
         // one CTA per SM (the table fills its shared memory); each writes
         // a partial table, one pass sums them into the sketch
         long long want = k / (2LL * rows * cols) + 1;
@@ -255,11 +256,12 @@ void sketch_saturate(int64_t *table, int rows, int64_t cols, int32_t *d_sat, cud
 }
 
 void sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *ha, const int64_t *hb,
-                const int64_t *keys, const int64_t *amounts, int64_t k, int32_t *d_sat,
-                cudaStream_t s) {
+                const int64_t *keys, const int64_t *amounts, int64_t k, int64_t n_amounts,
+                int32_t *d_sat, cudaStream_t s) {
     sketch_accumulate(table, rows, cols, ha, hb,
                       KeyAmounts{reinterpret_cast<const long long *>(keys),
-                                 reinterpret_cast<const long long *>(amounts)},
+                                 reinterpret_cast<const long long *>(amounts),
+                                 n_amounts == k ? 1LL : 0LL},
                       k, s);
     sketch_saturate(table, rows, cols, d_sat, s);
 }
@@ -297,23 +299,26 @@ int cvz_sketch_indices(const int64_t *hash_a, const int64_t *hash_b, int rows, i
 
 int cvz_sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *hash_a,
                    const int64_t *hash_b, const int64_t *keys, const int64_t *amounts,
-                   int64_t k, int validate, int32_t *d_saturated, void *stream) {
+                   int64_t k, int64_t n_amounts, int validate, int32_t *d_saturated,
+                   void *stream) {
     return guard([&] {
         CVZ_REQUIRE(rows >= 1 && cols >= 1 && cols < (1LL << 31), CVZ_ERR_VALUE,
                     "sketch needs 1 <= cols < 2^31 and rows >= 1");
+        CVZ_REQUIRE(k >= 0 && (n_amounts == k || n_amounts == 1), CVZ_ERR_VALUE,
+                    "array is not broadcastable to correct shape");
         cudaStream_t s = as_stream(stream);
         if (validate && k > 0) {
             Scratch sc(s);
             int *flag = sc.alloc<int>(1);
             CVZ_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
-            CVZ_LAUNCH(negative_check_kernel, grid_for(k, 256, 4, 4), 256, 0, s,
-                       reinterpret_cast<const long long *>(amounts), (long long)k, flag);
+            CVZ_LAUNCH(negative_check_kernel, grid_for(n_amounts, 256, 4, 4), 256, 0, s,
+                       reinterpret_cast<const long long *>(amounts), (long long)n_amounts, flag);
             int h = 0;
             CVZ_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
             CVZ_CUDA(cudaStreamSynchronize(s));
             CVZ_REQUIRE(!h, CVZ_ERR_VALUE, "amounts must be non-negative");
         }
-        sketch_add(table, rows, cols, hash_a, hash_b, keys, amounts, k, d_saturated, s);
+        sketch_add(table, rows, cols, hash_a, hash_b, keys, amounts, k, n_amounts, d_saturated, s);
     });
 }
 
@@ -325,7 +330,7 @@ int cvz_sketch_accumulate(int64_t *delta, int rows, int64_t cols, const int64_t 
                     "sketch needs 1 <= cols < 2^31 and rows >= 1");
         sketch_accumulate(delta, rows, cols, hash_a, hash_b,
                           KeyAmounts{reinterpret_cast<const long long *>(keys),
-                                     reinterpret_cast<const long long *>(amounts)},
+                                     reinterpret_cast<const long long *>(amounts), 1LL},
                           k, as_stream(stream));
     });
 }

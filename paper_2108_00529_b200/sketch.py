@@ -98,6 +98,7 @@ def sketch_add_many(s: CountMinSketch, keys, amounts) -> None:
     memory; keys/amounts may be numpy arrays or CUDA tensors."""
     T = nat.torch()
     kd, _ = _dev64(keys)
+    ndim = amounts.dim() if isinstance(amounts, T.Tensor) else np.ndim(amounts)
     ad, ah = _dev64(amounts)
     if ah is not None:
         if np.any(ah < 0):
@@ -105,11 +106,16 @@ def sketch_add_many(s: CountMinSketch, keys, amounts) -> None:
         validate = 0
     else:
         validate = 1
+    # np.add.at(table[r], idx[r], amounts) broadcasting: a scalar or one
+    # amount applies to every key; any other length mismatch is an error
+    k, na = int(kd.shape[0]), int(ad.shape[0])
+    if ndim > 1 or na not in (1, k):
+        raise ValueError("array is not broadcastable to correct shape")
     table = s.table_dev()
     a, b = s._hash_dev()
     sat = T.zeros(1, dtype=T.int32, device=nat.device())
     nat.call("cvz_sketch_add", nat.ptr(table), s.rows, s.cols, nat.ptr(a), nat.ptr(b),
-             nat.ptr(kd), nat.ptr(ad), int(kd.shape[0]), validate, nat.ptr(sat), nat.stream())
+             nat.ptr(kd), nat.ptr(ad), k, na, validate, nat.ptr(sat), nat.stream())
     s._table.set_dev(table)
     if int(sat.item()) and not s.saturated:
         s.saturated = True
