@@ -448,11 +448,69 @@ def run_c5(comm, rank, ws, reps=3):
     t1.record()
     torch.cuda.synchronize()
     ms = barrier_max(t0.elapsed_time(t1) / reps, ws)
-    out = {"scale": C5_SCALE, "nodes": n5, "edge_draws": m5, "edges_after_self_loops": g.edge_count,
+    m_kept = g.edge_count
+    # SURVEY.md 8(d) bytes of the stage: compaction 8 (read) + 8 (write) per
+    # draw, degrees 8 per kept edge + 8 per node (int64 counters), sketch
+    # (edge-based) 8 per kept edge (pair) + 2 label gathers of 8
+    ing_bytes = 16 * m5 / ws + 8 * m_kept / ws + 8 * n5 + 24 * m_kept / ws
+    out = {"scale": C5_SCALE, "nodes": n5, "edge_draws": m5, "edges_after_self_loops": m_kept,
            "ms": ms, "edges_per_s": m5 / (ms / 1e3),
+           "hbm_frac_per_rank": ing_bytes / (ms / 1e3) / 1e9 / peak_hbm()[0],
            "note": "edge-sharded compaction + degrees + sketch; labels = id // 64 (synthetic "
                    "communities; the order-dependent community pass is not sharded)"}
-    del e5, labels, g
+    del e5, labels
+    # node-sharded full-graph ForceAtlas2 on the same R-MAT-26 graph: every
+    # rank holds the whole compacted edge list (all-gather), builds its CSR
+    # over the rows it owns only, the full tree, and walks/moves its bodies
+    out["fa2"] = run_c5_fa2(comm, g, ws)
+    del g
+    torch.cuda.empty_cache()
+    return out
+
+
+C5_FA2_ITERS = int(os.environ.get("CVZ_C5_FA2_ITERS", "5"))
+
+
+def run_c5_fa2(comm, g_sh, ws):
+    import torch
+
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import sharded as sh
+    from paper_2108_00529_b200.layout import _init_positions_dev
+    g = g_sh.gather()
+    n = g.node_count
+    mass = (g.degree_dev() + 1).to(torch.float64)
+    e = g.edges_dev()
+    P = sh._layout_params(cv.LayoutParams(iterations=C5_FA2_ITERS + 1))
+    pos0 = _init_positions_dev(n, 0)
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    lay = sh.ShardLayout(comm, n, mass, e, None, P, pos0, C5_FA2_ITERS + 1)
+    t1.record()
+    torch.cuda.synchronize()
+    create_ms = barrier_max(t0.elapsed_time(t1), ws)
+    try:
+        lay.run(1)  # warm-up iteration (first tree build sizes its CUB temp)
+        torch.cuda.synchronize()
+        barrier(ws)
+        t0.record()
+        lay.run(C5_FA2_ITERS)
+        t1.record()
+        torch.cuda.synchronize()
+        it_ms = barrier_max(t0.elapsed_time(t1) / C5_FA2_ITERS, ws)
+        bad, _ = lay.finish()
+        disp = lay.hist.cpu().tolist()
+    finally:
+        lay.close()
+    out = {"ms_per_iter": it_ms, "iters_timed": C5_FA2_ITERS, "csr_setup_ms": create_ms,
+           "bodies": n, "half_edges": 2 * g.edge_count, "non_finite": bad,
+           "displacement": disp,
+           "note": "node-sharded full-graph ForceAtlas2 (mass = degree + 1, unit springs); "
+                   "each rank: CSR over its owned rows only, full Barnes-Hut tree, walk over "
+                   "its own bodies; per iteration 2 all-reduces + 1 position all-gather"}
+    del lay, pos0, mass, e, g
     torch.cuda.empty_cache()
     return out
 

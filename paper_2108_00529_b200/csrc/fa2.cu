@@ -1298,6 +1298,9 @@ __global__ void __launch_bounds__(XT) exact_kernel(const double2 *__restrict__ p
 }
 
 // ---- CSR for attraction ------------------------------------------------------
+// Half-edge h = 2k + side of edge k (row = e[k].x for side 0, e[k].y for side
+// 1; col = the other endpoint).  The CSR lists each row's half-edges in h
+// order, i.e. in the edge order C/layout.py:301-304 accumulates them.
 __global__ void half_edges_kernel(const int2 *__restrict__ e, long long m,
                                   unsigned *__restrict__ key, unsigned *__restrict__ val) {
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
@@ -1308,7 +1311,29 @@ __global__ void half_edges_kernel(const int2 *__restrict__ e, long long m,
     }
 }
 
-// rowptr from the node-sorted half-edge keys (no per-node atomics: hub rows
+// Node-sharded ranks keep only the half-edges of the rows they own.
+struct OwnedHalfEdge {
+    const int2 *e;
+    int lo, hi;
+    __device__ __forceinline__ bool operator()(long long h) const {
+        const int2 p = e[h >> 1];
+        const int r = (h & 1) ? p.y : p.x;
+        return r >= lo && r < hi;
+    }
+};
+
+// keys (row - lo) of the selected half-edges (already in h order)
+__global__ void owned_keys_kernel(const int2 *__restrict__ e, const unsigned *__restrict__ val,
+                                  long long cnt, int lo, unsigned *__restrict__ key) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < cnt;
+         j += (long long)gridDim.x * blockDim.x) {
+        const unsigned h = val[j];
+        const int2 p = e[h >> 1];
+        key[j] = (unsigned)(((h & 1) ? p.y : p.x) - lo);
+    }
+}
+
+// rowptr from the row-sorted half-edge keys (no per-node atomics: hub rows
 // serialised them): rows (skey[i-1], skey[i]] start at i, rows past the last
 // key at nh; every one of the n + 1 entries is written exactly once.
 __global__ void rowptr_kernel(const unsigned *__restrict__ skey, long long nh, long long n,
@@ -1321,7 +1346,9 @@ __global__ void rowptr_kernel(const unsigned *__restrict__ skey, long long nh, l
     }
 }
 
-// col = other endpoint; w = edge weight * sign (or sign)
+// col = other endpoint; w = edge weight * sign (C/layout.py:300).  Unit
+// weights (full graphs, C/layout.py:337) store no per-half-edge weight: the
+// kernels use the sign itself (mul(1.0, sign) == sign exactly).
 __global__ void csr_fill_kernel(const int2 *__restrict__ e, const unsigned *__restrict__ sval,
                                 long long nh, const double *__restrict__ w, double sign,
                                 int *__restrict__ col, double *__restrict__ cw) {
@@ -1331,7 +1358,7 @@ __global__ void csr_fill_kernel(const int2 *__restrict__ e, const unsigned *__re
         long long k = h >> 1;
         int2 p = e[k];
         col[j] = (h & 1) ? p.x : p.y;
-        cw[j] = mul(w ? w[k] : 1.0, sign);  // C/layout.py:300  w = weight[e] * sign
+        if (cw) cw[j] = mul(w[k], sign);
     }
 }
 
@@ -1363,10 +1390,12 @@ __global__ void classify_rows_kernel(const long long *__restrict__ rowptr, int l
     }
 }
 
+template <bool UNIT>
 __global__ void __launch_bounds__(FB) springs_heavy_kernel(
     const double2 *__restrict__ pos, const long long *__restrict__ rowptr,
-    const int *__restrict__ col, const double *__restrict__ cw, const int *__restrict__ heavy,
-    int nheavy, double2 *__restrict__ hsum, const StepScalars *__restrict__ sc) {
+    const int *__restrict__ col, const double *__restrict__ cw, double unit,
+    const int *__restrict__ heavy, int nheavy, double2 *__restrict__ hsum,
+    const StepScalars *__restrict__ sc) {
     griddep_wait();
     if (sc && sc->bad) return;
     const int lane = lane_id();
@@ -1386,7 +1415,7 @@ __global__ void __launch_bounds__(FB) springs_heavy_kernel(
 #pragma unroll
             for (int q = 0; q < 4; ++q) v[q] = col[j + 32 * q];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) c[q] = cw[j + 32 * q];
+            for (int q = 0; q < 4; ++q) c[q] = UNIT ? unit : cw[j + 32 * q];
 #pragma unroll
             for (int q = 0; q < 4; ++q) pv[q] = pos[v[q]];
 #pragma unroll
@@ -1397,7 +1426,7 @@ __global__ void __launch_bounds__(FB) springs_heavy_kernel(
         }
         for (; j < end; j += 32) {
             double2 pv = pos[col[j]];
-            double c = cw[j];
+            double c = UNIT ? unit : cw[j];
             fx = add(fx, mul(c, sub(pv.x, pu.x)));
             fy = add(fy, mul(c, sub(pv.y, pu.y)));
         }
@@ -1412,10 +1441,12 @@ __global__ void __launch_bounds__(FB) springs_heavy_kernel(
 // Springs of the light rows (<= HEAVY half-edges), one thread per row, in
 // edge order from zero.  Runs on a side stream concurrently with the tree
 // build + repulsion (it needs only positions); forces_kernel adds the sum.
+template <bool UNIT>
 __global__ void __launch_bounds__(FB) springs_light_kernel(
     const double2 *__restrict__ pos, const long long *__restrict__ rowptr,
-    const int *__restrict__ col, const double *__restrict__ cw, const int *__restrict__ hidx,
-    int lo, int hi, double2 *__restrict__ spr, const StepScalars *__restrict__ sc) {
+    const int *__restrict__ col, const double *__restrict__ cw, double unit,
+    const int *__restrict__ hidx, int lo, int hi, double2 *__restrict__ spr,
+    const StepScalars *__restrict__ sc) {
     griddep_wait();
     if (sc && sc->bad) return;
     for (int u = lo + blockIdx.x * blockDim.x + threadIdx.x; u < hi;
@@ -1425,7 +1456,7 @@ __global__ void __launch_bounds__(FB) springs_light_kernel(
         double fx = 0.0, fy = 0.0;
         for (long long j = rowptr[u]; j < rowptr[u + 1]; ++j) {
             double2 pv = pos[col[j]];
-            double w = cw[j];
+            double w = UNIT ? unit : cw[j];
             fx = add(fx, mul(w, sub(pv.x, pu.x)));
             fy = add(fy, mul(w, sub(pv.y, pu.y)));
         }
@@ -2109,40 +2140,81 @@ void repulsion_dev(const double *pos, const double *mass, long long n, double kr
 }
 
 struct Csr {
-    long long *rowptr;
+    long long *rowptr;  // indexed by node id; valid on [row_lo, row_hi]
     int *col;
-    double *w;
+    double *w;          // nullptr for unit weights: every half-edge weighs `unit`
+    double unit = 1.0;
+    long long nh = 0;   // half-edges stored (the owned rows' only)
     int *hidx;      // [n] heavy slot or -1
     int *heavy;     // [nheavy] heavy row ids
     int nheavy = 0;
     double2 *hsum;  // [nheavy] warp-summed springs
 };
 
-// Heavy rows are classified over [row_lo, row_hi) only (a node-sharded rank
-// sums the springs of the rows it owns); row_hi < 0 means all n.
+// CSR over the rows [row_lo, row_hi) (row_hi < 0: all n).  A node-sharded
+// rank stores only the half-edges of the rows it owns: a
+// stable select of those half-edges in h order, then a stable radix sort by
+// row - row_lo (⌈log2(row_hi - row_lo)⌉ bits).  Counts are 64-bit end to end
+// (2^30 R-MAT draws give 2.1·10^9 half-edges); h = 2k + side fits 32 bits
+// while m < 2^31.  The sort buffers live in a temporary arena, so a shard
+// keeps only rowptr + col (+ weights when they are not all 1).
 static Csr build_csr(const int2 *e, long long m, long long n, const double *weight, double sign,
                      Scratch &sc, cudaStream_t s, long long row_lo = 0, long long row_hi = -1) {
     if (row_hi < 0) row_hi = n;
+    CVZ_REQUIRE(m < (1LL << 31), CVZ_ERR_VALUE, "layout supports < 2^31 edges");
+    const bool all_rows = row_lo == 0 && row_hi == n;
+    const long long rows = row_hi - row_lo;
     Csr c;
-    long long nh = 2 * m;
-    c.rowptr = sc.alloc<long long>(n + 1);
-    c.col = sc.alloc<int>(nh);
-    c.w = sc.alloc<double>(nh);
-    const unsigned *sorted_key = nullptr;
-    if (m > 0) {
-        unsigned *key = sc.alloc<unsigned>(nh), *val = sc.alloc<unsigned>(nh);
-        unsigned *skey = sc.alloc<unsigned>(nh), *sval = sc.alloc<unsigned>(nh);
+    c.unit = sign;
+    long long nh = all_rows ? 2 * m : 0;
+    Scratch tmp_sc(s);  // sort keys / values / temp storage: freed on return
+    unsigned *key = nullptr, *val = nullptr;
+    if (m > 0 && all_rows) {
+        key = tmp_sc.alloc<unsigned>(nh);
+        val = tmp_sc.alloc<unsigned>(nh);
         CVZ_LAUNCH(half_edges_kernel, grid_for(m, FB, 1, 8), FB, 0, s, e, m, key, val);
+    } else if (m > 0 && rows > 0) {
+        // stable select of the owned half-edges (order = h order), then keys
+        long long *cnt_d = tmp_sc.alloc<long long>(1);
+        OwnedHalfEdge pred{e, (int)row_lo, (int)row_hi};
+        size_t tb = 0;
+        CVZ_CUDA(cub::DeviceSelect::If(nullptr, tb, thrust::counting_iterator<long long>(0),
+                                       (unsigned *)nullptr, cnt_d, 2 * m, pred, s));
+        void *tmp = tmp_sc.alloc<char>(tb);
+        // upper bound for the selection: every half-edge
+        unsigned *sel = tmp_sc.alloc<unsigned>(2 * m);
+        {
+            CVZ_REGION("cub_select:owned_half_edges", s);
+            CVZ_CUDA(cub::DeviceSelect::If(tmp, tb, thrust::counting_iterator<long long>(0), sel,
+                                           cnt_d, 2 * m, pred, s));
+            count_launches(2);
+        }
+        CVZ_CUDA(cudaMemcpyAsync(&nh, cnt_d, sizeof(nh), cudaMemcpyDeviceToHost, s));
+        CVZ_CUDA(cudaStreamSynchronize(s));
+        val = sel;
+        key = tmp_sc.alloc<unsigned>(nh > 0 ? nh : 1);
+        if (nh > 0)
+            CVZ_LAUNCH(owned_keys_kernel, grid_for(nh, FB, 1, 8), FB, 0, s, e, val, nh,
+                       (int)row_lo, key);
+    }
+    c.nh = nh;
+    long long *rowptr_rel = sc.alloc<long long>(rows + 1);
+    c.rowptr = rowptr_rel - row_lo;  // only [row_lo, row_hi] is ever indexed
+    c.col = sc.alloc<int>(nh > 0 ? nh : 1);
+    c.w = weight ? sc.alloc<double>(nh > 0 ? nh : 1) : nullptr;
+    const unsigned *sorted_key = nullptr;
+    if (nh > 0) {
+        unsigned *skey = tmp_sc.alloc<unsigned>(nh), *sval = tmp_sc.alloc<unsigned>(nh);
         int bits = 1;
-        while (bits < 32 && (1LL << bits) < n) ++bits;
+        while (bits < 32 && (1LL << bits) < rows) ++bits;
         // scratch in / out: sort over DoubleBuffers (no copy pass)
         cub::DoubleBuffer<unsigned> dk(key, skey), dv(val, sval);
         size_t tb = 0;
-        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)nh, 0, bits, s));
-        void *tmp = sc.alloc<char>(tb);
+        CVZ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, nh, 0, bits, s));
+        void *tmp = tmp_sc.alloc<char>(tb);
         {
             CVZ_REGION("cub_sort:csr", s);
-            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)nh, 0, bits, s));
+            CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, nh, 0, bits, s));
         }
         count_launches(1 + (bits + 7) / 8);
         sval = dv.Current();
@@ -2150,13 +2222,13 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
         CVZ_LAUNCH(csr_fill_kernel, grid_for(nh, FB, 1, 8), FB, 0, s, e, sval, nh, weight, sign,
                    c.col, c.w);
     }
-    CVZ_LAUNCH(rowptr_kernel, grid_for(nh + 1, FB, 1, 8), FB, 0, s, sorted_key, m > 0 ? nh : 0,
-               n, c.rowptr);
+    CVZ_LAUNCH(rowptr_kernel, grid_for(nh + 1, FB, 1, 8), FB, 0, s, sorted_key, nh, rows,
+               rowptr_rel);
     c.hidx = sc.alloc<int>(n);
-    c.heavy = sc.alloc<int>(n);
-    unsigned *nh_d = sc.alloc<unsigned>(1);
+    c.heavy = sc.alloc<int>(rows > 0 ? rows : 1);
+    unsigned *nh_d = tmp_sc.alloc<unsigned>(1);
     CVZ_CUDA(cudaMemsetAsync(nh_d, 0, sizeof(unsigned), s));
-    CVZ_LAUNCH(classify_rows_kernel, grid_for(row_hi - row_lo, FB, 1, 8), FB, 0, s, c.rowptr,
+    CVZ_LAUNCH(classify_rows_kernel, grid_for(rows, FB, 1, 8), FB, 0, s, c.rowptr,
                (int)row_lo, (int)row_hi, c.hidx, c.heavy, nh_d);
     unsigned nh_h = 0;
     CVZ_CUDA(cudaMemcpyAsync(&nh_h, nh_d, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
@@ -2169,24 +2241,35 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
 // all spring sums of rows [lo, hi) into c.hsum (heavy) / spr (light)
 static void springs(const double2 *pos, const Csr &c, const StepScalars *sc, int lo, int hi,
                     double2 *spr, cudaStream_t s) {
-    if (c.nheavy > 0)
-        CVZ_LAUNCH(springs_heavy_kernel, blocks_for((long long)c.nheavy * 32, FB), FB, 0, s, pos,
-                   c.rowptr, c.col, c.w, c.heavy, c.nheavy, c.hsum, sc);
-    if (hi > lo)
-        CVZ_LAUNCH(springs_light_kernel, blocks_for(hi - lo, FB), FB, 0, s, pos, c.rowptr, c.col,
-                   c.w, c.hidx, lo, hi, spr, sc);
+    // unit-weight graphs (no per-half-edge weights) get their own instances
+    if (c.nheavy > 0) {
+        if (c.w)
+            CVZ_LAUNCH(springs_heavy_kernel<false>, blocks_for((long long)c.nheavy * 32, FB), FB, 0,
+                       s, pos, c.rowptr, c.col, c.w, c.unit, c.heavy, c.nheavy, c.hsum, sc);
+        else
+            CVZ_LAUNCH(springs_heavy_kernel<true>, blocks_for((long long)c.nheavy * 32, FB), FB, 0,
+                       s, pos, c.rowptr, c.col, c.w, c.unit, c.heavy, c.nheavy, c.hsum, sc);
+    }
+    if (hi > lo) {
+        if (c.w)
+            CVZ_LAUNCH(springs_light_kernel<false>, blocks_for(hi - lo, FB), FB, 0, s, pos,
+                       c.rowptr, c.col, c.w, c.unit, c.hidx, lo, hi, spr, sc);
+        else
+            CVZ_LAUNCH(springs_light_kernel<true>, blocks_for(hi - lo, FB), FB, 0, s, pos,
+                       c.rowptr, c.col, c.w, c.unit, c.hidx, lo, hi, spr, sc);
+    }
 }
 
 __global__ void attraction_only_kernel(const double2 *__restrict__ pos, int n,
                                        const long long *__restrict__ rowptr,
                                        const int *__restrict__ col, const double *__restrict__ cw,
-                                       double2 *__restrict__ out) {
+                                       double unit, double2 *__restrict__ out) {
     for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
         double2 pu = pos[u];
         double2 f = out[u];
         for (long long j = rowptr[u]; j < rowptr[u + 1]; ++j) {
             double2 pv = pos[col[j]];
-            double w = cw[j];
+            double w = cw ? cw[j] : unit;
             f.x = add(f.x, mul(w, sub(pv.x, pu.x)));
             f.y = add(f.y, mul(w, sub(pv.y, pu.y)));
         }
@@ -2413,7 +2496,7 @@ int cvz_attraction(const double *pos, int64_t n, const int32_t *edges, int64_t m
         if (n <= 0 || m <= 0) return;
         Csr c = build_csr(reinterpret_cast<const int2 *>(edges), m, n, weight, sign, sc, s);
         CVZ_LAUNCH(attraction_only_kernel, grid_for(n, FB, 1, 8), FB, 0, s,
-                   reinterpret_cast<const double2 *>(pos), (int)n, c.rowptr, c.col, c.w,
+                   reinterpret_cast<const double2 *>(pos), (int)n, c.rowptr, c.col, c.w, c.unit,
                    reinterpret_cast<double2 *>(out));
     });
 }

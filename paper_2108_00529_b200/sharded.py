@@ -272,42 +272,75 @@ def _layout_params(params: LayoutParams):
                              _ATTRACTION_FORMS.index(params.attraction_form))
 
 
-def _run_shard(comm, n, mass, e, ew, P, pos0, iterations, ref_ids):
-    """One node-sharded FA2 run from pos0 (full, identical on every rank).
-    Returns (padded positions, displacement history, bad, jitter_seen)."""
-    T = nat.torch()
-    dev = nat.device()
-    rows = padded_rows(n, comm.world)
-    lo, hi = owned_nodes(n, comm.rank, comm.world)
-    full = T.zeros((comm.world * rows, 2), dtype=T.float64, device=dev)
-    full[:n].copy_(pos0)
-    pos = full[:n]
-    h = ctypes.c_void_p()
-    s = nat.stream()
-    nat.call("cvz_fa2_shard_create", nat.ptr(pos), nat.ptr(mass), n, nat.ptr(e),
-             int(e.shape[0]), nat.ptr(ew), ctypes.byref(P), lo, hi, int(ref_ids),
-             ctypes.byref(h), s)
-    try:
-        sums = T.zeros(2, dtype=T.float64, device=dev)
-        red = T.zeros(6, dtype=T.float64, device=dev)
-        hist = T.zeros(iterations, dtype=T.float64, device=dev)
+class ShardLayout:
+    """One node-sharded ForceAtlas2 run (cvz_fa2_shard_*) on this rank.
+
+    `create` builds the rank's CSR over the rows it owns only (a stable
+    select of their half-edges, C/layout.py:293-304 split by row) and the
+    per-iteration state; `run(k)` advances k iterations, each one
+    forces -> all-reduce(SUM) Σswing/Σtraction -> update -> all-reduce(MAX)
+    bbox/max-disp/bad -> all-gather of the owned position rows
+    (C/layout.py:363-398 split at its reductions)."""
+
+    def __init__(self, comm, n, mass, e, ew, P, pos0, iterations, ref_ids=False):
+        T = nat.torch()
+        dev = nat.device()
+        self.comm, self.n = comm, n
+        self.rows = padded_rows(n, comm.world)
+        lo, hi = owned_nodes(n, comm.rank, comm.world)
+        self.full = T.zeros((comm.world * self.rows, 2), dtype=T.float64, device=dev)
+        self.full[:n].copy_(pos0)
+        self.pos = self.full[:n]
+        self.h = ctypes.c_void_p()
+        self.s = nat.stream()
+        nat.call("cvz_fa2_shard_create", nat.ptr(self.pos), nat.ptr(mass), n, nat.ptr(e),
+                 int(e.shape[0]), nat.ptr(ew), ctypes.byref(P), lo, hi, int(ref_ids),
+                 ctypes.byref(self.h), self.s)
+        self.sums = T.zeros(2, dtype=T.float64, device=dev)
+        self.red = T.zeros(6, dtype=T.float64, device=dev)
+        self.hist = T.zeros(max(1, iterations), dtype=T.float64, device=dev)
+        self.done = 0
+
+    def run(self, k: int) -> None:
         lib = nat.load()
-        for _ in range(iterations):
+        h, s, pos, sums, red = self.h, self.s, self.pos, self.sums, self.red
+        for _ in range(k):
+            # absorb writes hist[iteration]; iterations past its length are not recorded
+            hist = nat.ptr(self.hist) if self.done < self.hist.shape[0] else None
             nat.check(lib.cvz_fa2_shard_forces(h, nat.ptr(pos), nat.ptr(sums), s), "forces")
-            comm.all_reduce(sums, "sum")
+            self.comm.all_reduce(sums, "sum")
             nat.check(lib.cvz_fa2_shard_update(h, nat.ptr(pos), nat.ptr(sums), nat.ptr(red), s),
                       "update")
-            comm.all_reduce(red, "max")
-            comm.all_gather_rows(full, rows)
-            nat.check(lib.cvz_fa2_shard_absorb(h, nat.ptr(red), nat.ptr(hist), s), "absorb")
+            self.comm.all_reduce(red, "max")
+            self.comm.all_gather_rows(self.full, self.rows)
+            nat.check(lib.cvz_fa2_shard_absorb(h, nat.ptr(red), hist, s), "absorb")
+            self.done += 1
+
+    def finish(self):
+        """(bad iteration (1-based, 0 = none), jitter seen)."""
         speed = ctypes.c_double(0)
         bad = ctypes.c_int64(0)
         jit = ctypes.c_int(0)
-        nat.call("cvz_fa2_shard_finish", h, ctypes.byref(speed), ctypes.byref(bad),
-                 ctypes.byref(jit), s)
+        nat.call("cvz_fa2_shard_finish", self.h, ctypes.byref(speed), ctypes.byref(bad),
+                 ctypes.byref(jit), self.s)
+        return int(bad.value), int(jit.value)
+
+    def close(self) -> None:
+        if self.h:
+            nat.load().cvz_fa2_shard_destroy(self.h, self.s)
+            self.h = ctypes.c_void_p()
+
+
+def _run_shard(comm, n, mass, e, ew, P, pos0, iterations, ref_ids):
+    """One node-sharded FA2 run from pos0 (full, identical on every rank).
+    Returns (padded positions, displacement history, bad, jitter_seen)."""
+    sh = ShardLayout(comm, n, mass, e, ew, P, pos0, iterations, ref_ids)
+    try:
+        sh.run(iterations)
+        bad, jit = sh.finish()
     finally:
-        nat.load().cvz_fa2_shard_destroy(h, s)
-    return full, hist, int(bad.value), int(jit.value)
+        sh.close()
+    return sh.full, sh.hist[:iterations], bad, jit
 
 
 def layout_sharded(obj, params: LayoutParams | None = None, comm: Comm | None = None,

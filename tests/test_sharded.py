@@ -238,3 +238,43 @@ def test_rmat_counter_stream_and_sharded_degrees():
     t = np.zeros((4, orc.default_cols(len(ee))), np.int64)
     orc.sketch_add_many(t, A, B, labels, deg)
     assert np.array_equal(s.table, t)
+
+
+def _rmat_fa2_worker(rank, world, port, out_dir, scale, iters):
+    dist = _init(rank, world, port)
+    import torch
+    torch.cuda.set_device(0)                      # both ranks share one B200
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import synth
+    from paper_2108_00529_b200.sharded import (Comm, from_edge_array_sharded, layout_sharded,
+                                               shard_range)
+    comm = Comm()
+    m = 16 << scale
+    lo, hi = shard_range(m, rank, world)
+    g = from_edge_array_sharded(synth.rmat_dev(scale, lo, hi - lo, seed=1), comm,
+                                node_count=1 << scale).gather()
+    r = layout_sharded(g, cv.LayoutParams(iterations=iters), comm)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), pos=r.positions, disp=r.displacement)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_sharded_fa2_rmat20_matches_single_gpu():
+    """C5-shaped node-sharded ForceAtlas2 (R-MAT scale 20: 2^20 bodies, 2^24
+    draws): two ranks, each with a CSR over the rows it owns only, give the
+    single-GPU layout within 1e-7 x diameter (only the Σswing/Σtraction sums
+    are regrouped)."""
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import synth
+    scale, iters = 20, 3
+    with tempfile.TemporaryDirectory() as d:
+        _spawn(_rmat_fa2_worker, 2, d, scale, iters)
+        r0, r1 = (np.load(os.path.join(d, f"r{i}.npz")) for i in (0, 1))
+    g = cv.from_edge_array(synth.rmat_dev(scale, 0, 16 << scale, seed=1), node_count=1 << scale)
+    ref = cv.layout(g, cv.LayoutParams(iterations=iters))
+    diam = np.hypot(*(ref.positions.max(0) - ref.positions.min(0)))
+    assert np.array_equal(r0["pos"], r1["pos"])
+    assert np.max(np.abs(r0["pos"] - ref.positions)) <= 1e-7 * diam
+    np.testing.assert_allclose(r0["disp"], ref.displacement, rtol=1e-6, atol=1e-9)
