@@ -22,7 +22,6 @@ import argparse
 import gc
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -55,59 +54,55 @@ def parse():
     p.add_argument("--config", default="C4")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-sharded", action="store_true")
+    p.add_argument("--no-secondary", action="store_true")
     return p.parse_args()
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock / throttle-reason sampler running during the timed region
+    (NVML polled every 20 ms from a thread; nvidia-smi's 200 ms loop missed
+    short regions)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, index=0):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    def __init__(self, index=0, period=0.02):
+        self.index, self.period = index, period
+        self.sm, self.mask, self.mx = [], 0, None
+        self._stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def loop():
+                while True:
+                    try:
+                        self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        self.mask |= int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+                    except Exception:  # noqa: BLE001 -- sampling must not fail the bench
+                        pass
+                    if self._stop.wait(self.period):
+                        return
+            self.t = threading.Thread(target=loop, daemon=True)
             self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+        except Exception:  # noqa: BLE001 -- no NVML: report no samples
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
+        self._stop.set()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = sorted(k for k, bit in self.REASONS.items() if self.mask & bit)
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None,
+                "sm_max_mhz": self.mx, "reasons": reasons, "samples": len(self.sm)}
 
 
 def dist_init(n_gpus):
@@ -170,7 +165,8 @@ def pipeline(cv, edges_dev, stats=None, mode="deterministic"):
                           contract_ms=ev[2].elapsed_time(ev[3]),
                           layout_ms=ev[3].elapsed_time(ev[4]),
                           m=g.edge_count, n=g.node_count, rounds=len(a.round_history),
-                          m_r=list(a.stream_edges), k=sg.node_count, se=sg.edge_count))
+                          m_r=list(a.stream_edges), m_dev=list(a.device_stream_edges),
+                          k=sg.node_count, se=sg.edge_count))
     return res
 
 
@@ -213,8 +209,10 @@ def kernel_bytes(name, st):
 
 def community_pass_bytes(st):
     """SURVEY.md 8(d): per round 16 m_r (pass read + relabel read) + 8 m_{r+1}
-    (compacted write) + 32 n (counters, labels, resolve, compose)."""
-    mr = st["m_r"]
+    (compacted write) + 32 n (counters, labels, resolve, compose), with m_r
+    the edges the device actually streams (dead edges dropped from the
+    stream are not read, so they are not counted)."""
+    mr = st["m_dev"]
     tot = 0
     for i, x in enumerate(mr):
         nxt = mr[i + 1] if i + 1 < len(mr) else 0
@@ -225,7 +223,7 @@ def community_pass_bytes(st):
 def roofline(prof, st, peak_gbs):
     ks = sorted(prof.items(), key=lambda kv: -kv[1][1])
     total = sum(v[1] for _, v in ks) or 1.0
-    top = [{"kernel": nm, "launches": c, "ms": round(ms, 4), "share": round(ms / total, 4)}
+    top = [{"kernel": nm, "n": c, "ms": round(ms, 3), "share": round(ms / total, 3)}
            for nm, (c, ms) in ks[:12]]
     name, (cnt, ms) = ks[0]
     b = kernel_bytes(name, st)
@@ -238,9 +236,8 @@ def roofline(prof, st, peak_gbs):
     if name.startswith("bh_"):
         # the tree walk is not HBM-bound: its node array is L1/L2-resident and
         # every visit is a dependent fp64 chain (profiles/r1g_ncu_full_c4_fa2.md)
-        roof["limiter"] = ("issue-bound tree walk, not HBM: ncu shows DRAM ~1% of peak, "
-                           "L1 hit ~96% (~15 distinct nodes per warp load), FP64 pipe ~37%, "
-                           "issue active ~59%; bytes are the compulsory body + tree reads")
+        roof["limiter"] = ("issue-bound fp64 tree walk (ncu: DRAM ~1%, L1 hit ~96%); "
+                           "see walk.fp64_frac")
     return roof, top
 
 
@@ -318,7 +315,8 @@ def run_ours(args, rank, ws):
         fms.append(f0.elapsed_time(f1))
     gc.enable()
     fast = dict(ms=float(np.median(fms)), ms_all=fms, rounds=len(fa.round_history),
-                m_r=list(fa.stream_edges), communities=fa.community_count)
+                m_r=list(fa.stream_edges), m_dev=list(fa.device_stream_edges),
+                communities=fa.community_count)
     del g
     # e2e through the public API from pinned host memory (warm-up as for the
     # device-resident steps: first calls pay pinned read-back buffer setup)
@@ -339,6 +337,99 @@ def run_ours(args, rank, ws):
     return dict(ms_step=ms_step, m_in=m_in, stage=st, launches=launches, clocks=clk.summary(),
                 bh_visits=bh_visits / ITERS, bh_inter=bh_inter / ITERS,
                 e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, prof=prof.kernels, fast=fast)
+
+
+# ------------------------------------------------- secondary named shapes
+def _timed(fn, reps):
+    """Median device time (ms) of fn() over reps calls after one warm-up."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    out = []
+    gc.collect()
+    gc.disable()
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b))
+    gc.enable()
+    return float(np.median(out))
+
+
+def run_secondary(reps=3):
+    """BASELINE.json configs[0..2] (north star: 'throughput on the named
+    shapes'), device-resident inputs, public API calls:
+      C1 full pipeline with 500 supergraph ForceAtlas2 iterations;
+      C2 deterministic community pass edges/s (and the whole path);
+      C3 BigGraphVis supergraph layout (pipeline mode, 100 iterations) vs
+         full-graph ForceAtlas2 (full mode, 500 iterations, C/cli.py:58) with
+         community colouring of every node (C/cli.py:191-203)."""
+    import torch
+
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import synth
+    from paper_2108_00529_b200.render import assign_colors, color_full_graph
+    out = {}
+    dev = {c: torch.from_numpy(synth.config_graph(c, seed=0)).to("cuda") for c in ("C1", "C2", "C3")}
+
+    def front(e):
+        g = cv.from_edge_array(e)
+        base = cv.degree_stats(g).mode_degree
+        a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+        s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+        cv.accumulate_sizes(s, a, g)
+        return g, a, cv.contract(g, a, s)
+
+    # C1: pipeline + 500 supergraph iterations
+    def c1():
+        g, a, sg = front(dev["C1"])
+        return cv.layout(sg, cv.LayoutParams(iterations=500, seed=0))
+    ms = _timed(c1, reps)
+    g, a, sg = front(dev["C1"])
+    out["C1"] = {"what": "full pipeline, 500 supergraph FA2 iterations", "ms_per_step": ms,
+                 "edges_per_s": g.edge_count / (ms / 1e3), "n": g.node_count, "m": g.edge_count,
+                 "supernodes": sg.node_count}
+    # C2: deterministic community pass
+    g2 = cv.from_edge_array(dev["C2"])
+    base2 = cv.degree_stats(g2).mode_degree
+    det_ms = _timed(lambda: cv.detect_communities(g2, cv.ThresholdSchedule(base=base2), seed=0,
+                                                  workers=1), reps)
+
+    def c2():
+        g, a, sg = front(dev["C2"])
+        return cv.layout(sg, cv.LayoutParams(iterations=ITERS, seed=0))
+    step2 = _timed(c2, reps)
+    out["C2"] = {"what": "deterministic (bit-exact) community pass; whole path with 100 "
+                         "supergraph iterations", "detect_ms": det_ms,
+                 "community_pass_edges_per_s": g2.edge_count / (det_ms / 1e3),
+                 "ms_per_step": step2, "n": g2.node_count, "m": g2.edge_count}
+    del g2
+    # C3: supergraph layout vs full-graph layout + colouring
+    g3, a3, sg3 = front(dev["C3"])
+    sup_ms = _timed(lambda: cv.layout(sg3, cv.LayoutParams(iterations=ITERS, seed=0)), reps)
+    full_iters = 500
+
+    def full_mode():
+        res = cv.layout(g3, cv.LayoutParams(iterations=full_iters, seed=0))
+        colors = assign_colors(sg3.weight)
+        return color_full_graph(a3.label, sg3.community_id, colors), res
+    full_ms = _timed(full_mode, 1)
+    front_ms = _timed(lambda: front(dev["C3"]), reps)
+    out["C3"] = {"what": "BigGraphVis supergraph layout (100 it) vs full-graph FA2 (500 it) + "
+                         "community colouring of every node",
+                 "front_ms": front_ms,
+                 "supergraph_layout_ms_per_iter": sup_ms / ITERS,
+                 "pipeline_mode_ms": front_ms + sup_ms,
+                 "full_graph_fa2_ms_per_iter": full_ms / full_iters,
+                 "full_mode_ms": front_ms + full_ms,
+                 "n": g3.node_count, "m": g3.edge_count, "supernodes": sg3.node_count,
+                 "superedges": sg3.edge_count}
+    del dev, g3, a3, sg3
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------ sharded stages
@@ -419,8 +510,9 @@ def run_c5(comm, rank, ws, reps=3):
     Each rank generates its own slice of the counter-based stream in HBM
     (cvz_rmat_edges, outside the timed region); the timed region is
     from_edge_array_sharded (compaction + degrees + all-reduce of 2^26 int64
-    degrees) + accumulate_sizes_sharded (edge-based +1 per endpoint under
-    labels = id // 64, all-reduce of the 4 x 107,375 counters, merge).
+    degrees) + accumulate_sizes_sharded (node-based: degree under label per
+    owned node, labels = id // 64, all-reduce of the 4 x 107,375 counters,
+    merge).
     Device time, max over ranks."""
     import torch
 
@@ -449,15 +541,15 @@ def run_c5(comm, rank, ws, reps=3):
     torch.cuda.synchronize()
     ms = barrier_max(t0.elapsed_time(t1) / reps, ws)
     m_kept = g.edge_count
-    # SURVEY.md 8(d) bytes of the stage: compaction 8 (read) + 8 (write) per
-    # draw, degrees 8 per kept edge + 8 per node (int64 counters), sketch
-    # (edge-based) 8 per kept edge (pair) + 2 label gathers of 8
-    ing_bytes = 16 * m5 / ws + 8 * m_kept / ws + 8 * n5 + 24 * m_kept / ws
+    # SURVEY.md 8(d) bytes per rank: compaction 8 (read pair) + 8 (write kept
+    # pair) per draw, degrees 8 per kept edge + 8 per node (int64 counters),
+    # sketch (node-based) 16 per owned node (label + degree)
+    ing_bytes = 16 * m5 / ws + 8 * m_kept / ws + 8 * n5 + 16 * n5 / ws
     out = {"scale": C5_SCALE, "nodes": n5, "edge_draws": m5, "edges_after_self_loops": m_kept,
            "ms": ms, "edges_per_s": m5 / (ms / 1e3),
            "hbm_frac_per_rank": ing_bytes / (ms / 1e3) / 1e9 / peak_hbm()[0],
-           "note": "edge-sharded compaction + degrees + sketch; labels = id // 64 (synthetic "
-                   "communities; the order-dependent community pass is not sharded)"}
+           "note": "edge-sharded compaction + degrees, node-sharded sketch; labels = id // 64 "
+                   "(synthetic communities; the order-dependent community pass is not sharded)"}
     del e5, labels
     # node-sharded full-graph ForceAtlas2 on the same R-MAT-26 graph: every
     # rank holds the whole compacted edge list (all-gather), builds its CSR
@@ -545,6 +637,63 @@ def cpu_pipeline_sample(config, seed=0):
                                layout_s_per_iter=(t2 - t1) / CPU_LAYOUT_ITERS, k=k, se=len(se))
 
 
+def reference_package_sample(config, seed=0):
+    """The shipped reference itself (commviz + numba, oracle/_ref packaged by
+    oracle/build_ref.py) on the same full graph, NUMBA_NUM_THREADS = all host
+    cores, after its own warmup_jit() (C/cli.py:278-287) plus one untimed
+    pass over the C1 graph (warmup_jit leaves the supergraph layout's
+    signatures uncompiled: 3.7 s of JIT on the first real call).  Every stage
+    in full except the layout, timed for CPU_LAYOUT_ITERS of the 100
+    iterations and extrapolated.  Run once per bench
+    invocation (about a minute at C4, dominated by contract's
+    np.unique(axis=0))."""
+    import importlib
+
+    from oracle import build_ref
+    from paper_2108_00529_b200 import synth
+    ref = build_ref.load()
+    importlib.import_module("commviz.cli").warmup_jit()
+
+    def run(e, st):
+        t = time.perf_counter()
+        g = ref.from_edge_array(e)
+        base = ref.degree_stats(g).mode_degree
+        st["ingest_s"] = time.perf_counter() - t
+        t = time.perf_counter()
+        a = ref.detect_communities(g, ref.ThresholdSchedule(base=base), seed=0, workers=1)
+        st["detect_s"] = time.perf_counter() - t
+        t = time.perf_counter()
+        s = ref.sketch_new(4, ref.default_cols(g.edge_count), seed=0)
+        ref.accumulate_sizes(s, a.label, g.degree)
+        sg = ref.contract(g, a.label, s)
+        st["sketch_contract_s"] = time.perf_counter() - t
+        t = time.perf_counter()
+        ref.layout(sg, ref.LayoutParams(iterations=CPU_LAYOUT_ITERS, seed=0))
+        st["layout_s_per_iter"] = (time.perf_counter() - t) / CPU_LAYOUT_ITERS
+        return a, sg
+
+    run(synth.config_graph("C1", seed=seed).astype(np.int64), {})  # warm-up
+    e = synth.config_graph(config, seed=seed).astype(np.int64)
+    st = {}
+    a, sg = run(e, st)
+    total = (st["ingest_s"] + st["detect_s"] + st["sketch_contract_s"]
+             + st["layout_s_per_iter"] * ITERS)
+    return {"value": len(e) / total, "unit": "edges/s", "kind": "reference",
+            "cores": os.cpu_count(), "s_per_step_est": total, "stages": st,
+            "communities": int(a.community_count), "supernodes": int(sg.node_count),
+            "sample": f"unmodified commviz package (numba {__import__('numba').__version__}, "
+                      f"NUMBA_NUM_THREADS={os.environ.get('NUMBA_NUM_THREADS', os.cpu_count())}) "
+                      f"on the full {config} graph after warmup_jit + a C1 pass; layout "
+                      f"{CPU_LAYOUT_ITERS} of {ITERS} iterations extrapolated; run once"}
+
+
+def config_dict(args, ws):
+    """The workload description both arms print (identical by construction)."""
+    return {"workload": workload(args.config), "layout_iterations": ITERS,
+            "community_mode": "deterministic", "parallelism": f"replicas x{ws}",
+            "l2": "inputs (262 MB edge list at C4) larger than the 126 MB L2"}
+
+
 def main():
     args = parse()
     rank, ws, local = dist_init(args.gpus)
@@ -564,70 +713,102 @@ def main():
                   f"(C/numpy port of commviz); layout timed for {CPU_LAYOUT_ITERS} of {ITERS} "
                   f"iterations and extrapolated ({det['layout_s_per_iter']:.2f} s/iter, "
                   f"measured {det['measured_s']:.1f} s per step)")
-        print(json.dumps({
+        line = {
             "impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32+f64",
-            "data": "synthetic", "config": {"workload": workload(args.config), "sample": sample},
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int32 ids / f64 layout", "data": "synthetic (seeded DC-SBM, no network)",
+            "config": config_dict(args, args.gpus),
             "cpu_baseline": {"value": v, "unit": "edges/s", "cores": orc.num_threads(),
                              "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}))
+                    "d2h_bytes_per_step": 0}}
+        # the shipped package itself beside the port (once; not the value)
+        try:
+            line["reference_package"] = reference_package_sample(args.config)
+        except Exception as ex:  # noqa: BLE001 -- report why, keep the port's line
+            line["reference_package"] = {"unavailable": f"{type(ex).__name__}: {ex}"[:200]}
+        print(json.dumps(line))
         return
 
     r = run_ours(args, rank, ws)
     shard = None if args.no_sharded else run_sharded(args, rank, ws)
+    secondary = None if (args.no_secondary or args.config != "C4") else run_secondary()
     if rank != 0:
         return
+    import ctypes
+
+    from paper_2108_00529_b200 import _native
     st = r["stage"]
     peak, _src = peak_hbm()
     roof, top = roofline(r["prof"], st, peak)
     roof["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs ({_src})"
+    fp64 = ctypes.c_double(0)
+    _native.call("cvz_probe_fp64", ctypes.byref(fp64), _native.stream())
     if roof.get("kernel", "").startswith("bh_flat") and r.get("bh_inter"):
         # per-iteration walk counts (instrumented step) over the timed walk:
         # ~20 fp64 flops per accepted term (d, 1/d^2 seed + cubic step, f,
         # f*d accumulate), ~6 per opened cell (d, d^2, theta^2 d^2 test)
         sec = roof["launch_ms"] / 1e3
         acc, vis = r["bh_inter"], r["bh_visits"]
+        gfl = (20 * acc + 6 * (vis - acc)) / sec / 1e9
         roof["walk"] = {"node_visits_per_iter": vis, "interactions_per_iter": acc,
-                        "interactions_per_s": acc / sec,
-                        "fp64_gflops_est": (20 * acc + 6 * (vis - acc)) / sec / 1e9}
+                        "interactions_per_s": acc / sec, "fp64_gflops_est": gfl,
+                        "fp64_peak_gflops": fp64.value,
+                        "fp64_peak_source": "cvz_probe_fp64 (measured DFMA throughput, this GPU)",
+                        "fp64_frac": gfl / fp64.value if fp64.value else None}
     try:  # DRAM bytes per launch from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             roof["traffic"] = json.load(fh).get(roof["kernel"])
     except (OSError, ValueError):
         pass
     value = r["m_in"] * ws / (r["ms_step"] / 1000.0)
+    fast_bytes = community_pass_bytes(dict(st, m_dev=r["fast"]["m_dev"]))
+    det_bytes = community_pass_bytes(st)
+    summary = {
+        # the BASELINE metric's three parts at C4, kept last so they survive
+        # any truncation of the line's head
+        "community_pass_edges_per_s": st["m"] / (st["detect_ms"] / 1000.0),
+        "community_pass_hbm_frac": det_bytes / (st["detect_ms"] / 1000.0) / 1e9 / peak,
+        "community_pass_fast_edges_per_s": st["m"] / (r["fast"]["ms"] / 1000.0),
+        "community_pass_fast_hbm_frac": fast_bytes / (r["fast"]["ms"] / 1000.0) / 1e9 / peak,
+        # edges the device streams, summed over rounds
+        "community_pass_stream_edges_per_s": sum(st["m_dev"]) / (st["detect_ms"] / 1000.0),
+        "ms_per_fa2_iter": st["layout_ms"] / ITERS,
+        "end_to_end_s": r["ms_step"] / 1000.0,
+        "e2e_s": r["e2e_ms"] / 1000.0,
+        "stage_ms": {k: round(st[k], 4) for k in ("ingest_ms", "detect_ms", "contract_ms",
+                                                   "layout_ms")},
+        "walk_fp64_frac": roof.get("walk", {}).get("fp64_frac"),
+    }
+    if shard:
+        c5 = shard.get("c5_rmat26_degrees_sketch") or {}
+        summary["c5_ingest_sketch_edges_per_s"] = c5.get("edges_per_s")
+        summary["c5_ingest_sketch_hbm_frac"] = c5.get("hbm_frac_per_rank")
+        summary["c5_full_graph_fa2_ms_per_iter"] = (c5.get("fa2") or {}).get("ms_per_iter")
+        summary["c4_full_graph_fa2_ms_per_iter"] = shard.get("full_graph_fa2_ms_per_iter")
+    if secondary:
+        summary["c1_ms_per_step_500it"] = secondary["C1"]["ms_per_step"]
+        summary["c2_community_pass_edges_per_s"] = secondary["C2"]["community_pass_edges_per_s"]
+        summary["c3_supergraph_ms_per_iter"] = secondary["C3"]["supergraph_layout_ms_per_iter"]
+        summary["c3_full_graph_ms_per_iter"] = secondary["C3"]["full_graph_fa2_ms_per_iter"]
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_step"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int32 ids / f64 layout", "data": "synthetic (seeded DC-SBM, no network)",
-        "config": {"workload": workload(args.config), "edges_in": r["m_in"], "n": st["n"], "m": st["m"],
-                   "rounds": st["rounds"], "supernodes": st["k"], "superedges": st["se"],
-                   "layout_iterations": ITERS, "community_mode": "deterministic",
-                   "parallelism": f"replicas x{ws}",
-                   "l2": "inputs (262 MB edge list) larger than the 126 MB L2"},
-        "community_pass_edges_per_s": st["m"] / (st["detect_ms"] / 1000.0),
-        # also the streamed edges summed over rounds per second
-        "community_pass_stream_edges_per_s": sum(st["m_r"]) / (st["detect_ms"] / 1000.0),
-        # sketch sizing + supergraph contraction, per input edge
-        "sketch_contract_edges_per_s": st["m"] / (st["contract_ms"] / 1000.0),
-        "ms_per_fa2_iter": st["layout_ms"] / ITERS,
-        "end_to_end_s": r["ms_step"] / 1000.0,
-        "stage_ms": {k: st[k] for k in ("ingest_ms", "detect_ms", "contract_ms", "layout_ms")},
-        "community_pass_fast": {
-            "edges_per_s": st["m"] / (r["fast"]["ms"] / 1000.0), "ms": r["fast"]["ms"],
-            "ms_per_call": r["fast"]["ms_all"],
-            "rounds": r["fast"]["rounds"], "communities": r["fast"]["communities"],
-            "hbm_frac": community_pass_bytes(dict(st, m_r=r["fast"]["m_r"])) /
-            (r["fast"]["ms"] / 1000.0) / 1e9 / peak},
-        "community_pass_hbm_frac": community_pass_bytes(st) / (st["detect_ms"] / 1000.0) / 1e9 / peak,
-        "roofline": roof,
-        "top_kernels": top,
+        "config": config_dict(args, ws),
+        "workload_stats": {"edges_in": r["m_in"], "n": st["n"], "m": st["m"],
+                           "rounds": st["rounds"], "m_r": st["m_r"], "m_r_streamed": st["m_dev"],
+                           "supernodes": st["k"], "superedges": st["se"],
+                           "fast_mode": {k: r["fast"][k] for k in ("ms", "rounds", "communities",
+                                                                    "m_dev")}},
         "gpu_launches": r["launches"],
-        "sharded": shard,
         "clocks": r["clocks"],
+        "roofline": roof,
+        "top_kernels": top[:8],
+        "sharded": shard,
+        "secondary": secondary,
         "e2e": {"value": r["m_in"] * ws / (r["e2e_ms"] / 1000.0), "unit": "edges/s",
                 "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
                 "ms_per_step": r["e2e_ms"]},
@@ -641,6 +822,7 @@ def main():
             "sample": f"same full graph ({m} edges); oracle stages in full, layout "
                       f"{CPU_LAYOUT_ITERS} of {ITERS} iterations extrapolated "
                       f"({det['layout_s_per_iter']:.2f} s/iter); est. {dt:.1f} s/step"}
+    line["summary"] = summary
     print(json.dumps(line))
 
 

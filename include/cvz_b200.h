@@ -66,6 +66,12 @@ const char *cvz_profile_report(void);
  * No reference counterpart. */
 int cvz_bh_stats(int enable, unsigned long long *totals);
 
+/* FP64 FMA throughput probe (the Barnes-Hut walk's compute roofline, which
+ * MEASURED_PEAKS.json does not carry): 8 independent DFMA chains per thread
+ * at full occupancy on every SM, best of 3 timed launches; *gflops [host].
+ * Synchronises `stream`.  Measurement only.  No reference counterpart. */
+int cvz_probe_fp64(double *gflops, void *stream);
+
 /* ---------------------------------------------------------------- graph */
 
 /* C/graph.py:114-122 from_edge_array (mask u==v keeping stream order) and

@@ -227,7 +227,8 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
     next_m = nat._I64(0)
     changed = ctypes.c_int(0)
     rs = 0 if round_stream == "contract" else 1
-    streamed = []  # m_r per executed round (bench roofline bytes; no reference counterpart)
+    streamed = []  # m_r per executed round (reference semantics; no reference counterpart)
+    on_device = []  # edges the device actually streams per round (m_r minus dead edges)
     # Edges between two saturated communities are no-ops in every later round
     # once the threshold is pinned at its cap; with the identity order they
     # can leave the device stream (counted in `dead`, see cvz_detect_round).
@@ -237,6 +238,7 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
         if m_cur + dead == 0:
             break
         streamed.append(m_cur + dead)
+        on_device.append(m_cur)
         thr = min(schedule.threshold(i), cap)
         nthr = min(schedule.threshold(i + 1), cap)
         drop = workers <= 1 and rs == 0 and nthr == cap
@@ -257,6 +259,7 @@ def detect_communities(g, schedule: ThresholdSchedule, seed: int = 0,
     a = CommunityAssignment(label=Dual(dev=node_lab), counter_degree=Dual(dev=deg),
                             round_history=_History(history))
     a.stream_edges = streamed
+    a.device_stream_edges = on_device
     a._label.prefetch()  # the labels reach the host while later stages run
     return a
 

@@ -9,8 +9,9 @@
 // Two add paths:
 //  * staged: the whole rows x cols table lives in shared memory as u64
 //    (default 4 x 6500 = 208 KB fits one CTA per SM); each CTA accumulates
-//    its slice of keys there with warp-aggregated shared atomics and flushes
-//    only non-zero cells with one global 64-bit RED each;
+//    its contiguous slice of keys there with plain 64-bit shared atomics
+//    (collisions inside a warp are rare over 6,500+ columns) and stores its
+//    partial table with coalesced plain stores; one pass sums the partials;
 //  * direct: warp-aggregated 64-bit global atomics into the L2-resident table
 //    for tables too big for shared memory (e.g. 4 x 107,375 at 2^30 edges).
 #include "common.cuh"
@@ -233,10 +234,11 @@ void sketch_accumulate(int64_t *table, int rows, int64_t cols, const int64_t *ha
                                           (int)STAGED_MAX_BYTES));
             return 1;
         });
-        // one CTA per SM (the table fills its shared memory); each writes
-        // a partial table, one pass sums them into the sketch
-        long long want = k / (2LL * rows * cols) + 1;
-        unsigned grid = (unsigned)std::min<long long>(want, num_sms());
+        // one CTA per SM (the table fills its shared memory), on every SM
+        // once there are >= 16K keys per CTA; each CTA writes a partial
+        // table, one pass sums them into the sketch
+        unsigned grid = (unsigned)std::max<long long>(
+            1, std::min<long long>((k + 16383) / 16384, num_sms()));
         Scratch sc(s);
         auto *partial = sc.alloc<unsigned long long>((size_t)grid * rows * cols);
         CVZ_LAUNCH(add_staged_kernel<Src>, grid, 1024, bytes, s, partial, pa, pb, rows,

@@ -8,10 +8,12 @@ counterparts while splitting the work:
   contiguous slice of the edge stream (stable self-loop drop, C/graph.py:
   117-118) and counts degrees over it; one all-reduce(SUM) of the int64
   histogram gives np.bincount of the whole stream (C/graph.py:121), bit-exact.
-* `accumulate_sizes_sharded` -- edge-sharded sketch build: +1 under the
-  label of each endpoint of the local edges into a rank-local delta table, one
-  all-reduce(SUM) of rows x cols counters, then merge + saturate.  Integer
-  addition mod 2^64 makes this bit-identical to C/supergraph.py:42-46.
+* `accumulate_sizes_sharded` -- node-sharded sketch build: degree under the
+  label of each node of the rank's node range into a rank-local delta table
+  (the degrees are global after the ingest all-reduce), one all-reduce(SUM)
+  of rows x cols counters, then merge + saturate.  Integer addition mod 2^64
+  makes this bit-identical to C/supergraph.py:42-46
+  (`accumulate_sizes_edges_sharded` is the edge-based form).
 * `layout_sharded` -- node-sharded ForceAtlas2: every rank holds all
   positions, builds the full Barnes-Hut tree, and moves the nodes it owns;
   per iteration two tiny all-reduces (Σswing/Σtraction, bbox/max-disp/bad)
@@ -241,9 +243,41 @@ def broadcast_labels(labels, n: int, comm: Comm | None = None, src: int = 0):
 
 # ---------------------------------------------------------------- sketch
 def accumulate_sizes_sharded(sketch, labels, g: ShardedGraph) -> None:
-    """Edge-sharded C/supergraph.py:42-46: each rank adds +1 under the label
-    of both endpoints of its local edges; counters are summed across ranks
-    (bit-identical to the node-based single-GPU table)."""
+    """Node-sharded C/supergraph.py:42-46: after the degree all-reduce every
+    rank holds the global degrees, so each adds degree[v] under label[v] for
+    the nodes v of its own contiguous node range into a rank-local delta
+    table; the deltas are summed across ranks (all-reduce of rows x cols
+    counters) and merged + saturated once.  Integer addition mod 2^64 makes
+    this bit-identical to the single-GPU node-based table, and each rank
+    streams 16 B per owned node instead of gathering a label per endpoint of
+    its edges (node ranges or edge ranges)."""
+    T = nat.torch()
+    lab = _labels_dev(labels)
+    if int(lab.shape[0]) < g.node_count:
+        raise ValueError("one label per node required")
+    delta = T.zeros((sketch.rows, sketch.cols), dtype=T.int64, device=nat.device())
+    a, b = sketch._hash_dev()
+    lo, hi = shard_range(g.node_count, g.comm.rank, g.comm.world)
+    deg = g.degree_dev()
+    if hi > lo:
+        nat.call("cvz_sketch_accumulate", nat.ptr(delta), sketch.rows, sketch.cols,
+                 nat.ptr(a), nat.ptr(b), nat.ptr(lab[lo:hi]), nat.ptr(deg[lo:hi]), hi - lo,
+                 nat.stream())
+    g.comm.all_reduce(delta, "sum")
+    table = sketch.table_dev()
+    sat = T.zeros(1, dtype=T.int32, device=nat.device())
+    nat.call("cvz_sketch_merge", nat.ptr(table), nat.ptr(delta), sketch.rows, sketch.cols,
+             nat.ptr(sat), nat.stream())
+    sketch._table.set_dev(table)
+    if int(sat.item()) and not sketch.saturated:
+        sketch.saturated = True
+        warnings.warn("sketch counter overflow, counts saturated", RuntimeWarning, stacklevel=2)
+
+
+def accumulate_sizes_edges_sharded(sketch, labels, g: ShardedGraph) -> None:
+    """The edge-sharded form (+1 under the label of both endpoints of each
+    local edge; identical counters to the node-based form).
+    Kept for graphs whose degree array is not replicated."""
     T = nat.torch()
     lab = _labels_dev(labels)
     if int(lab.shape[0]) < g.node_count:

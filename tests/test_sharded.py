@@ -114,6 +114,14 @@ def _cpu_worker(rank, world, port, out_dir):
     table = np.zeros((4, cols), np.int64)
     orc.sketch_add_many(table, A, B, lab, deg)    # node-based, single process
     assert np.array_equal(dt.numpy(), table)
+    # node-range form (accumulate_sizes_sharded): degree under label per
+    # owned node after the degree all-reduce
+    nlo, nhi = shard_range(n_full, rank, world)
+    nd = np.zeros((4, cols), np.int64)
+    orc.sketch_add_many(nd, A, B, lab[nlo:nhi], deg_loc.numpy()[nlo:nhi])
+    ndt = torch.from_numpy(nd)
+    comm.all_reduce(ndt, "sum")
+    assert np.array_equal(ndt.numpy(), table)
     dist.barrier()
     dist.destroy_process_group()
     open(os.path.join(out_dir, f"ok{rank}"), "w").close()
@@ -221,7 +229,8 @@ def test_rmat_counter_stream_and_sharded_degrees():
     import paper_2108_00529_b200 as cv
     from oracle import oracle as orc
     from paper_2108_00529_b200 import synth
-    from paper_2108_00529_b200.sharded import (Comm, accumulate_sizes_sharded,
+    from paper_2108_00529_b200.sharded import (Comm, accumulate_sizes_edges_sharded,
+                                               accumulate_sizes_sharded,
                                                from_edge_array_sharded)
     scale, m = 14, 16 << 14
     host = synth.rmat_counter(scale, 0, m, seed=3)
@@ -238,6 +247,9 @@ def test_rmat_counter_stream_and_sharded_degrees():
     t = np.zeros((4, orc.default_cols(len(ee))), np.int64)
     orc.sketch_add_many(t, A, B, labels, deg)
     assert np.array_equal(s.table, t)
+    s2 = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    accumulate_sizes_edges_sharded(s2, labels, g)   # edge-based form, same counters
+    assert np.array_equal(s2.table, t)
 
 
 def _rmat_fa2_worker(rank, world, port, out_dir, scale, iters):
