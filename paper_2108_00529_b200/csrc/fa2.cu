@@ -1732,11 +1732,13 @@ static unsigned long long *g_bh_stats = nullptr;
 constexpr int TS_THREADS = 256;
 constexpr int TS_ITEMS = 8;
 constexpr int TS_TILE = TS_THREADS * TS_ITEMS;
+// tile counts up to this use per-CTA digit sums (CVZ_TS_SMALL overrides)
+constexpr int TS_SMALL_TILES = 64;
 
 __global__ void __launch_bounds__(TS_THREADS) tree_sort_coop_kernel(
     const unsigned *kin, const unsigned *vin, unsigned *kout,
     unsigned *vout, unsigned *kalt, unsigned *valt, unsigned *hist, unsigned *prefix, int n,
-    int end_bit) {
+    int end_bit, int small_tiles) {
     namespace cg = cooperative_groups;
     using Sort = cub::BlockRadixSort<unsigned, TS_THREADS, TS_ITEMS, unsigned>;
     using Scan = cub::BlockScan<unsigned, TS_THREADS>;
@@ -1779,26 +1781,41 @@ __global__ void __launch_bounds__(TS_THREADS) tree_sort_coop_kernel(
         __syncthreads();
         if (c < tiles) hist[(size_t)c * 256 + t] = cnt[t];
         grid.sync();
-        // per digit, an exclusive scan over tiles (CTA g takes digits g,
-        // g + grid, ...): one L2 round trip per digit instead of a
-        // tiles-long dependent chain in every CTA
-        for (int d = c; d < 256; d += gridDim.x) {
-            unsigned run = 0;
-            for (int c0 = 0; c0 < tiles; c0 += TS_THREADS) {
-                const int cc = c0 + t;
-                const unsigned h = cc < tiles ? __ldcg(hist + (size_t)cc * 256 + d) : 0u;
-                unsigned ex, agg;
-                Scan(tmp.scan).ExclusiveSum(h, ex, agg);
-                __syncthreads();
-                if (cc < tiles) prefix[(size_t)cc * 256 + d] = run + ex;
-                run += agg;
+        unsigned pre, run;  // this tile's start within digit t, digit t's total
+        if (tiles <= small_tiles) {
+            // few tiles: every CTA sums the digit columns itself (thread t =
+            // digit t, independent L2 loads) -- no second grid barrier and
+            // no per-digit block-scan chain (a 1-tile grid used to walk all
+            // 256 digits serially: 376 us per launch at C1)
+            pre = 0;
+            run = 0;
+            for (int cc = 0; cc < tiles; ++cc) {
+                const unsigned h = __ldcg(hist + (size_t)cc * 256 + t);
+                pre += cc < c ? h : 0u;
+                run += h;
             }
-            if (t == 0) prefix[(size_t)tiles * 256 + d] = run;  // digit total
+        } else {
+            // per digit, an exclusive scan over tiles (CTA g takes digits g,
+            // g + grid, ...): one L2 round trip per digit instead of a
+            // tiles-long dependent chain in every CTA
+            for (int d = c; d < 256; d += gridDim.x) {
+                unsigned r = 0;
+                for (int c0 = 0; c0 < tiles; c0 += TS_THREADS) {
+                    const int cc = c0 + t;
+                    const unsigned h = cc < tiles ? __ldcg(hist + (size_t)cc * 256 + d) : 0u;
+                    unsigned ex, agg;
+                    Scan(tmp.scan).ExclusiveSum(h, ex, agg);
+                    __syncthreads();
+                    if (cc < tiles) prefix[(size_t)cc * 256 + d] = r + ex;
+                    r += agg;
+                }
+                if (t == 0) prefix[(size_t)tiles * 256 + d] = r;  // digit total
+            }
+            grid.sync();
+            pre = c < tiles ? __ldcg(prefix + (size_t)c * 256 + t) : 0u;
+            run = __ldcg(prefix + (size_t)tiles * 256 + t);
         }
-        grid.sync();
         if (c < tiles) {
-            const unsigned pre = __ldcg(prefix + (size_t)c * 256 + t);
-            const unsigned run = __ldcg(prefix + (size_t)tiles * 256 + t);
             unsigned dbase;
             Scan(tmp.scan).ExclusiveSum(run, dbase);
             __syncthreads();
@@ -1823,6 +1840,11 @@ __global__ void __launch_bounds__(TS_THREADS) tree_sort_coop_kernel(
         ks = kd;
         vs = vd;
     }
+}
+
+static int ts_small_tiles() {
+    static const int v = getenv("CVZ_TS_SMALL") ? atoi(getenv("CVZ_TS_SMALL")) : TS_SMALL_TILES;
+    return v;
 }
 
 // Largest n the cooperative sort takes on this device (0 = unavailable).
@@ -1951,7 +1973,7 @@ struct Tree {
         if (sort_alt) {  // supergraph sizes: one cooperative launch
             CVZ_COOP_N(tree_sort_coop_kernel, (unsigned)((n + TS_TILE - 1) / TS_TILE), TS_THREADS,
                        s, klo, idx, klo2, idx2, sort_alt, sort_alt + n, sort_hist,
-                       sort_hist + tiles_ts * 256, n, 2 * top_digits);
+                       sort_hist + tiles_ts * 256, n, 2 * top_digits, ts_small_tiles());
         } else {
             CVZ_REGION("cub_sort:tree_keys", s);
             CVZ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, klo, klo2, idx, idx2, n, 0,
