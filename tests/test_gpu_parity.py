@@ -247,6 +247,40 @@ def test_fast_mode_within_tolerance(cv, orc, name):
         assert np.all(lab[lab] == lab)
 
 
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_fast_mode_within_tolerance_at_scale(cv, orc, name, monkeypatch):
+    """The same envelope gate at the bench's shapes (C4 is the one the bench
+    reports fast mode on).  Reference envelope: the oracle's sequential pass
+    under workers in {1, 4, 64} (one seed each); the interleaved processing
+    orders come from the native make_schedule, which is bit-exact with the
+    oracle's Python loop (tests/test_host.py) and ~200x faster -- the loop
+    would take minutes per round at 34M edges."""
+    from paper_2108_00529_b200 import synth
+    from paper_2108_00529_b200.community import make_schedule
+    monkeypatch.setattr(orc, "make_schedule", make_schedule)
+    e = synth.config_graph(name)
+    g = cv.from_edge_array(e)
+    base = cv.degree_stats(g).mode_degree
+    n, ee, deg = orc.from_edge_array(e)
+    qs, ks, ts = [], [], []
+    for workers in (1, 4, 64):
+        lab, _, _ = orc.detect_communities(n, ee, deg, base, 10, 0, workers=workers)
+        qs.append(orc.modularity(ee, deg, lab))
+        ks.append(len(np.unique(lab)))
+        ts.append(_top10(lab))
+    runs = [cv.detect_communities(g, cv.ThresholdSchedule(base=base), workers=1, mode="fast")
+            for _ in range(3)]
+    q_fast = float(np.median([orc.modularity(g.edges, g.degree, f.label) for f in runs]))
+    assert min(qs) - 0.02 <= q_fast <= max(qs) + 0.02, (q_fast, min(qs), max(qs))
+    kf = float(np.median([f.community_count for f in runs]))
+    assert 0.95 * min(ks) <= kf <= 1.05 * max(ks), (kf, min(ks), max(ks))
+    t = float(np.median([_top10(f.label) for f in runs]))
+    assert min(ts) - 0.02 <= t <= max(ts) + 0.02, (t, min(ts), max(ts))
+    for f in runs:
+        lab = f.label
+        assert np.all(lab[lab] == lab)
+
+
 def test_gpu_modularity_matches_oracle(cv, orc):
     from paper_2108_00529_b200 import synth
     e = synth.config_graph("C1")
@@ -697,6 +731,29 @@ def test_long_layout_final_stress_within_2pct(cv, orc):
     ref = _stress(pos, sg.edges, ew)
     assert np.all(np.abs(ours - ref) <= 0.02 * np.abs(ref)), (ours, ref)
     assert abs(res.displacement[-1] - disp[-1]) <= 0.02 * max(disp[-1], 1e-12) + 1e-9
+
+
+def test_c4_supergraph_100_iterations_final_stress(cv, orc):
+    """The bench's own layout workload: the C4 supergraph (318,813 supernodes,
+    5.17M superedges) laid out for the full 100 iterations, gated on final
+    stress and final displacement within 2 % of the oracle's run from the
+    same initial positions."""
+    from paper_2108_00529_b200 import synth
+    e = synth.config_graph("C4")
+    g = cv.from_edge_array(e)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=cv.degree_stats(g).mode_degree),
+                              workers=1)
+    s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    cv.accumulate_sizes(s, a, g)
+    sg = cv.contract(g, a, s)
+    res = cv.layout(sg, cv.LayoutParams(iterations=100))
+    mass, ew = orc.masses_supergraph(sg.weight, sg.multiplicity)
+    pos, disp = orc.layout(sg.node_count, mass, sg.edges, ew, iterations=100)
+    ours = _stress(res.positions, sg.edges, ew)
+    ref = _stress(pos, sg.edges, ew)
+    assert np.all(np.abs(ours - ref) <= 0.02 * np.abs(ref)), (ours, ref)
+    assert abs(res.displacement[-1] - disp[-1]) <= 0.02 * max(disp[-1], 1e-12) + 1e-9
+    assert np.all(np.isfinite(res.positions))
 
 
 def _pipeline_vs_oracle(cv, orc, e, node_count=None, iters=3, check_layout=True):
