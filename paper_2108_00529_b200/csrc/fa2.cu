@@ -2028,7 +2028,9 @@ struct Tree {
         return force_flat || !binary;
     }
     // reference cell numbering of the current tree (see cell_entries_kernel)
-    void build_ids(cudaStream_t s) {
+    // scratch of build_ids: allocated before a CUDA-graph capture (stream-
+    // ordered allocation inside the capture is refused)
+    void alloc_ids(cudaStream_t s) {
         if (!idslot) {
             ne = 2 * (n - 1) + n;
             ekey = scr->alloc<unsigned long long>(ne);
@@ -2044,6 +2046,9 @@ struct Tree {
             CVZ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, etmp_scan, ecnt2, eexcl, ne, s));
             etmp = scr->alloc<char>(std::max(etmp_sort, etmp_scan));
         }
+    }
+    void build_ids(cudaStream_t s) {
+        alloc_ids(s);
         CVZ_CUDA(cudaMemsetAsync(visit, 0, sizeof(unsigned) * (n - 1), s));
         CVZ_LAUNCH(i12_kernel, grid_for(n, FB, 1, 8), FB, 0, s, bodies, n, left, last, parent_int,
                    parent_leaf, rc_by_split, visit, i12);
@@ -2609,6 +2614,7 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
         };
 
         auto run_all = [&](bool ids) {
+            if (ids && !exact) tree.alloc_ids(s);  // never allocate inside the capture
             bbox_dev(p2, N, bbox, sc, s);  // first bbox; later ones come from update
             bool use_graph =
                 getenv("CVZ_NO_GRAPH") == nullptr && P->iterations > 1 && !prof_on();
