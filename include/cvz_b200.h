@@ -74,6 +74,16 @@ int cvz_probe_fp64(double *gflops, void *stream);
 
 /* ---------------------------------------------------------------- graph */
 
+/* Host (m,2) edge array [host, pageable or pinned; int64 or int32 per
+ * in_is_int32] -> dev_out [dev] int32 pairs, same order.  The drop-in input
+ * path of C/graph.py:114-122 (the reference takes int64 numpy arrays): ids
+ * are range-checked and narrowed to int32 on the host by a thread pool into
+ * page-locked staging buffers whose DMA overlaps the next chunk's
+ * conversion.  Ids outside [0, 2^31) -> CVZ_ERR_RANGE.  Returns with the
+ * copies queued on `stream` (the host array may be reused immediately). */
+int cvz_edges_upload(const void *host_edges, int in_is_int32, int64_t m, int32_t *dev_out,
+                     void *stream);
+
 /* C/graph.py:114-122 from_edge_array (mask u==v keeping stream order) and
  * C/graph.py:121 np.bincount.  Stable single-pass compaction of an (m,2)
  * edge array ([dev] int64 or int32, in_is_int32 selects) into int32 pairs,

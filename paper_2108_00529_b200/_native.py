@@ -47,6 +47,7 @@ SIGNATURES = {
     "cvz_profile_report": [],
     "cvz_bh_stats": [_I32, _P],
     "cvz_probe_fp64": [ctypes.POINTER(_D), _P],
+    "cvz_edges_upload": [_P, _I32, _I64, _P, _P],
     "cvz_edges_compact": [_P, _I32, _I64, _P, _P, _P, _I32, _P],
     "cvz_degree_count": [_P, _I64, _I64, _P, _P],
     "cvz_degree_stats": [_P, _I64, _P, _P],

@@ -254,6 +254,23 @@ def write_edge_list(g: Graph, path_or_file) -> None:
         path_or_file.write(body.decode("ascii"))
 
 
+def upload_edges(edges):
+    """A host (m, 2) edge array (the reference's int64 numpy input, or int32;
+    pageable or pinned) as an (m, 2) int32 CUDA tensor: range-checked and
+    narrowed on the host into page-locked staging buffers whose DMA overlaps
+    the next chunk's conversion (cvz_edges_upload)."""
+    T = nat.torch()
+    arr = np.asarray(edges)
+    if arr.dtype not in (np.int32, np.int64):
+        arr = np.asarray(arr, dtype=np.int64)
+    arr = np.ascontiguousarray(arr).reshape(-1, 2)
+    m = int(arr.shape[0])
+    dev = T.empty((max(m, 1), 2), dtype=T.int32, device=nat.device())
+    nat.call("cvz_edges_upload", arr.ctypes.data_as(ctypes.c_void_p),
+             int(arr.dtype == np.int32), m, nat.ptr(dev), nat.stream())
+    return dev[:m]
+
+
 def from_edge_array(edges, node_count=None) -> Graph:
     """C/graph.py:114-122 on the GPU: stable self-loop drop + degree histogram.
 
@@ -266,11 +283,7 @@ def from_edge_array(edges, node_count=None) -> Graph:
             src = nat.to_dev(src, T.int64)
         src = src.contiguous()
     else:
-        arr = np.asarray(edges)
-        if arr.dtype == np.int32:
-            src = nat.to_dev(arr.reshape(-1, 2), T.int32)
-        else:
-            src = nat.to_dev(np.asarray(arr, dtype=np.int64).reshape(-1, 2), T.int64)
+        src = upload_edges(edges)
     m_in = int(src.shape[0])
     out = T.empty((max(m_in, 1), 2), dtype=T.int32, device=nat.device())
     scal = T.zeros(2, dtype=T.int64, device=nat.device())

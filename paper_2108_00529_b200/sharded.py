@@ -36,7 +36,7 @@ import warnings
 import numpy as np
 
 from . import _native as nat
-from .graph import Graph
+from .graph import Graph, upload_edges
 from .layout import (_ATTRACTION_FORMS, _SPEED_FORMS, LayoutParams, LayoutResult,
                      _device_model, _init_positions_dev, init_positions)
 from ._native import LayoutError
@@ -198,10 +198,7 @@ def from_edge_array_sharded(edges_local, comm: Comm | None = None,
             src = nat.to_dev(src, T.int64)
         src = src.contiguous()
     else:
-        arr = np.asarray(edges_local)
-        dt = T.int32 if arr.dtype == np.int32 else T.int64
-        src = nat.to_dev(np.asarray(arr, dtype=np.int32 if dt == T.int32 else np.int64)
-                         .reshape(-1, 2), dt)
+        src = upload_edges(edges_local)
     m_in = int(src.shape[0])
     dev = nat.device()
     out = T.empty((max(m_in, 1), 2), dtype=T.int32, device=dev)

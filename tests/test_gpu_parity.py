@@ -71,6 +71,29 @@ def test_parse_and_degree_kats(cv):
         cv.from_edge_array(np.array([[0, -1]]))
 
 
+def test_host_upload_staging(cv):
+    """cvz_edges_upload (the drop-in host input path): int64 and int32
+    pageable arrays across several staging chunks (4M edges each) arrive
+    bit-identical; ids outside [0, 2^31) raise ValueError like the compaction
+    check."""
+    from paper_2108_00529_b200.graph import upload_edges
+    rng = np.random.default_rng(3)
+    m = 9_500_001  # three staging chunks, ragged tail
+    e = rng.integers(0, 2**31 - 1, size=(m, 2), dtype=np.int64)
+    e[-1] = [2**31 - 1, 0]
+    for arr in (e, e.astype(np.int32)):
+        d = upload_edges(arr).cpu().numpy()
+        assert d.dtype == np.int32 and np.array_equal(d, e.astype(np.int32))
+    g = cv.from_edge_array(e[:1000] % 5000)
+    assert np.array_equal(g.edges, (e[:1000] % 5000)[(e[:1000] % 5000)[:, 0] != (e[:1000] % 5000)[:, 1]])
+    for bad in ([[0, -1]], [[0, 2**31]], [[2**40, 1]]):
+        with pytest.raises(ValueError):
+            cv.from_edge_array(np.array(bad, dtype=np.int64))
+    with pytest.raises(ValueError):
+        cv.from_edge_array(np.array([[3, -2]], dtype=np.int32))
+    assert cv.from_edge_array(np.zeros((0, 2), np.int64)).edge_count == 0
+
+
 def test_degrees_at_scale(cv, orc):
     from paper_2108_00529_b200 import synth
     e = synth.rmat_edges(18, 16, seed=3)
