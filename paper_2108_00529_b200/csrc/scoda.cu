@@ -673,6 +673,218 @@ __global__ void det_finalize_kernel(long long n, const int *__restrict__ seg_sta
     }
 }
 
+// ---- top-T formulation (T <= TOPT_MAX) -------------------------------------
+// A node's active slots are its first b = T - d0 occurrences in stream order
+// (a later post-increment counter exceeds T), so instead of sorting all 2m
+// slots by node, every node keeps the b smallest slot ids in a sorted list
+// of S = round_up(T, 4) <= TOPT_MAX entries.  Insertion is a lock-free atomicMin cascade: position
+// i keeps the running minimum of everything that reached it and passes the
+// larger value on, so position i ends as the (i+1)-th smallest slot
+// whatever the interleaving.  Entries only decrease, so a slot larger than
+// the current b-th entry can be rejected by a plain read, and the cascade may
+// start at the first entry larger than the slot (earlier positions would
+// pass it on unchanged).  Slots rejected or pushed past position b-1 set the
+// node's overflow flag (counter T + 1).  With a roughly in-order stream most
+// slots cost one sector read; the inserted ones one atomic.
+constexpr int TOPT_MAX = 16;
+constexpr unsigned TOPT_INF = 0xffffffffu;
+
+// thr[x] >= the current b-th entry of x's list (an upper bound that only
+// decreases): a slot above it is not among x's b smallest -- one read of a
+// 4-byte-per-node array rejects most slots without touching the list.  ovf
+// is written only if it is not set yet (a node's later occurrences would
+// otherwise store to the same byte again and again).
+//
+// Continue the cascade of v from position i (old = the value it displaced
+// there, already known not to be TOPT_INF).
+__device__ __noinline__ void topt_cascade(unsigned *__restrict__ A, int i, int b, unsigned v,
+                                          unsigned old, unsigned *__restrict__ thr,
+                                          unsigned char *__restrict__ ovf, int x) {
+    v = max(old, v);
+    for (++i; i < b; ++i) {
+        old = atomicMin(A + i, v);
+        if (i == b - 1) atomicMin(thr + x, min(old, v));
+        if (old == TOPT_INF) return;
+        v = max(old, v);
+    }
+    if (!__ldcg(ovf + x)) ovf[x] = 1;  // the largest of b + 1 values falls off the end
+}
+
+// one thread per pair of edges (one 128-bit load), this launch's nodes in
+// [xlo, xhi); slot 2k = u, 2k+1 = v, the second slot of a self-loop is not a
+// slot (bumped once, C/community.py:104-109); nodes whose seed exceeds T
+// have no active slot.  Per iteration the four slots' dependent chains are
+// issued phase by phase (threshold + overflow reads, list reads, first
+// atomics) so their L2 round trips overlap, and the next pair is prefetched.
+template <int S>  // list stride: 4, 8, 12 or 16 entries
+__global__ void __launch_bounds__(TB, 8) topt_kernel(const int4 *__restrict__ E2, const int2 *__restrict__ E, long long m,
+                            const long long *__restrict__ d0, long long T,
+                            unsigned *__restrict__ list, unsigned *__restrict__ thr,
+                            unsigned char *__restrict__ ovf, int xlo, int xhi) {
+    const long long pairs = (m + 1) / 2;
+    const long long W = (long long)gridDim.x * blockDim.x;
+    auto load = [&](long long i, int (&x)[4]) {
+        if (i >= pairs) {
+            x[0] = x[1] = x[2] = x[3] = -1;
+            return;
+        }
+        if (2 * i + 1 < m && E2) {
+            const int4 p = __ldcs(E2 + i);
+            x[0] = p.x;
+            x[1] = p.x == p.y ? -1 : p.y;
+            x[2] = p.z;
+            x[3] = p.z == p.w ? -1 : p.w;
+        } else {
+            const int2 p = __ldcs(E + 2 * i);
+            x[0] = p.x;
+            x[1] = p.x == p.y ? -1 : p.y;
+            if (2 * i + 1 < m) {
+                const int2 q = __ldcs(E + 2 * i + 1);
+                x[2] = q.x;
+                x[3] = q.x == q.y ? -1 : q.y;
+            } else {
+                x[2] = x[3] = -1;
+            }
+        }
+    };
+    int nx[4];
+    load((long long)blockIdx.x * blockDim.x + threadIdx.x, nx);
+    // warp-uniform trip count + __syncwarp per iteration: the inserts'
+    // data-dependent branches would otherwise let the lanes of a warp drift
+    // into different iterations (independent thread scheduling does not
+    // reconverge them inside the loop: ncu showed 2.7 active lanes per
+    // instruction)
+    for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < pairs; i0 += W) {
+        __syncwarp();
+        const long long i = i0 + threadIdx.x;
+        int x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = (nx[j] >= xlo && nx[j] < xhi) ? nx[j] : -1;
+        load(i + W, nx);
+        int b[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            b[j] = x[j] < 0 ? -1 : (int)(T - (d0 ? __ldg(d0 + x[j]) : 0LL));
+        unsigned t[4];
+        unsigned char o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            t[j] = b[j] > 0 ? __ldcg(thr + x[j]) : 0u;
+            o[j] = b[j] >= 0 ? __ldcg(ovf + x[j]) : (unsigned char)1;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const unsigned v = (unsigned)(4 * i + j);
+            const bool ins = b[j] > 0 && t[j] >= v;
+            // b == 0 (seed T): every occurrence overflows; b < 0: seed > T,
+            // counter unchanged; a slot above the threshold overflows
+            if (b[j] >= 0 && !ins && !o[j]) ovf[x[j]] = 1;
+            if (!ins) continue;
+            unsigned *A = list + (size_t)x[j] * S;
+            // the cascade may start at the first entry above v (earlier
+            // entries are smaller and only decrease)
+            int st = 0;
+#pragma unroll
+            for (int q = 0; q < S / 4; ++q) {
+                const uint4 g = __ldcg(reinterpret_cast<const uint4 *>(A) + q);
+                st += (g.x < v) + (g.y < v) + (g.z < v) + (g.w < v);
+            }
+            st = min(st, b[j] - 1);
+            const unsigned old = atomicMin(A + st, v);
+            if (st == b[j] - 1) atomicMin(thr + x[j], min(old, v));
+            if (old != TOPT_INF) topt_cascade(A, st, b[j], v, old, thr, ovf, x[j]);
+        }
+    }
+}
+
+// per node: counters of its active slots (d0 + rank), everything else keeps
+// the T + 1 prefill; then the parents / final write of the node as in
+// node_parents_kernel, from the list instead of the sorted segment
+template <class CT>
+__global__ void topt_counters_kernel(long long n, int S, const unsigned *__restrict__ list,
+                                     const long long *__restrict__ d0, long long T,
+                                     CT *__restrict__ cval) {
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long d = d0 ? d0[x] : 0;
+        if (d >= T) continue;
+        const uint4 *A = reinterpret_cast<const uint4 *>(list + (size_t)x * S);
+        const int b = (int)(T - d);
+        for (int q = 0; q < (b + 3) / 4; ++q) {
+            const uint4 v = A[q];
+            const unsigned e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int r = 4 * q + j;
+                if (r < b && e[j] != TOPT_INF) cval[e[j]] = (CT)(d + r + 1);
+            }
+            if (v.w == TOPT_INF) break;
+        }
+    }
+}
+
+__global__ void topt_parents_kernel(long long n, int S, const unsigned *__restrict__ list,
+                                    const long long *__restrict__ d0, long long T,
+                                    const signed char *__restrict__ role,
+                                    int *__restrict__ parent, int *__restrict__ finalw) {
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long d = d0 ? d0[x] : 0;
+        int last = -1;
+        if (d < T) {
+            const uint4 *A = reinterpret_cast<const uint4 *>(list + (size_t)x * S);
+            const int b = (int)(T - d);
+            for (int q = 0; q < (b + 3) / 4; ++q) {
+                const uint4 v = A[q];
+                const unsigned e[4] = {v.x, v.y, v.z, v.w};
+                signed char ro[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    ro[j] = (4 * q + j < b && e[j] != TOPT_INF) ? role[e[j] >> 1] : (signed char)-2;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (ro[j] == -2) continue;
+                    const signed char side = (signed char)(e[j] & 1);
+                    if (ro[j] >= 0 && ro[j] != side) parent[e[j] >> 1] = last;  // event reads x
+                    if (ro[j] == side) last = (int)(e[j] >> 1);                 // event writes x
+                }
+                if (v.w == TOPT_INF) break;
+            }
+        }
+        finalw[x] = last;
+    }
+}
+
+// final counter / label per node: deg = d0 if d0 > T, T + 1 on overflow,
+// else d0 + (active slots); label = initial label of the last write's origin
+__global__ void topt_finalize_kernel(long long n, int S, const unsigned *__restrict__ list,
+                                     const unsigned char *__restrict__ ovf,
+                                     const int *__restrict__ finalw, const int *__restrict__ origin,
+                                     const long long *__restrict__ d0,
+                                     const long long *__restrict__ lab0, long long T,
+                                     long long *__restrict__ deg_out,
+                                     long long *__restrict__ lab_out) {
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long d = d0 ? d0[x] : 0;
+        long long deg = d;
+        if (d <= T) {
+            if (ovf[x]) {
+                deg = T + 1;
+            } else {
+                const unsigned *A = list + (size_t)x * S;
+                int c = 0;
+                while (c < T - d && A[c] != TOPT_INF) ++c;
+                deg = d + c;
+            }
+        }
+        deg_out[x] = deg;
+        const int fw = finalw[x];
+        const long long src = fw >= 0 ? (long long)origin[fw] : x;
+        lab_out[x] = lab0 ? lab0[src] : src;
+    }
+}
+
 // ---- fast (racy) pass ------------------------------------------------------
 
 // FU edges per thread in flight (grid-stride over the stream, W threads
@@ -756,6 +968,117 @@ __global__ void __launch_bounds__(TB) fast_pass_kernel(const int2 *__restrict__ 
     }
 }
 
+// North-star form of the racy pass: two edges per 128-bit load and
+// warp-aggregated counter atomics -- lanes bumping the same node are
+// grouped with __match_any_sync, the lowest one adds the group size, and
+// each member takes old + (its rank in the group) + 1, i.e. the group's
+// increments in lane order (one valid interleaving of the racy pass).  The
+// four endpoint positions of a thread are aggregated one after the other.
+// Warp-uniform trip counts (match_any needs every lane).
+__global__ void __launch_bounds__(TB) fast_pass4_kernel(const int4 *__restrict__ E2,
+                                                        const int2 *__restrict__ E, long long m,
+                                                        const long long *__restrict__ d0,
+                                                        long long T, int tie,
+                                                        unsigned *__restrict__ cnt,
+                                                        long long *lab) {
+    const long long W = (long long)gridDim.x * blockDim.x;
+    const long long pairs = (m + 1) / 2;
+    const int lane = lane_id();
+    const unsigned lt = (1u << lane) - 1;
+    auto load = [&](long long j, int (&x)[4]) {
+        if (j >= pairs) {
+            x[0] = x[1] = x[2] = x[3] = -1;
+        } else if (E2 && 2 * j + 1 < m) {
+            const int4 p = __ldcs(E2 + j);
+            x[0] = p.x;
+            x[1] = p.y;
+            x[2] = p.z;
+            x[3] = p.w;
+        } else {
+            const int2 a = __ldcs(E + 2 * j);
+            x[0] = a.x;
+            x[1] = a.y;
+            if (2 * j + 1 < m) {
+                const int2 b = __ldcs(E + 2 * j + 1);
+                x[2] = b.x;
+                x[3] = b.y;
+            } else {
+                x[2] = x[3] = -1;
+            }
+        }
+    };
+    int nx[4];
+    load((long long)blockIdx.x * blockDim.x + threadIdx.x, nx);
+    for (long long jb = (long long)blockIdx.x * blockDim.x; jb < pairs; jb += W) {
+        int x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = nx[q];
+        load(jb + W + threadIdx.x, nx);
+        long long d[4];
+        bool need[4], live[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            // the second slot of a self-loop is not bumped (C/community.py:104-109)
+            live[q] = x[q] >= 0 && !((q & 1) && x[q] == x[q - 1]);
+            d[q] = (d0 && live[q]) ? __ldg(d0 + x[q]) : 0;
+        }
+        unsigned c[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            need[q] = live[q] && d[q] <= T;
+            c[q] = need[q] ? __ldcg(cnt + x[q]) : 0u;
+        }
+        long long dd[4];  // post-increment counter of each slot
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool a = need[q] && (long long)c[q] < T + 1 - d[q];
+            unsigned o = 0;
+            if (__ballot_sync(0xffffffffu, a)) {  // no bumping lane: no match / atomic
+                const unsigned key = a ? (unsigned)x[q] : (0x80000000u | (unsigned)lane);
+                const unsigned peers = __match_any_sync(0xffffffffu, key);
+                const int leader = __ffs(peers) - 1;
+                unsigned old = 0;
+                if (a && lane == leader) old = atomicAdd(cnt + x[q], (unsigned)__popc(peers));
+                old = __shfl_sync(0xffffffffu, old, leader);
+                o = old + __popc(peers & lt);
+            }
+            dd[q] = !need[q] ? d[q] : (a ? min(d[q] + (long long)o + 1, T + 1) : T + 1);
+        }
+        int tgt[2], src[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            tgt[u] = -1;
+            const int a = x[2 * u], b = x[2 * u + 1];
+            if (a < 0 || a == b) continue;
+            const long long du = dd[2 * u], dv = dd[2 * u + 1];
+            if (du > T || dv > T) continue;  // C/community.py:110-111
+            if (du < dv || (du == dv && tie == 0)) {  // :112-113, :116-117
+                tgt[u] = a;
+                src[u] = b;
+            } else if (dv < du || (du == dv && tie == 1)) {  // :114-115, :118-119
+                tgt[u] = b;
+                src[u] = a;
+            }
+        }
+        long long val[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            if (tgt[u] >= 0) val[u] = __ldcg(lab + src[u]);
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            if (tgt[u] >= 0) __stcg(lab + tgt[u], val[u]);
+    }
+}
+
+__global__ void any_negative_kernel(const long long *__restrict__ v, long long n,
+                                    int *__restrict__ flag) {
+    bool neg = false;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        neg |= v[i] < 0;
+    if (__any_sync(0xffffffffu, neg) && lane_id() == 0) atomicExch(flag, 1);
+}
+
 __global__ void fast_finalize_kernel(long long n, const unsigned *__restrict__ cnt,
                                      const long long *__restrict__ d0, long long T,
                                      long long *__restrict__ deg_out) {
@@ -837,17 +1160,19 @@ __global__ void compose_kernel(long long n, const long long *__restrict__ rep,
 constexpr int RITEMS = 8;
 constexpr int RTILE = TB * RITEMS;
 
-constexpr long long SAT_BIT = 1LL << 62;
-constexpr long long SAT_MASK = SAT_BIT - 1;
+// int32 relabel map (4-byte gathers; ids < 2^31): bit 31 = saturation flag
+constexpr unsigned SAT_BIT = 0x80000000u;
+constexpr unsigned SAT_MASK = SAT_BIT - 1;
 
 // map[x] = rep[x] | SAT_BIT if rep[x]'s community has >= Tn + 2 members
+// (size == nullptr: no flag)
 __global__ void pack_map_kernel(const long long *__restrict__ rep, long long n,
                                 const unsigned *__restrict__ size, long long Tn,
-                                long long *__restrict__ out) {
+                                unsigned *__restrict__ out) {
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
          x += (long long)gridDim.x * blockDim.x) {
-        long long r = rep[x];
-        out[x] = (long long)size[r] >= Tn + 2 ? (r | SAT_BIT) : r;
+        const unsigned r = (unsigned)rep[x];
+        out[x] = (size && (long long)size[r] >= Tn + 2) ? (r | SAT_BIT) : r;
     }
 }
 
@@ -858,44 +1183,38 @@ __global__ void pack_map_kernel(const long long *__restrict__ rep, long long n,
 // stay equal to themselves, and sizes only grow.  Such edges are counted
 // (*d_dead) instead of written.  size == nullptr disables the drop.
 __global__ void __launch_bounds__(TB) relabel_compact_kernel(
-    const int2 *__restrict__ in, long long m, const long long *__restrict__ map,
+    const int2 *__restrict__ in, long long m, const unsigned *__restrict__ map,
     int2 *__restrict__ out, LookbackState st, unsigned long long *__restrict__ d_count,
-    unsigned num_tiles, const unsigned *__restrict__ size, long long Tn,
-    unsigned long long *__restrict__ d_dead) {
+    unsigned num_tiles, bool drop, unsigned long long *__restrict__ d_dead) {
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_prefix;
     const unsigned tile = acquire_tile(st, &s_tile);
     const long long base = (long long)tile * RTILE;
-    int2 e[RITEMS];
+    int2 p[RITEMS];
     bool keep[RITEMS];
     unsigned dead = 0;
 #pragma unroll
     for (int j = 0; j < RITEMS; ++j) {
         long long i = base + (long long)j * TB + threadIdx.x;
+        p[j] = i < m ? __ldcs(in + i) : make_int2(-1, -1);
+    }
+    int2 e[RITEMS];
+#pragma unroll
+    for (int j = 0; j < RITEMS; ++j) {
         keep[j] = false;
-        if (i < m) {
-            int2 p = __ldg(in + i);
-            int a = 0, b = 0;
-            if (!size) {
-                a = (int)__ldg(map + p.x);
-                b = (int)__ldg(map + p.y);
-                e[j] = make_int2(a, b);
-                keep[j] = a != b;
-            }
-            if (size) {  // map carries the saturation flag in bit 62 (pack_map_kernel)
-                const long long ma = __ldg(map + p.x), mb = __ldg(map + p.y);
-                a = (int)(ma & SAT_MASK);
-                b = (int)(mb & SAT_MASK);
-                e[j] = make_int2(a, b);
-                keep[j] = a != b;
-                if (keep[j] && (ma & mb & SAT_BIT)) {
-                    keep[j] = false;
-                    ++dead;
-                }
+        if (p[j].x >= 0) {
+            // map carries the saturation flag in bit 31 (pack_map_kernel)
+            const unsigned ma = __ldg(map + p[j].x), mb = __ldg(map + p[j].y);
+            const int a = (int)(ma & SAT_MASK), b = (int)(mb & SAT_MASK);
+            e[j] = make_int2(a, b);
+            keep[j] = a != b;
+            if (drop && keep[j] && (ma & mb & SAT_BIT)) {
+                keep[j] = false;
+                ++dead;
             }
         }
     }
-    if (size) {
+    if (drop) {
         for (int o = 16; o > 0; o >>= 1) dead += __shfl_xor_sync(0xffffffffu, dead, o);
         if (lane_id() == 0 && dead) atomicAdd(d_dead, (unsigned long long)dead);
     }
@@ -1087,12 +1406,97 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
                reinterpret_cast<long long *>(deg_out), reinterpret_cast<long long *>(lab_out));
 }
 
+// Exactly the resident grid: iteration k of every thread covers one
+// contiguous window of the stream, so slots arrive nearly in stream order and
+// most inserts append (one atomic).  An oversubscribed grid-stride launch
+// spreads the first wave over the whole stream, and random arrival order
+// turns inserts into dependent atomic cascades.
+template <int S>
+static void launch_topt(const int4 *E2, const int2 *E, long long m, long long pairs,
+                        const long long *d0, long long T, unsigned *list, unsigned *thr,
+                        unsigned char *ovf, int lo, int hi, cudaStream_t s) {
+    static DeviceCache occ;
+    const int per_sm = occ.get([] {
+        int b = 0;
+        CVZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, topt_kernel<S>, TB, 0));
+        return b < 1 ? 1 : b;
+    });
+    const unsigned grid = (unsigned)std::max<long long>(
+        1, std::min<long long>((long long)per_sm * num_sms(), (pairs + TB - 1) / TB));
+    CVZ_LAUNCH(topt_kernel<S>, grid, TB, 0, s, E2, E, m, d0, T, list, thr, ovf, lo, hi);
+}
+
+// Deterministic pass, top-T formulation (T <= TOPT_MAX, see topt_insert):
+// no slot sort; lists of the b smallest slot ids per node replace the
+// sorted segments.  Same events, parents and results as det_pass_t.
+static void det_pass_topt(const int2 *E, long long m, long long n, long long T, int tie,
+                          const int64_t *d0, const int64_t *lab0, int64_t *deg_out,
+                          int64_t *lab_out, Scratch &sc, cudaStream_t s) {
+    auto *d0p = reinterpret_cast<const long long *>(d0);
+    const int S = (int)std::max(4LL, (T + 3) & ~3LL);  // list stride: whole 16-byte groups
+    unsigned *list = sc.alloc<unsigned>((size_t)n * S);
+    unsigned char *ovf = sc.alloc<unsigned char>(n);
+    int *finalw = sc.alloc<int>(n);
+    int *origin = sc.alloc<int>(m > 0 ? m : 1);
+    unsigned *thr = sc.alloc<unsigned>(n);
+    CVZ_CUDA(cudaMemsetAsync(list, 0xff, sizeof(unsigned) * (size_t)n * S, s));
+    CVZ_CUDA(cudaMemsetAsync(thr, 0xff, sizeof(unsigned) * n, s));
+    CVZ_CUDA(cudaMemsetAsync(ovf, 0, n, s));
+    if (m > 0) {
+        const bool al = (reinterpret_cast<uintptr_t>(E) & 15) == 0;
+        // (one pass over the stream; splitting the nodes into L2-sized ranges
+        // with one pass each measured slower: the pass is latency-, not
+        // capacity-bound)
+        const long long pairs = (m + 1) / 2;
+        const int4 *E2 = al ? reinterpret_cast<const int4 *>(E) : nullptr;
+        const int hi = (int)n;
+        switch (S) {
+            case 4: launch_topt<4>(E2, E, m, pairs, d0p, T, list, thr, ovf, 0, hi, s); break;
+            case 8: launch_topt<8>(E2, E, m, pairs, d0p, T, list, thr, ovf, 0, hi, s); break;
+            case 12: launch_topt<12>(E2, E, m, pairs, d0p, T, list, thr, ovf, 0, hi, s); break;
+            default: launch_topt<16>(E2, E, m, pairs, d0p, T, list, thr, ovf, 0, hi, s); break;
+        }
+        unsigned char *cval = sc.alloc<unsigned char>(2 * m);
+        CVZ_CUDA(cudaMemsetAsync(cval, (int)(T + 1), 2 * m, s));
+        CVZ_LAUNCH(topt_counters_kernel<unsigned char>, grid_for(n, TB, 1, 8), TB, 0, s, n, S,
+                   list, d0p, T, cval);
+        auto *role = sc.alloc<signed char>(m);
+        CVZ_LAUNCH(edge_role_kernel<unsigned char>, grid_for(m, TB, 1, 16), TB, 0, s, E, m, cval,
+                   T, tie, role);
+        int *parent = sc.alloc<int>(m);
+        CVZ_LAUNCH(topt_parents_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n, S, list, d0p, T, role,
+                   parent, finalw);
+        int *ptr = sc.alloc<int>(m);
+        int *wa = sc.alloc<int>(m), *wb = sc.alloc<int>(m);
+        const int R = bits_for_value((unsigned long long)m) + 2;
+        unsigned *cnt = sc.alloc<unsigned>(R + 1);
+        CVZ_CUDA(cudaMemsetAsync(cnt, 0, (R + 1) * sizeof(unsigned), s));
+        CVZ_LAUNCH(events_init_kernel, grid_for(m, TB, 1, 16), TB, 0, s, E, m, role, parent,
+                   origin, ptr, wa, cnt);
+        CVZ_COOP(events_coop_kernel, CB, s, wa, wb, cnt, R, origin, ptr);
+    } else {
+        CVZ_CUDA(cudaMemsetAsync(finalw, 0xff, sizeof(int) * n, s));
+    }
+    CVZ_LAUNCH(topt_finalize_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n, S, list, ovf, finalw, origin,
+               d0p, reinterpret_cast<const long long *>(lab0), T,
+               reinterpret_cast<long long *>(deg_out), reinterpret_cast<long long *>(lab_out));
+}
+
+// seeds_nonneg: every d0 >= 0 (the top-T lists hold at most TOPT_MAX = b
+// entries only then; detect's size seeds always are)
 void scoda_pass_dev(const int2 *E, long long m, long long n, long long T, int tie, int mode,
                     const int64_t *d0, const int64_t *lab0, int64_t *deg_out, int64_t *lab_out,
-                    Scratch &sc, cudaStream_t s) {
+                    Scratch &sc, cudaStream_t s, bool seeds_nonneg) {
     CVZ_REQUIRE(2 * m < (1LL << 31) - 1, CVZ_ERR_VALUE,
                 "edge stream too long for one pass (2m must be < 2^31)");
     if (mode == CVZ_SCODA_DETERMINISTIC) {
+        // top-T lists for the usual small thresholds (CVZ_DET_SORT=1: the
+        // slot-sort formulation for every T)
+        static const bool force_sort = getenv("CVZ_DET_SORT") != nullptr;
+        if (T >= 0 && T <= TOPT_MAX && !force_sort && (seeds_nonneg || !d0)) {
+            det_pass_topt(E, m, n, T, tie, d0, lab0, deg_out, lab_out, sc, s);
+            return;
+        }
         if (T < 255)
             det_pass_t<unsigned char>(E, m, n, T, tie, d0, lab0, deg_out, lab_out, sc, s);
         else if (T < (1LL << 30))
@@ -1115,9 +1519,22 @@ void scoda_pass_dev(const int2 *E, long long m, long long n, long long T, int ti
                                           : FAST_WINDOW_DIV;
         long long window = std::max(256LL, std::min(m / wdiv, 2048LL * num_sms() * FU));
         unsigned blocks = (unsigned)((window / FU + TB - 1) / TB);
-        CVZ_LAUNCH(fast_pass_kernel, blocks, TB, 0, s, E, m,
-                   reinterpret_cast<const long long *>(d0), T, tie, cnt,
-                   reinterpret_cast<long long *>(lab_out));
+        // default: per-edge int2 loads and plain atomics (fast_pass_kernel);
+        // CVZ_FAST_AGG=1: 128-bit loads + warp-aggregated atomics
+        // (fast_pass4_kernel, measured slower at C4: 0.82 vs 0.70 ms --
+        // in-warp duplicate nodes are rare in a shuffled stream, so the
+        // match costs more than the atomics it saves)
+        static const bool plain = getenv("CVZ_FAST_AGG") == nullptr;
+        const bool al = (reinterpret_cast<uintptr_t>(E) & 15) == 0;
+        if (plain)
+            CVZ_LAUNCH(fast_pass_kernel, blocks, TB, 0, s, E, m,
+                       reinterpret_cast<const long long *>(d0), T, tie, cnt,
+                       reinterpret_cast<long long *>(lab_out));
+        else
+            CVZ_LAUNCH(fast_pass4_kernel, blocks, TB, 0, s,
+                       al ? reinterpret_cast<const int4 *>(E) : nullptr, E, m,
+                       reinterpret_cast<const long long *>(d0), T, tie, cnt,
+                       reinterpret_cast<long long *>(lab_out));
     }
     CVZ_LAUNCH(fast_finalize_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n, cnt,
                reinterpret_cast<const long long *>(d0), T, reinterpret_cast<long long *>(deg_out));
@@ -1184,7 +1601,16 @@ int cvz_scoda_pass(const int32_t *edges, int64_t m, const int64_t *order, int64_
         CVZ_CUDA(cudaMemcpyAsync(d0, deg, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, s));
         CVZ_CUDA(cudaMemcpyAsync(l0, lab, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, s));
         int64_t *raw = lab_raw ? lab_raw : sc.alloc<int64_t>(n);
-        scoda_pass_dev(E, m, n, threshold, tie_code, mode, d0, l0, deg, raw, sc, s);
+        // caller-supplied counters may be negative: the top-T path only
+        // when they are not (one reduction + a sync on this test seam)
+        int *neg = sc.alloc<int>(1);
+        CVZ_CUDA(cudaMemsetAsync(neg, 0, sizeof(int), s));
+        CVZ_LAUNCH(any_negative_kernel, grid_for(n, TB, 1, 4), TB, 0, s,
+                   reinterpret_cast<const long long *>(d0), (long long)n, neg);
+        int hneg = 0;
+        CVZ_CUDA(cudaMemcpyAsync(&hneg, neg, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CVZ_CUDA(cudaStreamSynchronize(s));
+        scoda_pass_dev(E, m, n, threshold, tie_code, mode, d0, l0, deg, raw, sc, s, hneg == 0);
         resolve_dev(raw, n, lab, true, sc, s);
     });
 }
@@ -1231,7 +1657,7 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
         }
         // 3. pass + resolve (labels restart at arange(n), :262-265)
         int64_t *raw = sc.alloc<int64_t>(n), *rep = sc.alloc<int64_t>(n);
-        scoda_pass_dev(E, m_cur, n, T, tie_code, mode, d0, nullptr, deg_out, raw, sc, s);
+        scoda_pass_dev(E, m_cur, n, T, tie_code, mode, d0, nullptr, deg_out, raw, sc, s, true);
         resolve_dev(raw, n, rep, false, sc, s);
         // 4. compose + history + early-stop test (:266-269)
         int *dchg = sc.alloc<int>(1);
@@ -1252,7 +1678,7 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
         // 5. next stream: contract (:272-278) or restream (:274-276)
         const int2 *src = round_stream == 0 ? cur : reinterpret_cast<const int2 *>(orig_edges);
         long long msrc = round_stream == 0 ? m_cur : m_orig;
-        const long long *map = reinterpret_cast<const long long *>(round_stream == 0 ? rep : node_lab);
+        const int64_t *map64 = round_stream == 0 ? rep : node_lab;
         unsigned tiles = (unsigned)((msrc + RTILE - 1) / RTILE);
         if (tiles == 0) tiles = 1;
         auto *status = sc.alloc<unsigned long long>(tiles);
@@ -1270,15 +1696,13 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
             CVZ_LAUNCH(size_hist_kernel, grid_for(n, TB, 1, 8), TB, 0, s,
                        reinterpret_cast<const long long *>(node_lab), (long long)n, nsize);
         }
-        if (nsize) {
-            long long *packed = sc.alloc<long long>(n);
-            CVZ_LAUNCH(pack_map_kernel, grid_for(n, TB, 1, 8), TB, 0, s, map, (long long)n, nsize,
-                       (long long)next_threshold, packed);
-            map = packed;
-        }
+        unsigned *map = sc.alloc<unsigned>(n);
+        CVZ_LAUNCH(pack_map_kernel, grid_for(n, TB, 1, 8), TB, 0, s,
+                   reinterpret_cast<const long long *>(map64), (long long)n, nsize,
+                   (long long)next_threshold, map);
         CVZ_LAUNCH(relabel_compact_kernel, tiles, TB, 0, s, src, msrc, map,
                    reinterpret_cast<int2 *>(next_edges), LookbackState{status, ctr}, dcount, tiles,
-                   nsize, (long long)next_threshold, dcount + 1);
+                   nsize != nullptr, dcount + 1);
         unsigned long long hm[2] = {0, 0};
         CVZ_CUDA(cudaMemcpyAsync(hm, dcount, sizeof(hm), cudaMemcpyDeviceToHost, s));
         CVZ_CUDA(cudaStreamSynchronize(s));

@@ -419,6 +419,40 @@ def test_contract_at_scale(cv, orc):
     assert np.all(sg.edges[:, 0] < sg.edges[:, 1])
 
 
+def test_contract_segment_tiers_vs_oracle(cv, orc):
+    """Superedge aggregation with skewed per-community crossing counts (one
+    community with 70K crossing edges, others with 9K / 600 / a few) and
+    heavy duplicate pairs in both orientations, vs np.unique(axis=0)."""
+    rng = np.random.default_rng(7)
+    n = 200_000
+    lab = (np.arange(n) // 4).astype(np.int64)  # 50,000 communities of 4 nodes
+    parts = []
+    # hub community 0 (the smallest id, so always `lo`): 70K crossing edges
+    # to 3,000 communities (global-scratch tier), community 4 -> 9,000 edges
+    # (shared tier), community 8 -> 600 (warp tier), the rest sparse
+    for hub, cnt, spread in ((0, 70_000, 3_000), (4, 9_000, 20_000), (8, 600, 40)):
+        u = rng.integers(hub * 4, hub * 4 + 4, cnt)
+        v = rng.integers(40, 40 + spread, cnt) * 4 + rng.integers(0, 4, cnt)
+        parts.append(np.stack([u, v], 1))
+    parts.append(rng.integers(0, n, (300_000, 2)))
+    e = np.concatenate(parts)
+    e = e[rng.permutation(len(e))]
+    e = e[e[:, 0] != e[:, 1]]
+    e[::2] = e[::2, ::-1]  # both orientations
+    g = cv.from_edge_array(e, node_count=n)
+    n_, ee, deg = orc.from_edge_array(e, node_count=n)
+    s = cv.sketch_new(3, 5000, seed=1)
+    cv.accumulate_sizes(s, lab, g.degree)
+    sg = cv.contract(g, lab, s)
+    A, B = orc.sketch_params(3, 1)
+    t = np.zeros((3, 5000), np.int64)
+    orc.sketch_add_many(t, A, B, lab, deg)
+    k, se, w, mult, comm = orc.contract(ee, lab, t, A, B)
+    assert sg.node_count == k
+    assert np.array_equal(sg.edges, se) and np.array_equal(sg.multiplicity, mult)
+    assert np.array_equal(sg.weight, w) and np.array_equal(sg.community_id, comm)
+
+
 # ----------------------------------------------------------------- layout
 def test_repulsion_golden(cv):
     """BH / exact repulsion vs the reference (C/layout.py:215-290) on the
