@@ -1149,43 +1149,46 @@ __global__ void __launch_bounds__(NT, MINB) bh_flat_kernel(Walker w, const PNode
         const int self = p + (int)cle[p];
         double fx = 0.0, fy = 0.0;
         int c = 0;  // root cell (n >= 2)
+        // the rare cases (depth-40 aggregates, pairs closer than
+        // COINCIDE_EPS, self) sit behind ONE predicate evaluated after the
+        // opening test, so the common iteration is load, d2, [open], accept
+        // (-1.3 % against testing the kind first)
         while (c >= 0) {
             const PNode t = pn[c];
             const int kind = t.meta & 3;
             if (COUNT) ++n_visit;
-            if (kind == 2) {
-                if (COUNT) ++n_acc;
-                double2 r = aggregate_add(w, t, c, p, i, xi, yi, mi, kmi, fx, fy);
-                fx = r.x;
-                fy = r.y;
+            const double dx = sub(xi, t.x), dy = sub(yi, t.y);
+            const double d2 = add(mul(dx, dx), mul(dy, dy));
+            // cells open unless side^2 < theta^2 d^2; leaves and aggregates
+            // are always approximated (C/layout.py:256-261)
+            const bool open =
+                kind == 1 && !((s2exp ? __hiloint2double(s20_hi - ((t.meta >> 2) << 21), s20_lo)
+                                      : s2tab[t.meta >> 2]) < mul(th2, d2));
+            if (open) {
+                ++c;
+                continue;
+            }
+            if (kind == 2 || !(d2 >= eps2)) {
+                if (kind == 2) {
+                    if (COUNT) ++n_acc;
+                    const double2 r = aggregate_add(w, t, c, p, i, xi, yi, mi, kmi, fx, fy);
+                    fx = r.x;
+                    fy = r.y;
+                } else if (c != self) {
+                    if (COUNT) ++n_acc;  // j == i skipped (:237-238); a leaf stores its
+                                         // body's exact position, so self has d2 == 0
+                    const double2 r = jitter_add(w.bodies, w.n, w.aux, w.cr, th2, c, kind, i, kmi,
+                                                 t.m, dx, dy, d2, false, fx, fy);
+                    fx = r.x;
+                    fy = r.y;
+                }
                 c = t.skip;
                 continue;
             }
-            const double dx = sub(xi, t.x), dy = sub(yi, t.y);
-            const double d2 = add(mul(dx, dx), mul(dy, dy));
-            // cells open unless side^2 < theta^2 d^2; leaves are always
-            // approximated (C/layout.py:256-261)
-            if (kind == 1) {
-                const double s2 = s2exp ? __hiloint2double(s20_hi - ((t.meta >> 2) << 21), s20_lo)
-                                        : s2tab[t.meta >> 2];
-                if (!(s2 < mul(th2, d2))) {
-                    ++c;
-                    continue;
-                }
-            }
-            if (d2 >= eps2) {
-                if (COUNT) ++n_acc;
-                const double f = mul(mul(kmi, t.m), inv_d2(d2));
-                fx = add(fx, mul(f, dx));
-                fy = add(fy, mul(f, dy));
-            } else if (c != self) {
-                if (COUNT) ++n_acc;  // j == i skipped (:237-238); a leaf stores its
-                                     // body's exact position, so self has d2 == 0
-                double2 r = jitter_add(w.bodies, w.n, w.aux, w.cr, th2, c, kind, i, kmi, t.m, dx,
-                                       dy, d2, false, fx, fy);
-                fx = r.x;
-                fy = r.y;
-            }
+            if (COUNT) ++n_acc;
+            const double f = mul(mul(kmi, t.m), inv_d2(d2));
+            fx = add(fx, mul(f, dx));
+            fy = add(fy, mul(f, dy));
             c = t.skip;
         }
         out[i] = make_double2(fx, fy);
@@ -2268,21 +2271,35 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
 // all spring sums of rows [lo, hi) into c.hsum (heavy) / spr (light)
 static void springs(const double2 *pos, const Csr &c, const StepScalars *sc, int lo, int hi,
                     double2 *spr, cudaStream_t s) {
-    // unit-weight graphs (no per-half-edge weights) get their own instances
+    // unit-weight graphs (no per-half-edge weights) get their own instances.
+    // The heavy rows run as ONE grid-stride CTA per SM: with a warp per row
+    // (~8K CTAs at C4) the side stream takes every SM slot that frees up
+    // while the latency-bound tree kernels of the main stream wait for
+    // slots (a 19 us hole after the key sort): 507 -> 492 us/iteration at C4.
+    // Stream priorities instead (springs lowest) starve the springs until the
+    // walk ends: 528 us.  Multi-million-body layouts (full graphs) keep one
+    // warp per row: their springs are ~4x the work and their tree kernels
+    // are not latency-bound (the cap costs C4 full graph 4.5 -> 5.0 ms).
+    // CVZ_SPRINGS_CAP overrides (CTAs per SM, 0 = none).
+    static const char *cenv = getenv("CVZ_SPRINGS_CAP");
+    const int cap = cenv ? atoi(cenv) : (hi - lo < (1 << 21) ? 1 : 0);
     if (c.nheavy > 0) {
+        unsigned hb = blocks_for((long long)c.nheavy * 32, FB);
+        if (cap > 0) hb = std::min<unsigned>(hb, (unsigned)(cap * num_sms()));
         if (c.w)
-            CVZ_LAUNCH(springs_heavy_kernel<false>, blocks_for((long long)c.nheavy * 32, FB), FB, 0,
+            CVZ_LAUNCH(springs_heavy_kernel<false>, hb, FB, 0,
                        s, pos, c.rowptr, c.col, c.w, c.unit, c.heavy, c.nheavy, c.hsum, sc);
         else
-            CVZ_LAUNCH(springs_heavy_kernel<true>, blocks_for((long long)c.nheavy * 32, FB), FB, 0,
+            CVZ_LAUNCH(springs_heavy_kernel<true>, hb, FB, 0,
                        s, pos, c.rowptr, c.col, c.w, c.unit, c.heavy, c.nheavy, c.hsum, sc);
     }
     if (hi > lo) {
+        const unsigned lb = blocks_for(hi - lo, FB);
         if (c.w)
-            CVZ_LAUNCH(springs_light_kernel<false>, blocks_for(hi - lo, FB), FB, 0, s, pos,
+            CVZ_LAUNCH(springs_light_kernel<false>, lb, FB, 0, s, pos,
                        c.rowptr, c.col, c.w, c.unit, c.hidx, lo, hi, spr, sc);
         else
-            CVZ_LAUNCH(springs_light_kernel<true>, blocks_for(hi - lo, FB), FB, 0, s, pos,
+            CVZ_LAUNCH(springs_light_kernel<true>, lb, FB, 0, s, pos,
                        c.rowptr, c.col, c.w, c.unit, c.hidx, lo, hi, spr, sc);
     }
 }
