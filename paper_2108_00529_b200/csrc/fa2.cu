@@ -1989,10 +1989,13 @@ struct Tree {
         const int tiles = (n + TILE_DD - 1) / TILE_DD;
         Keys K{khi3, klo3, n};
         if (aux) {
-            CVZ_LAUNCH_PDL(gather_keys_kernel, g, FB, 0, s, idx2, klo2, khi, n, khi3, klo3,
-                           top_digits);
+            // the body gather + prefix sums need only the sorted order: they
+            // start on the main stream as soon as the tie fix-up is done,
+            // while the side stream gathers the keys and runs karras
             CVZ_CUDA(cudaEventRecord(ev_a, s));
             CVZ_CUDA(cudaStreamWaitEvent(aux, ev_a, 0));
+            CVZ_LAUNCH(gather_keys_kernel, g, FB, 0, aux, idx2, klo2, khi, n, khi3, klo3,
+                       top_digits);
             CVZ_LAUNCH(karras_only_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, aux, K, left, first,
                        last, delta, parent_int, parent_leaf, pdelta, rc_by_split);
             CVZ_CUDA(cudaEventRecord(ev_b, aux));
@@ -2545,6 +2548,28 @@ int cvz_attraction(const double *pos, int64_t n, const int32_t *edges, int64_t m
     });
 }
 
+// Per-thread, per-device layout resources (never destroyed: process lifetime).
+struct LayoutRes {
+    cudaStream_t side = nullptr, aux = nullptr, cs = nullptr;
+    cudaEvent_t ev[6] = {};
+    cudaGraphExec_t exec = nullptr;
+};
+
+static LayoutRes &layout_res() {
+    constexpr int kMax = 64;
+    static thread_local LayoutRes res[kMax];
+    const int d = current_device();
+    CVZ_REQUIRE(d >= 0 && d < kMax, CVZ_ERR_VALUE, "device index out of range");
+    LayoutRes &r = res[d];
+    if (!r.side) {
+        CVZ_CUDA(cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking));
+        CVZ_CUDA(cudaStreamCreateWithFlags(&r.aux, cudaStreamNonBlocking));
+        CVZ_CUDA(cudaStreamCreateWithFlags(&r.cs, cudaStreamNonBlocking));
+        for (auto &e : r.ev) CVZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return r;
+}
+
 int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *edges, int64_t m,
                    const double *weight, const cvz_layout_params *P, double *prev_force,
                    double *speed, double *disp_hist, int64_t *bad_iteration, void *stream) {
@@ -2566,10 +2591,16 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
         CVZ_CUDA(cudaMemsetAsync(ctrs, 0, 2 * sizeof(unsigned), s));
         double *bbox = sc.alloc<double>(4);
         StepScalars *scal = sc.alloc<StepScalars>(1);
-        StepScalars init{};
-        CVZ_CUDA(cudaMemcpyAsync(&init.speed, speed, sizeof(double), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
-        CVZ_CUDA(cudaMemcpyAsync(scal, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+        // zeroed scalars + the caller's speed, stream-ordered (no host sync
+        // before the layout starts; speed0 keeps the value for a rerun)
+        double *speed0 = sc.alloc<double>(1);
+        CVZ_CUDA(cudaMemcpyAsync(speed0, speed, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        auto reset_scalars = [&] {
+            CVZ_CUDA(cudaMemsetAsync(scal, 0, sizeof(StepScalars), s));
+            CVZ_CUDA(cudaMemcpyAsync(&scal->speed, speed0, sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+        };
+        reset_scalars();
         const bool exact = P->theta <= 0;
         Tree tree;
         if (!exact) tree.alloc(N, sc);
@@ -2581,29 +2612,26 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
 
         double2 *spr = sc.alloc<double2>(n);
         // springs only need positions: they run on a side stream while the
-        // tree is built and walked (fork/join events, captured into the graph)
-        cudaStream_t side;
-        CVZ_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-        cudaEvent_t ev_fork, ev_join;
-        CVZ_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-        CVZ_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-        struct SideGuard {
-            cudaStream_t s;
-            cudaEvent_t a, b;
-            ~SideGuard() {
-                cudaStreamSynchronize(s);
-                cudaStreamDestroy(s);
-                cudaEventDestroy(a);
-                cudaEventDestroy(b);
+        // tree is built and walked (fork/join events, captured into the
+        // graph); karras of the tree build runs on a second side stream.
+        // Streams, events and the instantiated iteration graph persist per
+        // thread and device (creating + destroying three streams and
+        // instantiating the graph cost ~0.6 ms of host time per call).
+        LayoutRes &lr = layout_res();
+        cudaStream_t side = lr.side, aux = lr.aux;
+        cudaEvent_t ev_fork = lr.ev[0], ev_join = lr.ev[1], ev_ka = lr.ev[2], ev_kb = lr.ev[3];
+        // whatever happens (errors included), the side streams' work is
+        // ordered before the scratch arena's stream-ordered frees on s
+        struct JoinGuard {
+            cudaStream_t s, a, b;
+            cudaEvent_t e;
+            ~JoinGuard() {
+                for (cudaStream_t x : {a, b}) {
+                    cudaEventRecord(e, x);
+                    cudaStreamWaitEvent(s, e, 0);
+                }
             }
-        } side_guard{side, ev_fork, ev_join};
-        // karras of the tree build runs on a second side stream
-        cudaStream_t aux;
-        CVZ_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
-        cudaEvent_t ev_ka, ev_kb;
-        CVZ_CUDA(cudaEventCreateWithFlags(&ev_ka, cudaEventDisableTiming));
-        CVZ_CUDA(cudaEventCreateWithFlags(&ev_kb, cudaEventDisableTiming));
-        SideGuard aux_guard{aux, ev_ka, ev_kb};
+        } join_guard{s, side, aux, lr.ev[5]};
         static const bool split_build = getenv("CVZ_TREE_SPLIT") == nullptr ||
                                         std::string(getenv("CVZ_TREE_SPLIT")) != "0";
         auto one_iteration = [&](cudaStream_t st, bool ids) {
@@ -2636,15 +2664,14 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
             bool use_graph =
                 getenv("CVZ_NO_GRAPH") == nullptr && P->iterations > 1 && !prof_on();
             if (use_graph) {
-                // capture one iteration on a private stream, then replay
-                cudaStream_t cs;
-                CVZ_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-                cudaEvent_t ev;
-                CVZ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                // capture one iteration on a private stream, then replay; the
+                // previous call's executable graph is updated in place when
+                // the topology matches (only kernel arguments differ)
+                cudaStream_t cs = lr.cs;
+                cudaEvent_t ev = lr.ev[4];
                 CVZ_CUDA(cudaEventRecord(ev, s));
                 CVZ_CUDA(cudaStreamWaitEvent(cs, ev, 0));
                 cudaGraph_t graph = nullptr;
-                cudaGraphExec_t exec = nullptr;
                 long long before = g_launches.load();
                 CVZ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
                 bool ok = true;
@@ -2656,23 +2683,35 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                 cudaError_t ce = cudaStreamEndCapture(cs, &graph);
                 long long per_iter = g_launches.load() - before;
                 g_launches.fetch_sub(per_iter);
-                if (ok && ce == cudaSuccess &&
-                    cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+                bool ready = false;
+                if (ok && ce == cudaSuccess) {
+                    if (lr.exec) {
+                        cudaGraphExecUpdateResultInfo info;
+                        if (cudaGraphExecUpdate(lr.exec, graph, &info) == cudaSuccess) {
+                            ready = true;
+                        } else {
+                            cudaGetLastError();
+                            cudaGraphExecDestroy(lr.exec);
+                            lr.exec = nullptr;
+                        }
+                    }
+                    if (!ready && cudaGraphInstantiate(&lr.exec, graph, 0) == cudaSuccess)
+                        ready = true;
+                }
+                if (ready) {
                     for (long long it = 0; it < P->iterations; ++it) {
-                        CVZ_CUDA(cudaGraphLaunch(exec, cs));
+                        CVZ_CUDA(cudaGraphLaunch(lr.exec, cs));
                         g_launches.fetch_add(per_iter);
                     }
                     CVZ_CUDA(cudaEventRecord(ev, cs));
                     CVZ_CUDA(cudaStreamWaitEvent(s, ev, 0));
                 } else {
                     cudaGetLastError();
+                    if (lr.exec) cudaGraphExecDestroy(lr.exec);
+                    lr.exec = nullptr;
                     use_graph = false;
                 }
-                if (exec) cudaGraphExecDestroy(exec);
                 if (graph) cudaGraphDestroy(graph);
-                CVZ_CUDA(cudaStreamSynchronize(cs));
-                cudaStreamDestroy(cs);
-                cudaEventDestroy(ev);
             }
             if (!use_graph)
                 for (long long it = 0; it < P->iterations; ++it) one_iteration(s, ids);
@@ -2686,7 +2725,7 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
             CVZ_CUDA(cudaMemcpyAsync(p2, pos0, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
             CVZ_CUDA(cudaMemcpyAsync(prev, prev0, sizeof(double2) * n, cudaMemcpyDeviceToDevice,
                                      s));
-            CVZ_CUDA(cudaMemcpyAsync(scal, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+            reset_scalars();
             CVZ_CUDA(cudaMemsetAsync(ctrs, 0, 2 * sizeof(unsigned), s));
             run_all(true);
         }
