@@ -28,6 +28,7 @@ for _ in range(5):
     ts.append(a0.elapsed_time(a1))
     qs.append(cv.modularity(g, f))
     ks.append(f.community_count)
-print(f"{cfg} div={os.environ.get('CVZ_FAST_WINDOW_DIV', 'default')} Q_det={qd:.5f} "
+print(f"{cfg} div={os.environ.get('CVZ_FAST_WINDOW_DIV', 'default')} "
+      f"all={os.environ.get('CVZ_FAST_ALL', '0')} rounds={len(f.round_history)} Q_det={qd:.5f} "
       f"Q_fast={np.mean(qs):.5f}+-{np.std(qs):.5f} k_det={det.community_count} "
       f"k_fast={np.mean(ks):.0f} ms={np.median(ts[1:]):.3f}")
