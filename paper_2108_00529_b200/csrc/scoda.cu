@@ -41,8 +41,14 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int TB = 256;
-// fast mode: edges in flight <= m / FAST_WINDOW_DIV
+// fast mode: edges in flight <= m / FAST_WINDOW_DIV (m / FAST_WINDOW_DIV_SMALL
+// below 2^20 edges: at C1 (99K edges) a 774-edge window spread the top-10
+// community share over 0.35-0.56 across runs, past the reference's own
+// 0.34-0.51 envelope; the 256-edge floor keeps it at 0.34-0.46.  Large
+// streams keep full occupancy -- 0.8 % of m in flight stays within the
+// envelope there and the window does not change their time)
 constexpr long long FAST_WINDOW_DIV = 128;
+constexpr long long FAST_WINDOW_DIV_SMALL = 512;
 
 
 struct MaxOp {
@@ -689,6 +695,29 @@ __global__ void det_finalize_kernel(long long n, const int *__restrict__ seg_sta
 constexpr int TOPT_MAX = 16;
 constexpr unsigned TOPT_INF = 0xffffffffu;
 
+// Packed per-node state of the top-b pass, one 8-byte word read per slot:
+// bits 0-31 thr (see below), byte 4 the overflow flag, byte 5 the seed d0
+// clipped to 255 (written once per round by topt_state_kernel).
+__device__ __forceinline__ unsigned *st_thr(unsigned long long *st, int x) {
+    return reinterpret_cast<unsigned *>(st + x);
+}
+__device__ __forceinline__ unsigned char *st_ovf_byte(unsigned long long *st, int x) {
+    return reinterpret_cast<unsigned char *>(st + x) + 4;
+}
+__device__ __forceinline__ unsigned st_thr_of(unsigned long long w) { return (unsigned)w; }
+__device__ __forceinline__ bool st_ovf(unsigned long long w) { return (w >> 32) & 0xff; }
+__device__ __forceinline__ int st_d8(unsigned long long w) { return (int)((w >> 40) & 0xff); }
+
+__global__ void topt_state_kernel(long long n, const long long *__restrict__ d0,
+                                  unsigned long long *__restrict__ st) {
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long d = d0 ? d0[x] : 0;
+        const unsigned long long d8 = (unsigned long long)(d < 0 ? 0 : (d > 255 ? 255 : d));
+        st[x] = (unsigned long long)TOPT_INF | (d8 << 40);
+    }
+}
+
 // thr[x] >= the current b-th entry of x's list (an upper bound that only
 // decreases): a slot above it is not among x's b smallest -- one read of a
 // 4-byte-per-node array rejects most slots without touching the list.  ovf
@@ -698,16 +727,16 @@ constexpr unsigned TOPT_INF = 0xffffffffu;
 // Continue the cascade of v from position i (old = the value it displaced
 // there, already known not to be TOPT_INF).
 __device__ __noinline__ void topt_cascade(unsigned *__restrict__ A, int i, int b, unsigned v,
-                                          unsigned old, unsigned *__restrict__ thr,
-                                          unsigned char *__restrict__ ovf, int x) {
+                                          unsigned old, unsigned long long *__restrict__ st,
+                                          int x) {
     v = max(old, v);
     for (++i; i < b; ++i) {
         old = atomicMin(A + i, v);
-        if (i == b - 1) atomicMin(thr + x, min(old, v));
+        if (i == b - 1) atomicMin(st_thr(st, x), min(old, v));
         if (old == TOPT_INF) return;
         v = max(old, v);
     }
-    if (!__ldcg(ovf + x)) ovf[x] = 1;  // the largest of b + 1 values falls off the end
+    if (!st_ovf(__ldcg(st + x))) *st_ovf_byte(st, x) = 1;  // the largest of b + 1 falls off
 }
 
 // one thread per pair of edges (one 128-bit load), this launch's nodes in
@@ -718,9 +747,8 @@ __device__ __noinline__ void topt_cascade(unsigned *__restrict__ A, int i, int b
 // atomics) so their L2 round trips overlap, and the next pair is prefetched.
 template <int S>  // list stride: 4, 8, 12 or 16 entries
 __global__ void __launch_bounds__(TB, 8) topt_kernel(const int4 *__restrict__ E2, const int2 *__restrict__ E, long long m,
-                            const long long *__restrict__ d0, long long T,
-                            unsigned *__restrict__ list, unsigned *__restrict__ thr,
-                            unsigned char *__restrict__ ovf, int xlo, int xhi) {
+                            long long T, unsigned *__restrict__ list,
+                            unsigned long long *__restrict__ st, int xlo, int xhi) {
     const long long pairs = (m + 1) / 2;
     const long long W = (long long)gridDim.x * blockDim.x;
     auto load = [&](long long i, int (&x)[4]) {
@@ -761,38 +789,33 @@ __global__ void __launch_bounds__(TB, 8) topt_kernel(const int4 *__restrict__ E2
 #pragma unroll
         for (int j = 0; j < 4; ++j) x[j] = (nx[j] >= xlo && nx[j] < xhi) ? nx[j] : -1;
         load(i + W, nx);
+        unsigned long long w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = x[j] >= 0 ? __ldcg(st + x[j]) : 0ull;
         int b[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            b[j] = x[j] < 0 ? -1 : (int)(T - (d0 ? __ldg(d0 + x[j]) : 0LL));
-        unsigned t[4];
-        unsigned char o[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            t[j] = b[j] > 0 ? __ldcg(thr + x[j]) : 0u;
-            o[j] = b[j] >= 0 ? __ldcg(ovf + x[j]) : (unsigned char)1;
-        }
+        for (int j = 0; j < 4; ++j) b[j] = x[j] < 0 ? -1 : (int)(T - st_d8(w[j]));
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const unsigned v = (unsigned)(4 * i + j);
-            const bool ins = b[j] > 0 && t[j] >= v;
+            const bool ins = b[j] > 0 && st_thr_of(w[j]) >= v;
             // b == 0 (seed T): every occurrence overflows; b < 0: seed > T,
             // counter unchanged; a slot above the threshold overflows
-            if (b[j] >= 0 && !ins && !o[j]) ovf[x[j]] = 1;
+            if (b[j] >= 0 && !ins && !st_ovf(w[j])) *st_ovf_byte(st, x[j]) = 1;
             if (!ins) continue;
             unsigned *A = list + (size_t)x[j] * S;
             // the cascade may start at the first entry above v (earlier
             // entries are smaller and only decrease)
-            int st = 0;
+            int s0 = 0;
 #pragma unroll
             for (int q = 0; q < S / 4; ++q) {
                 const uint4 g = __ldcg(reinterpret_cast<const uint4 *>(A) + q);
-                st += (g.x < v) + (g.y < v) + (g.z < v) + (g.w < v);
+                s0 += (g.x < v) + (g.y < v) + (g.z < v) + (g.w < v);
             }
-            st = min(st, b[j] - 1);
-            const unsigned old = atomicMin(A + st, v);
-            if (st == b[j] - 1) atomicMin(thr + x[j], min(old, v));
-            if (old != TOPT_INF) topt_cascade(A, st, b[j], v, old, thr, ovf, x[j]);
+            s0 = min(s0, b[j] - 1);
+            const unsigned old = atomicMin(A + s0, v);
+            if (s0 == b[j] - 1) atomicMin(st_thr(st, x[j]), min(old, v));
+            if (old != TOPT_INF) topt_cascade(A, s0, b[j], v, old, st, x[j]);
         }
     }
 }
@@ -802,11 +825,11 @@ __global__ void __launch_bounds__(TB, 8) topt_kernel(const int4 *__restrict__ E2
 // node_parents_kernel, from the list instead of the sorted segment
 template <class CT>
 __global__ void topt_counters_kernel(long long n, int S, const unsigned *__restrict__ list,
-                                     const long long *__restrict__ d0, long long T,
+                                     const unsigned long long *__restrict__ st, long long T,
                                      CT *__restrict__ cval) {
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
          x += (long long)gridDim.x * blockDim.x) {
-        const long long d = d0 ? d0[x] : 0;
+        const long long d = st_d8(st[x]);
         if (d >= T) continue;
         const uint4 *A = reinterpret_cast<const uint4 *>(list + (size_t)x * S);
         const int b = (int)(T - d);
@@ -824,12 +847,12 @@ __global__ void topt_counters_kernel(long long n, int S, const unsigned *__restr
 }
 
 __global__ void topt_parents_kernel(long long n, int S, const unsigned *__restrict__ list,
-                                    const long long *__restrict__ d0, long long T,
+                                    const unsigned long long *__restrict__ st, long long T,
                                     const signed char *__restrict__ role,
                                     int *__restrict__ parent, int *__restrict__ finalw) {
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
          x += (long long)gridDim.x * blockDim.x) {
-        const long long d = d0 ? d0[x] : 0;
+        const long long d = st_d8(st[x]);
         int last = -1;
         if (d < T) {
             const uint4 *A = reinterpret_cast<const uint4 *>(list + (size_t)x * S);
@@ -858,7 +881,7 @@ __global__ void topt_parents_kernel(long long n, int S, const unsigned *__restri
 // final counter / label per node: deg = d0 if d0 > T, T + 1 on overflow,
 // else d0 + (active slots); label = initial label of the last write's origin
 __global__ void topt_finalize_kernel(long long n, int S, const unsigned *__restrict__ list,
-                                     const unsigned char *__restrict__ ovf,
+                                     const unsigned long long *__restrict__ st,
                                      const int *__restrict__ finalw, const int *__restrict__ origin,
                                      const long long *__restrict__ d0,
                                      const long long *__restrict__ lab0, long long T,
@@ -866,10 +889,13 @@ __global__ void topt_finalize_kernel(long long n, int S, const unsigned *__restr
                                      long long *__restrict__ lab_out) {
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
          x += (long long)gridDim.x * blockDim.x) {
-        const long long d = d0 ? d0[x] : 0;
+        const unsigned long long w = st[x];
+        // a seed above T leaves the counter unchanged: d0 itself (the clipped
+        // byte is exact below 255)
+        const long long d = st_d8(w) < 255 ? st_d8(w) : d0[x];
         long long deg = d;
         if (d <= T) {
-            if (ovf[x]) {
+            if (st_ovf(w)) {
                 deg = T + 1;
             } else {
                 const unsigned *A = list + (size_t)x * S;
@@ -1412,9 +1438,8 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
 // spreads the first wave over the whole stream, and random arrival order
 // turns inserts into dependent atomic cascades.
 template <int S>
-static void launch_topt(const int4 *E2, const int2 *E, long long m, long long pairs,
-                        const long long *d0, long long T, unsigned *list, unsigned *thr,
-                        unsigned char *ovf, int lo, int hi, cudaStream_t s) {
+static void launch_topt(const int4 *E2, const int2 *E, long long m, long long pairs, long long T,
+                        unsigned *list, unsigned long long *st, int lo, int hi, cudaStream_t s) {
     static DeviceCache occ;
     const int per_sm = occ.get([] {
         int b = 0;
@@ -1423,7 +1448,7 @@ static void launch_topt(const int4 *E2, const int2 *E, long long m, long long pa
     });
     const unsigned grid = (unsigned)std::max<long long>(
         1, std::min<long long>((long long)per_sm * num_sms(), (pairs + TB - 1) / TB));
-    CVZ_LAUNCH(topt_kernel<S>, grid, TB, 0, s, E2, E, m, d0, T, list, thr, ovf, lo, hi);
+    CVZ_LAUNCH(topt_kernel<S>, grid, TB, 0, s, E2, E, m, T, list, st, lo, hi);
 }
 
 // Deterministic pass, top-T formulation (T <= TOPT_MAX, see topt_insert):
@@ -1435,13 +1460,11 @@ static void det_pass_topt(const int2 *E, long long m, long long n, long long T, 
     auto *d0p = reinterpret_cast<const long long *>(d0);
     const int S = (int)std::max(4LL, (T + 3) & ~3LL);  // list stride: whole 16-byte groups
     unsigned *list = sc.alloc<unsigned>((size_t)n * S);
-    unsigned char *ovf = sc.alloc<unsigned char>(n);
+    auto *st = sc.alloc<unsigned long long>(n);
     int *finalw = sc.alloc<int>(n);
     int *origin = sc.alloc<int>(m > 0 ? m : 1);
-    unsigned *thr = sc.alloc<unsigned>(n);
     CVZ_CUDA(cudaMemsetAsync(list, 0xff, sizeof(unsigned) * (size_t)n * S, s));
-    CVZ_CUDA(cudaMemsetAsync(thr, 0xff, sizeof(unsigned) * n, s));
-    CVZ_CUDA(cudaMemsetAsync(ovf, 0, n, s));
+    CVZ_LAUNCH(topt_state_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n, d0p, st);
     if (m > 0) {
         const bool al = (reinterpret_cast<uintptr_t>(E) & 15) == 0;
         // (one pass over the stream; splitting the nodes into L2-sized ranges
@@ -1451,20 +1474,20 @@ static void det_pass_topt(const int2 *E, long long m, long long n, long long T, 
         const int4 *E2 = al ? reinterpret_cast<const int4 *>(E) : nullptr;
         const int hi = (int)n;
         switch (S) {
-            case 4: launch_topt<4>(E2, E, m, pairs, d0p, T, list, thr, ovf, 0, hi, s); break;
-            case 8: launch_topt<8>(E2, E, m, pairs, d0p, T, list, thr, ovf, 0, hi, s); break;
-            case 12: launch_topt<12>(E2, E, m, pairs, d0p, T, list, thr, ovf, 0, hi, s); break;
-            default: launch_topt<16>(E2, E, m, pairs, d0p, T, list, thr, ovf, 0, hi, s); break;
+            case 4: launch_topt<4>(E2, E, m, pairs, T, list, st, 0, hi, s); break;
+            case 8: launch_topt<8>(E2, E, m, pairs, T, list, st, 0, hi, s); break;
+            case 12: launch_topt<12>(E2, E, m, pairs, T, list, st, 0, hi, s); break;
+            default: launch_topt<16>(E2, E, m, pairs, T, list, st, 0, hi, s); break;
         }
         unsigned char *cval = sc.alloc<unsigned char>(2 * m);
         CVZ_CUDA(cudaMemsetAsync(cval, (int)(T + 1), 2 * m, s));
         CVZ_LAUNCH(topt_counters_kernel<unsigned char>, grid_for(n, TB, 1, 8), TB, 0, s, n, S,
-                   list, d0p, T, cval);
+                   list, st, T, cval);
         auto *role = sc.alloc<signed char>(m);
         CVZ_LAUNCH(edge_role_kernel<unsigned char>, grid_for(m, TB, 1, 16), TB, 0, s, E, m, cval,
                    T, tie, role);
         int *parent = sc.alloc<int>(m);
-        CVZ_LAUNCH(topt_parents_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n, S, list, d0p, T, role,
+        CVZ_LAUNCH(topt_parents_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n, S, list, st, T, role,
                    parent, finalw);
         int *ptr = sc.alloc<int>(m);
         int *wa = sc.alloc<int>(m), *wb = sc.alloc<int>(m);
@@ -1477,7 +1500,7 @@ static void det_pass_topt(const int2 *E, long long m, long long n, long long T, 
     } else {
         CVZ_CUDA(cudaMemsetAsync(finalw, 0xff, sizeof(int) * n, s));
     }
-    CVZ_LAUNCH(topt_finalize_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n, S, list, ovf, finalw, origin,
+    CVZ_LAUNCH(topt_finalize_kernel, grid_for(n, TB, 1, 8), TB, 0, s, n, S, list, st, finalw, origin,
                d0p, reinterpret_cast<const long long *>(lab0), T,
                reinterpret_cast<long long *>(deg_out), reinterpret_cast<long long *>(lab_out));
 }
@@ -1514,9 +1537,10 @@ void scoda_pass_dev(const int2 *E, long long m, long long n, long long T, int ti
         // reference's own parallel schedules (C/community.py:164-195) only
         // while the edges in flight are a small fraction of the stream
         // (DESIGN.md "fast mode"); at C4 scale this is full occupancy anyway.
-        static const long long wdiv =
-            getenv("CVZ_FAST_WINDOW_DIV") ? std::max(1LL, atoll(getenv("CVZ_FAST_WINDOW_DIV")))
-                                          : FAST_WINDOW_DIV;
+        static const long long wenv =
+            getenv("CVZ_FAST_WINDOW_DIV") ? std::max(1LL, atoll(getenv("CVZ_FAST_WINDOW_DIV"))) : 0;
+        const long long wdiv =
+            wenv ? wenv : (m < (1LL << 20) ? FAST_WINDOW_DIV_SMALL : FAST_WINDOW_DIV);
         long long window = std::max(256LL, std::min(m / wdiv, 2048LL * num_sms() * FU));
         unsigned blocks = (unsigned)((window / FU + TB - 1) / TB);
         // default: per-edge int2 loads and plain atomics (fast_pass_kernel);
