@@ -25,6 +25,7 @@
 // swing, last block -> global speed] [update, clamp, disp max, bbox, last
 // block -> next bbox].  The whole iteration is captured once into a CUDA
 // graph and replayed `iterations` times; all scalars live on the device.
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -2553,6 +2554,7 @@ struct LayoutRes {
     cudaStream_t side = nullptr, aux = nullptr, cs = nullptr;
     cudaEvent_t ev[6] = {};
     cudaGraphExec_t exec = nullptr;
+    long long key[4] = {-1, -1, -1, -1};  // what `exec` was captured for
 };
 
 static LayoutRes &layout_res() {
@@ -2684,7 +2686,18 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                 long long per_iter = g_launches.load() - before;
                 g_launches.fetch_sub(per_iter);
                 bool ready = false;
+                // the iteration's node set is fixed by these (launch
+                // configurations may differ, which an update allows); a
+                // different shape gets a fresh instantiation instead of a
+                // failed update
+                const long long key[4] = {(long long)n, (long long)csr.nheavy > 0,
+                                          (long long)exact, (long long)ids};
+                if (lr.exec && !std::equal(key, key + 4, lr.key)) {
+                    cudaGraphExecDestroy(lr.exec);
+                    lr.exec = nullptr;
+                }
                 if (ok && ce == cudaSuccess) {
+                    std::copy(key, key + 4, lr.key);
                     if (lr.exec) {
                         cudaGraphExecUpdateResultInfo info;
                         if (cudaGraphExecUpdate(lr.exec, graph, &info) == cudaSuccess) {
