@@ -392,7 +392,6 @@ int cvz_contract(const int32_t *edges, int64_t m, const int64_t *labels, int64_t
                 superedges<unsigned>(e, m, dense, k, B, sc, s, res);
             else
                 superedges<unsigned long long>(e, m, dense, k, B, sc, s, res);
-            CVZ_CUDA(cudaStreamSynchronize(s));
         } catch (...) {
             // the result buffers live outside the arena: release them here,
             // the caller never sees a half-filled result

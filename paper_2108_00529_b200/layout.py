@@ -10,6 +10,8 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass
 
+import functools
+
 import numpy as np
 
 from . import _native as nat
@@ -70,6 +72,14 @@ def init_positions(n: int, seed: int = 0) -> np.ndarray:
     return np.random.default_rng(seed).uniform(-side / 2, side / 2, size=(n, 2))
 
 
+@functools.lru_cache(maxsize=64)
+def _pcg64_state(seed: int):
+    """numpy's PCG64 state for default_rng(seed) (SeedSequence hashing costs
+    ~0.1 ms of host time per call, while the GPU would sit idle)."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    return int(st["state"]), int(st["inc"])
+
+
 def _init_positions_dev(n: int, seed: int = 0):
     """init_positions drawn on the GPU (cvz_pcg64_uniform): numpy's PCG64
     stream seeded by numpy on the host, bit-identical values, no host loop
@@ -77,8 +87,11 @@ def _init_positions_dev(n: int, seed: int = 0):
     T = nat.torch()
     side = max(np.sqrt(n), 1.0)
     low, high = -side / 2, side / 2
-    st = np.random.default_rng(seed).bit_generator.state["state"]
-    s, inc = int(st["state"]), int(st["inc"])
+    if isinstance(seed, (int, np.integer)):
+        s, inc = _pcg64_state(int(seed))
+    else:  # None / SeedSequence / Generator-like seeds: never cached
+        st = np.random.default_rng(seed).bit_generator.state["state"]
+        s, inc = int(st["state"]), int(st["inc"])
     m64 = (1 << 64) - 1
     out = T.empty((n, 2), dtype=T.float64, device=nat.device())
     nat.call("cvz_pcg64_uniform", s >> 64, s & m64, inc >> 64, inc & m64, low, high - low,

@@ -92,35 +92,46 @@ def contract(g, labels, sketch: CountMinSketch) -> SuperGraph:
     nat.call("cvz_contract", nat.ptr(e), int(e.shape[0]), nat.ptr(lab), g.node_count,
              nat.ptr(sketch.table_dev()), sketch.rows, sketch.cols, nat.ptr(a), nat.ptr(b),
              ctypes.byref(res), nat.stream())
-    dev = nat.device()
     k, se = int(res.k), int(res.se)
-    comm = T.empty(k, dtype=T.int64, device=dev)
-    weight = T.empty(k, dtype=T.int64, device=dev)
-    edges = T.empty((se, 2), dtype=T.int64, device=dev)
-    mult = T.empty(se, dtype=T.int64, device=dev)
-    try:
-        cudart = _memcpy_d2d
-        cudart(comm, res.comm_id, 8 * k)
-        cudart(weight, res.weight, 8 * k)
-        cudart(edges, res.se_edges, 16 * se)
-        cudart(mult, res.mult, 8 * se)
-    finally:
-        nat.call("cvz_contract_release", ctypes.byref(res), nat.stream())
+    owner = _ContractBuffers(res)
+    comm = owner.tensor(res.comm_id, (k,))
+    weight = owner.tensor(res.weight, (k,))
+    edges = owner.tensor(res.se_edges, (se, 2))
+    mult = owner.tensor(res.mult, (se,))
     return SuperGraph._from_device(k, edges, weight, mult, comm)
 
 
-def _memcpy_d2d(dst, src_ptr, nbytes):
-    """Copy a library-owned device buffer into a torch tensor (stream-ordered)."""
-    if nbytes == 0:
-        return
-    T = nat.torch()
-    # wrap the raw pointer via __cuda_array_interface__ and copy on the stream
-    class _Raw:
-        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
-                                    "data": (int(src_ptr), False), "version": 3,
-                                    "stream": None}
-    src = T.as_tensor(_Raw(), device=dst.device)
-    dst.view(T.uint8).reshape(-1)[:nbytes].copy_(src)
+class _ContractBuffers:
+    """Owner of the four result buffers cvz_contract allocated.  The returned
+    tensors VIEW them (no device-to-device copies); each view keeps this
+    owner alive, and the last one to go releases all four (stream-ordered
+    cudaFreeAsync, cvz_contract_release)."""
+
+    def __init__(self, res):
+        self.res = res
+
+    def tensor(self, ptr, shape):
+        T = nat.torch()
+        if not ptr or 0 in shape:
+            return T.empty(shape, dtype=T.int64, device=nat.device())
+        return T.as_tensor(_View(self, ptr, shape), device=nat.device())
+
+    def __del__(self):
+        try:
+            nat.call("cvz_contract_release", ctypes.byref(self.res), nat.stream())
+        except Exception:  # interpreter shutdown: the CUDA context is gone anyway
+            pass
+
+
+class _View:
+    """__cuda_array_interface__ of one int64 result buffer (torch.as_tensor
+    holds a reference to this object for the tensor's lifetime)."""
+
+    def __init__(self, owner, ptr, shape):
+        self.owner = owner
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<i8",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "stream": None}
 
 
 def export_supernodes_tsv(sg: SuperGraph, path) -> None:

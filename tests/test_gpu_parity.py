@@ -419,6 +419,39 @@ def test_contract_at_scale(cv, orc):
     assert np.all(sg.edges[:, 0] < sg.edges[:, 1])
 
 
+def test_contract_results_are_views_released_with_the_supergraph(cv, monkeypatch):
+    """contract() hands out zero-copy views of the library's result buffers;
+    they stay valid while any view is alive and are released once, when the
+    last one goes."""
+    import gc
+    from paper_2108_00529_b200 import supergraph as sgm
+    from paper_2108_00529_b200 import synth
+    released = []
+    orig = sgm._ContractBuffers.__del__
+    monkeypatch.setattr(sgm._ContractBuffers, "__del__",
+                        lambda self: (released.append(1), orig(self)))
+    e = synth.config_graph("C1")
+    g = cv.from_edge_array(e)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=cv.degree_stats(g).mode_degree))
+    s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    cv.accumulate_sizes(s, a, g)
+    sg = cv.contract(g, a, s)
+    mult_dev = sg.multiplicity_dev()  # a view that outlives the SuperGraph
+    ref_edges, ref_mult = sg.edges.copy(), sg.multiplicity.copy()
+    del sg
+    gc.collect()
+    assert not released
+    sg2 = cv.contract(g, a, s)  # a second result must not alias the first
+    assert np.array_equal(mult_dev.cpu().numpy(), ref_mult)
+    assert np.array_equal(sg2.edges, ref_edges)
+    del mult_dev
+    gc.collect()
+    assert len(released) == 1
+    del sg2
+    gc.collect()
+    assert len(released) == 2
+
+
 def test_contract_segment_tiers_vs_oracle(cv, orc):
     """Superedge aggregation with skewed per-community crossing counts (one
     community with 70K crossing edges, others with 9K / 600 / a few) and
