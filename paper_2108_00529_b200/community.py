@@ -182,10 +182,10 @@ def scoda_round(g, a: CommunityAssignment, threshold: int,
 
 
 def _mode_degree(g) -> int:
-    from .graph import _stats_dev
+    from .graph import _graph_stats
     if g.node_count == 0:
         return 1
-    mode, _, _ = _stats_dev(g.degree_dev(), g.node_count)
+    mode, _, _ = _graph_stats(g)
     return mode if mode > 0 else 1  # C/community.py:243-244
 
 

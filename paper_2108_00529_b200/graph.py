@@ -25,7 +25,7 @@ class ParseError(ValueError):
 class Graph:
     """Immutable undirected multigraph over dense ids (C/graph.py:24-40)."""
 
-    __slots__ = ("node_count", "_edges", "_degree", "_edges32")
+    __slots__ = ("node_count", "_edges", "_degree", "_edges32", "_stats")
 
     def __init__(self, node_count: int, edges, degree):
         edges = np.asarray(edges)
@@ -38,6 +38,7 @@ class Graph:
         self._edges = Dual(host=edges)
         self._degree = Dual(host=degree)
         self._edges32 = None
+        self._stats = None
 
     @classmethod
     def _from_device(cls, n: int, edges32, degree64):
@@ -46,6 +47,7 @@ class Graph:
         g._edges = Dual(dev=edges32)
         g._degree = Dual(dev=degree64)
         g._edges32 = edges32
+        g._stats = None
         return g
 
     @property
@@ -308,11 +310,23 @@ def _stats_dev(degree_dev, n):
     return [int(v) for v in out.cpu().tolist()]
 
 
+def _graph_stats(g: Graph):
+    """(mode of nonzero degrees, degree sum, max degree), computed once per
+    Graph while its degrees live only on the device (detect_communities
+    needs the mode again after degree_stats; a host copy the caller could
+    mutate disables the cache)."""
+    if not g._degree.on_device:
+        return _stats_dev(g.degree_dev(), g.node_count)
+    if g._stats is None:
+        g._stats = tuple(_stats_dev(g.degree_dev(), g.node_count))
+    return g._stats
+
+
 def degree_stats(g: Graph) -> DegreeStats:
     """C/graph.py:125-136 on the GPU (mode of nonzero degrees, ties -> smaller)."""
     if g.edge_count == 0:
         raise ValueError("degree stats undefined for a graph with no edges")
-    mode, total, mx = _stats_dev(g.degree_dev(), g.node_count)
+    mode, total, mx = _graph_stats(g)
     return DegreeStats(mode_degree=mode,
                        average_degree=float(np.int64(total) / g.node_count),
                        max_degree=mx)
