@@ -746,7 +746,7 @@ __device__ __noinline__ void topt_cascade(unsigned *__restrict__ A, int i, int b
 // issued phase by phase (threshold + overflow reads, list reads, first
 // atomics) so their L2 round trips overlap, and the next pair is prefetched.
 template <int S>  // list stride: 4, 8, 12 or 16 entries
-__global__ void __launch_bounds__(TB, 8) topt_kernel(const int4 *__restrict__ E2, const int2 *__restrict__ E, long long m,
+__global__ void __launch_bounds__(TB, 6) topt_kernel(const int4 *__restrict__ E2, const int2 *__restrict__ E, long long m,
                             long long T, unsigned *__restrict__ list,
                             unsigned long long *__restrict__ st, int xlo, int xhi) {
     const long long pairs = (m + 1) / 2;
@@ -777,6 +777,10 @@ __global__ void __launch_bounds__(TB, 8) topt_kernel(const int4 *__restrict__ E2
     };
     int nx[4];
     load((long long)blockIdx.x * blockDim.x + threadIdx.x, nx);
+    __shared__ unsigned s_qx[TB / 32][128], s_qv[TB / 32][128];
+    __shared__ unsigned char s_qb[TB / 32][128];
+    unsigned *qx = s_qx[threadIdx.x >> 5], *qv = s_qv[threadIdx.x >> 5];
+    unsigned char *qb = s_qb[threadIdx.x >> 5];
     // warp-uniform trip count + __syncwarp per iteration: the inserts'
     // data-dependent branches would otherwise let the lanes of a warp drift
     // into different iterations (independent thread scheduling does not
@@ -795,6 +799,12 @@ __global__ void __launch_bounds__(TB, 8) topt_kernel(const int4 *__restrict__ E2
         int b[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) b[j] = x[j] < 0 ? -1 : (int)(T - st_d8(w[j]));
+        // inserts are compacted across the warp (each lane's four slots ->
+        // one shared queue) so the list read -> atomic chain runs once or
+        // twice per lane per iteration instead of once per slot position
+        // with the other lanes idle (four serialised phases per iteration)
+        const int lane = lane_id();
+        unsigned base = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const unsigned v = (unsigned)(4 * i + j);
@@ -802,21 +812,56 @@ __global__ void __launch_bounds__(TB, 8) topt_kernel(const int4 *__restrict__ E2
             // b == 0 (seed T): every occurrence overflows; b < 0: seed > T,
             // counter unchanged; a slot above the threshold overflows
             if (b[j] >= 0 && !ins && !st_ovf(w[j])) *st_ovf_byte(st, x[j]) = 1;
-            if (!ins) continue;
-            unsigned *A = list + (size_t)x[j] * S;
+            const unsigned mk = __ballot_sync(0xffffffffu, ins);
+            if (ins) {
+                const unsigned q = base + __popc(mk & ((1u << lane) - 1));
+                qx[q] = x[j];
+                qv[q] = v;
+                qb[q] = (unsigned char)b[j];
+            }
+            base += __popc(mk);
+        }
+        __syncwarp();
+        // at most four entries per lane: list reads first, then the atomics
+        unsigned ex[4], ev[4], eb[4], es[4];
+        int ne = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const unsigned q = lane + 32u * r;
+            if (q < base) {
+                ex[r] = qx[q];
+                ev[r] = qv[q];
+                eb[r] = qb[q];
+                ne = r + 1;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r >= ne) break;
+            const unsigned *A = list + (size_t)ex[r] * S;
             // the cascade may start at the first entry above v (earlier
             // entries are smaller and only decrease)
             int s0 = 0;
 #pragma unroll
             for (int q = 0; q < S / 4; ++q) {
                 const uint4 g = __ldcg(reinterpret_cast<const uint4 *>(A) + q);
-                s0 += (g.x < v) + (g.y < v) + (g.z < v) + (g.w < v);
+                s0 += (g.x < ev[r]) + (g.y < ev[r]) + (g.z < ev[r]) + (g.w < ev[r]);
             }
-            s0 = min(s0, b[j] - 1);
-            const unsigned old = atomicMin(A + s0, v);
-            if (s0 == b[j] - 1) atomicMin(st_thr(st, x[j]), min(old, v));
-            if (old != TOPT_INF) topt_cascade(A, s0, b[j], v, old, st, x[j]);
+            es[r] = (unsigned)min(s0, (int)eb[r] - 1);
         }
+        unsigned old[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            if (r < ne) old[r] = atomicMin(list + (size_t)ex[r] * S + es[r], ev[r]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r >= ne) break;
+            if ((int)es[r] == (int)eb[r] - 1) atomicMin(st_thr(st, (int)ex[r]), min(old[r], ev[r]));
+            if (old[r] != TOPT_INF)
+                topt_cascade(list + (size_t)ex[r] * S, (int)es[r], (int)eb[r], ev[r], old[r], st,
+                             (int)ex[r]);
+        }
+        __syncwarp();  // the queue is reused by the next iteration
     }
 }
 
