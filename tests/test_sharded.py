@@ -34,14 +34,14 @@ def _spawn(fn, world, *args):
     mp.spawn(fn, args=(world, port) + args, nprocs=world, join=True)
 
 
-def _init(rank, world, port):
+def _init(rank, world, port, backend="gloo"):
     import sys
     if ROOT not in sys.path:
         sys.path.insert(0, ROOT)
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group(backend, rank=rank, world_size=world)
     return dist
 
 
@@ -172,6 +172,65 @@ def _gpu_worker(rank, world, port, out_dir, iters):
              exact_pos=r_exact.positions, coin_pos=r_coin.positions, p0=p0)
     dist.barrier()
     dist.destroy_process_group()
+
+
+# ------------------------------------------------------------- GPU (NCCL)
+def _nccl_worker(rank, world, port, out_dir):
+    """A world of one over NCCL with the collectives forced on (Comm.force):
+    every NCCL call of the sharded stages -- in-place all_reduce (int64 sum,
+    fp64 sum / max), broadcast, all_gather_into_tensor -- runs on real NCCL
+    device buffers (a multi-GPU box is not available to the tests)."""
+    import torch
+    torch.cuda.set_device(0)
+    dist = _init(rank, world, port, "nccl")
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import synth
+    from paper_2108_00529_b200.sharded import (Comm, accumulate_sizes_sharded,
+                                               broadcast_labels, from_edge_array_sharded,
+                                               layout_sharded)
+    comm = Comm()
+    assert comm.backend == "nccl" and not comm.staged
+    comm.force = True
+    e = synth.planted_partition(4000, 40000, 40, seed=5).copy()
+    e[::53, 1] = e[::53, 0]
+    sg = from_edge_array_sharded(e, comm)
+    g = sg.gather()
+    base = cv.degree_stats(g).mode_degree
+    lab = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+    labels = broadcast_labels(lab, g.node_count, comm)
+    s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    accumulate_sizes_sharded(s, labels, sg)
+    sup = cv.contract(g, labels, s)
+    r_sup = layout_sharded(sup, cv.LayoutParams(iterations=10), comm)
+    np.savez(os.path.join(out_dir, "nccl.npz"), degree=sg.degree, edges=g.edges,
+             labels=labels.cpu().numpy(), table=s.table, sup_pos=r_sup.positions,
+             sup_disp=r_sup.displacement)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_sharded_nccl_branch_matches_single_gpu():
+    import paper_2108_00529_b200 as cv
+    from paper_2108_00529_b200 import synth
+    with tempfile.TemporaryDirectory() as d:
+        _spawn(_nccl_worker, 1, d)
+        r = np.load(os.path.join(d, "nccl.npz"))
+    e = synth.planted_partition(4000, 40000, 40, seed=5).copy()
+    e[::53, 1] = e[::53, 0]
+    g = cv.from_edge_array(e)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=cv.degree_stats(g).mode_degree),
+                              seed=0, workers=1)
+    s = cv.sketch_new(4, cv.default_cols(g.edge_count), seed=0)
+    cv.accumulate_sizes(s, a, g)
+    sup = cv.contract(g, a, s)
+    ref = cv.layout(sup, cv.LayoutParams(iterations=10))
+    assert np.array_equal(r["degree"], g.degree) and np.array_equal(r["edges"], g.edges)
+    assert np.array_equal(r["labels"], a.label) and np.array_equal(r["table"], s.table)
+    diam = np.hypot(*(ref.positions.max(0) - ref.positions.min(0)))
+    assert np.max(np.abs(r["sup_pos"] - ref.positions)) <= 1e-7 * diam
+    np.testing.assert_allclose(r["sup_disp"], ref.displacement, rtol=1e-6, atol=1e-9)
 
 
 @pytest.mark.gpu
