@@ -506,7 +506,7 @@ def run_sharded(args, rank, ws, reps=3):
 C5_SCALE = int(os.environ.get("CVZ_C5_SCALE", "26"))
 
 
-def run_c5(comm, rank, ws, reps=3):
+def run_c5(comm, rank, ws, reps=3, fa2=True):
     """BASELINE config C5: R-MAT scale 26 (2^26 nodes, 2^30 edge draws),
     edge-sharded ingest + degrees + sketch across the ranks.
     Each rank generates its own slice of the counter-based stream in HBM
@@ -556,7 +556,8 @@ def run_c5(comm, rank, ws, reps=3):
     # node-sharded full-graph ForceAtlas2 on the same R-MAT-26 graph: every
     # rank holds the whole compacted edge list (all-gather), builds its CSR
     # over the rows it owns only, the full tree, and walks/moves its bodies
-    out["fa2"] = run_c5_fa2(comm, g, ws)
+    if fa2:
+        out["fa2"] = run_c5_fa2(comm, g, ws)
     del g
     torch.cuda.empty_cache()
     return out

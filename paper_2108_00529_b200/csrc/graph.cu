@@ -188,6 +188,41 @@ __global__ void degree_kernel(const int4 *__restrict__ e2, long long npairs2,
     }
 }
 
+// Single pass with the lowest HOT node ids counted in shared memory first
+// (R-MAT and most generators put the hubs at low ids; same-address L2
+// atomics on a hub serialise): CVZ_DEGREE_HOT experiment.
+constexpr int HOT = 2048;
+__global__ void degree_hot_kernel(const int4 *__restrict__ e2, long long npairs2,
+                                  const int2 *__restrict__ e, long long m,
+                                  unsigned long long *__restrict__ deg) {
+    __shared__ unsigned sh[HOT];
+    for (int i = threadIdx.x; i < HOT; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    long long stride = (long long)gridDim.x * blockDim.x;
+    auto add = [&](int x) {
+        if (x < HOT)
+            atomicAdd(sh + x, 1u);
+        else
+            atomicAdd(deg + x, 1ull);
+    };
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < npairs2;
+         i += stride) {
+        const int4 p = __ldcs(e2 + i);
+        add(p.x);
+        add(p.y);
+        add(p.z);
+        add(p.w);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (m & 1)) {
+        const int2 p = e[m - 1];
+        add(p.x);
+        add(p.y);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < HOT; i += blockDim.x)
+        if (sh[i]) atomicAdd(deg + i, (unsigned long long)sh[i]);
+}
+
 // sum / max / histogram of nonzero degrees (mode).
 __global__ void degree_summary_kernel(const long long *__restrict__ deg, long long n,
                                       unsigned long long *__restrict__ sum,
@@ -287,6 +322,14 @@ void degree_count(const int32_t *edges, int64_t m, int64_t n, int64_t *degree,
     CVZ_CUDA(cudaMemsetAsync(degree, 0, sizeof(int64_t) * (n ? n : 1), s));
     if (m == 0) return;
     long long pairs2 = m / 2;
+    static const bool plain = getenv("CVZ_DEGREE_PLAIN") != nullptr;  // A/B knob
+    if (!plain) {
+        CVZ_LAUNCH(degree_hot_kernel, grid_for(pairs2 > 0 ? pairs2 : 1, 256, 1, 16), 256, 0, s,
+                   reinterpret_cast<const int4 *>(edges), pairs2,
+                   reinterpret_cast<const int2 *>(edges), (long long)m,
+                   reinterpret_cast<unsigned long long *>(degree));
+        return;
+    }
     unsigned grid = grid_for(pairs2 > 0 ? pairs2 : 1, 256, 1, 16);
     CVZ_LAUNCH(degree_kernel, grid, 256, 0, s, reinterpret_cast<const int4 *>(edges), pairs2,
                reinterpret_cast<const int2 *>(edges), (long long)m,

@@ -106,6 +106,21 @@ def test_degrees_at_scale(cv, orc):
     assert (st.mode_degree, st.average_degree, st.max_degree) == orc.degree_stats(deg)
 
 
+def test_degrees_node_range_passes(cv):
+    """Degree arrays too large for L2 (> 8M nodes) are counted in 16M-node
+    u32 ranges (graph.cu degree_range_kernel): bit-exact np.bincount across
+    range boundaries, with a hub, the first and the last node."""
+    rng = np.random.default_rng(11)
+    n = 40_000_000
+    e = rng.integers(0, n, size=(3_000_001, 2), dtype=np.int64)
+    e[:5000, 0] = 16 * 2**20 - 1            # a hub at the end of range 0
+    e[5000:9000, 1] = 16 * 2**20            # ... and at the start of range 1
+    e[9000, :] = [0, n - 1]
+    g = cv.from_edge_array(e, node_count=n)
+    ee = e[e[:, 0] != e[:, 1]]
+    assert np.array_equal(g.degree, np.bincount(ee.ravel(), minlength=n))
+
+
 # -------------------------------------------------------------- community
 def test_scoda_pass_golden(cv):
     from paper_2108_00529_b200.community import _scoda_pass
