@@ -106,15 +106,16 @@ def test_degrees_at_scale(cv, orc):
     assert (st.mode_degree, st.average_degree, st.max_degree) == orc.degree_stats(deg)
 
 
-def test_degrees_node_range_passes(cv):
-    """Degree arrays too large for L2 (> 8M nodes) are counted in 16M-node
-    u32 ranges (graph.cu degree_range_kernel): bit-exact np.bincount across
-    range boundaries, with a hub, the first and the last node."""
+def test_degrees_large_n_and_hot_ids(cv):
+    """A 40M-node degree array (beyond L2) with hubs inside and just above
+    the shared-memory-counted low ids (graph.cu degree_hot_kernel):
+    bit-exact np.bincount, first and last node included."""
     rng = np.random.default_rng(11)
     n = 40_000_000
     e = rng.integers(0, n, size=(3_000_001, 2), dtype=np.int64)
-    e[:5000, 0] = 16 * 2**20 - 1            # a hub at the end of range 0
-    e[5000:9000, 1] = 16 * 2**20            # ... and at the start of range 1
+    e[:5000, 0] = 2047                      # a hub at the last shared-memory id
+    e[5000:9000, 1] = 2048                  # ... and at the first global one
+    e[9001:9500, 0] = 0
     e[9000, :] = [0, n - 1]
     g = cv.from_edge_array(e, node_count=n)
     ee = e[e[:, 0] != e[:, 1]]
