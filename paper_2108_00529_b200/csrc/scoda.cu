@@ -401,36 +401,58 @@ __global__ void node_parents_kernel(const unsigned *__restrict__ key,
 }
 
 // events: origin[k] = node whose initial label event k carries (-1 pending)
+// EI_ITEMS events per thread per sweep (block-uniform trip count): the
+// worklist append costs one block scan + one atomic per EI_ITEMS * TB
+// events, and each thread's role / edge / parent loads are issued together
+constexpr int EI_ITEMS = 8;
 __global__ void events_init_kernel(const int2 *__restrict__ E, long long m,
                                    const signed char *__restrict__ role,
                                    const int *__restrict__ parent, int *__restrict__ origin,
                                    int *__restrict__ ptr, int *__restrict__ work,
                                    unsigned *__restrict__ nwork) {
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long k0 = (long long)blockIdx.x * blockDim.x; k0 < m; k0 += stride) {
-        const long long k = k0 + threadIdx.x;  // block-uniform trip count
-        bool pend = false;
-        if (k < m) {
-            signed char r = role[k];
-            if (r >= 0) {
-                int2 p = __ldg(E + k);
-                int src = r == 0 ? p.y : p.x;
-                int par = parent[k];
-                if (par < 0) {
-                    origin[k] = src;
-                } else {
-                    origin[k] = -1;
-                    ptr[k] = par;
-                    pend = true;
-                }
+    const long long stride = (long long)gridDim.x * blockDim.x * EI_ITEMS;
+    __shared__ unsigned s_wcnt[TB / 32], s_base;
+    const int wid = threadIdx.x >> 5, lane = lane_id();
+    for (long long k0 = (long long)blockIdx.x * blockDim.x * EI_ITEMS; k0 < m; k0 += stride) {
+        signed char r[EI_ITEMS];
+#pragma unroll
+        for (int j = 0; j < EI_ITEMS; ++j) {
+            const long long k = k0 + (long long)j * blockDim.x + threadIdx.x;  // coalesced
+            r[j] = k < m ? role[k] : (signed char)-1;
+        }
+        int2 p[EI_ITEMS];
+        int par[EI_ITEMS];
+#pragma unroll
+        for (int j = 0; j < EI_ITEMS; ++j) {
+            const long long k = k0 + (long long)j * blockDim.x + threadIdx.x;
+            if (r[j] >= 0) {
+                p[j] = __ldg(E + k);
+                par[j] = parent[k];
+            }
+        }
+        unsigned pmask = 0;
+#pragma unroll
+        for (int j = 0; j < EI_ITEMS; ++j) {
+            const long long k = k0 + (long long)j * blockDim.x + threadIdx.x;
+            if (r[j] < 0) continue;
+            const int src = r[j] == 0 ? p[j].y : p[j].x;
+            if (par[j] < 0) {
+                origin[k] = src;
+            } else {
+                origin[k] = -1;
+                ptr[k] = par[j];
+                pmask |= 1u << j;
             }
         }
         // one worklist atomic per block and sweep (a per-warp atomic on the
         // single counter serialised ~1M warps in round 1 at C4)
-        __shared__ unsigned s_wcnt[TB / 32], s_base;
-        const unsigned mask = __ballot_sync(0xffffffffu, pend);
-        const int wid = threadIdx.x >> 5;
-        if (lane_id() == 0) s_wcnt[wid] = __popc(mask);
+        unsigned bal[EI_ITEMS], mine = 0;
+#pragma unroll
+        for (int j = 0; j < EI_ITEMS; ++j) {
+            bal[j] = __ballot_sync(0xffffffffu, (pmask >> j) & 1u);
+            mine += __popc(bal[j]);
+        }
+        if (lane == 0) s_wcnt[wid] = mine;
         __syncthreads();
         if (threadIdx.x == 0) {
             unsigned tot = 0;
@@ -442,8 +464,13 @@ __global__ void events_init_kernel(const int2 *__restrict__ E, long long m,
             s_base = tot ? atomicAdd(nwork, tot) : 0;
         }
         __syncthreads();
-        if (pend)
-            work[s_base + s_wcnt[wid] + __popc(mask & ((1u << lane_id()) - 1))] = (int)k;
+        unsigned base = s_base + s_wcnt[wid];
+#pragma unroll
+        for (int j = 0; j < EI_ITEMS; ++j) {
+            const long long k = k0 + (long long)j * blockDim.x + threadIdx.x;
+            if ((pmask >> j) & 1u) work[base + __popc(bal[j] & ((1u << lane) - 1))] = (int)k;
+            base += __popc(bal[j]);
+        }
         __syncthreads();
     }
 }
@@ -1458,7 +1485,7 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
         const int R = bits_for_value((unsigned long long)m) + 2;
         unsigned *cnt = sc.alloc<unsigned>(R + 1);
         CVZ_CUDA(cudaMemsetAsync(cnt, 0, (R + 1) * sizeof(unsigned), s));
-        CVZ_LAUNCH(events_init_kernel, grid_for(m, TB, 1, 16), TB, 0, s, E, m, role, parent,
+        CVZ_LAUNCH(events_init_kernel, grid_for(m, TB, EI_ITEMS, 8), TB, 0, s, E, m, role, parent,
                    origin, ptr, wa, cnt);
         CVZ_COOP(events_coop_kernel, CB, s, wa, wb, cnt, R, origin, ptr);
         if (getenv("CVZ_DEBUG_RESOLVE")) {  // development aid: event worklist per sweep
@@ -1539,7 +1566,7 @@ static void det_pass_topt(const int2 *E, long long m, long long n, long long T, 
         const int R = bits_for_value((unsigned long long)m) + 2;
         unsigned *cnt = sc.alloc<unsigned>(R + 1);
         CVZ_CUDA(cudaMemsetAsync(cnt, 0, (R + 1) * sizeof(unsigned), s));
-        CVZ_LAUNCH(events_init_kernel, grid_for(m, TB, 1, 16), TB, 0, s, E, m, role, parent,
+        CVZ_LAUNCH(events_init_kernel, grid_for(m, TB, EI_ITEMS, 8), TB, 0, s, E, m, role, parent,
                    origin, ptr, wa, cnt);
         CVZ_COOP(events_coop_kernel, CB, s, wa, wb, cnt, R, origin, ptr);
     } else {
