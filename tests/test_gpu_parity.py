@@ -193,11 +193,12 @@ def test_detect_interleaved_orders_bit_exact(cv, orc):
         assert np.array_equal(a.label, ref[0])
 
 
-@pytest.mark.parametrize("base", [8, 40, 100, 300])
+@pytest.mark.parametrize("base", [3, 8, 12, 16, 40, 100, 300])
 def test_detect_thresholds_both_parent_paths(cv, orc, base):
-    """Dense graph, thresholds below and above DIRECT_PARENTS_MAX_T (64): the
-    bounded backward scan and the segmented max-scan give the reference's
-    labels, counters and history bit for bit."""
+    """Dense graph, every formulation of the deterministic pass: top-b lists
+    of stride 4 / 8 / 12 / 16 (thresholds <= 16), the slot sort with the
+    bounded parent scan (<= 64) and with the segmented max-scan (> 64) --
+    the reference's labels, counters and history bit for bit."""
     from paper_2108_00529_b200 import synth
     e = synth.planted_partition(600, 90000, 6, seed=9)
     g = cv.from_edge_array(e)
