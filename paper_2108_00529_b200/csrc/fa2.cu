@@ -2554,7 +2554,7 @@ struct LayoutRes {
     cudaStream_t side = nullptr, aux = nullptr, cs = nullptr;
     cudaEvent_t ev[6] = {};
     cudaGraphExec_t exec = nullptr;
-    long long key[4] = {-1, -1, -1, -1};  // what `exec` was captured for
+    long long key[5] = {-1, -1, -1, -1, -1};  // what `exec` was captured for
 };
 
 static LayoutRes &layout_res() {
@@ -2676,28 +2676,43 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                 cudaGraph_t graph = nullptr;
                 long long before = g_launches.load();
                 CVZ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+                // small layouts (< 2^16 bodies, launch-bound: C1's 121-body
+                // supergraph runs ~80 us per iteration) capture several
+                // iterations per graph -- the largest divisor of the
+                // iteration count up to 8: 82.5 -> 76.5 us/iter at C1; at C4
+                // it measured slower (476 -> 490 us), so larger layouts keep
+                // one iteration per graph.  CVZ_GRAPH_UNROLL overrides.
+                static const char *uenv = getenv("CVZ_GRAPH_UNROLL");
+                const long long umax =
+                    uenv ? std::max(1LL, atoll(uenv)) : (n < (1 << 16) ? 8LL : 1LL);
+                long long unroll = 1;
+                for (long long u = std::min(umax, (long long)P->iterations); u > 1; --u)
+                    if (P->iterations % u == 0) {
+                        unroll = u;
+                        break;
+                    }
                 bool ok = true;
                 try {
-                    one_iteration(cs, ids);
+                    for (long long u = 0; u < unroll; ++u) one_iteration(cs, ids);
                 } catch (...) {
                     ok = false;
                 }
                 cudaError_t ce = cudaStreamEndCapture(cs, &graph);
-                long long per_iter = g_launches.load() - before;
+                long long per_iter = g_launches.load() - before;  // per graph launch
                 g_launches.fetch_sub(per_iter);
                 bool ready = false;
                 // the iteration's node set is fixed by these (launch
                 // configurations may differ, which an update allows); a
                 // different shape gets a fresh instantiation instead of a
                 // failed update
-                const long long key[4] = {(long long)n, (long long)csr.nheavy > 0,
-                                          (long long)exact, (long long)ids};
-                if (lr.exec && !std::equal(key, key + 4, lr.key)) {
+                const long long key[5] = {(long long)n, (long long)csr.nheavy > 0,
+                                          (long long)exact, (long long)ids, unroll};
+                if (lr.exec && !std::equal(key, key + 5, lr.key)) {
                     cudaGraphExecDestroy(lr.exec);
                     lr.exec = nullptr;
                 }
                 if (ok && ce == cudaSuccess) {
-                    std::copy(key, key + 4, lr.key);
+                    std::copy(key, key + 5, lr.key);
                     if (lr.exec) {
                         cudaGraphExecUpdateResultInfo info;
                         if (cudaGraphExecUpdate(lr.exec, graph, &info) == cudaSuccess) {
@@ -2712,7 +2727,7 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
                         ready = true;
                 }
                 if (ready) {
-                    for (long long it = 0; it < P->iterations; ++it) {
+                    for (long long it = 0; it < P->iterations; it += unroll) {
                         CVZ_CUDA(cudaGraphLaunch(lr.exec, cs));
                         g_launches.fetch_add(per_iter);
                     }
