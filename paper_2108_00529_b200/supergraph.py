@@ -109,6 +109,7 @@ class _ContractBuffers:
 
     def __init__(self, res):
         self.res = res
+        self.stream = nat.stream()  # released (stream-ordered) where it was made
 
     def tensor(self, ptr, shape):
         T = nat.torch()
@@ -118,7 +119,7 @@ class _ContractBuffers:
 
     def __del__(self):
         try:
-            nat.call("cvz_contract_release", ctypes.byref(self.res), nat.stream())
+            nat.call("cvz_contract_release", ctypes.byref(self.res), self.stream)
         except Exception:  # interpreter shutdown: the CUDA context is gone anyway
             pass
 
