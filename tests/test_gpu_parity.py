@@ -193,6 +193,32 @@ def test_detect_interleaved_orders_bit_exact(cv, orc):
         assert np.array_equal(a.label, ref[0])
 
 
+@pytest.mark.parametrize("workers,inter,rs", [(4, "random", "contract"),
+                                              (16, "roundrobin", "contract"),
+                                              (1, "random", "restream")])
+def test_detect_orders_and_restream_bit_exact_at_c2(cv, orc, workers, inter, rs, monkeypatch):
+    """C2 (335K nodes / 926K edges): interleaved processing orders (seeded
+    make_schedule, C/community.py:164-195) and the restream round stream
+    (C/community.py:274-276) through the top-b formulation, bit-exact labels,
+    counters and per-round history.  The oracle takes the native schedule
+    (bit-exact with its Python loop, tests/test_host.py) for speed."""
+    from paper_2108_00529_b200 import synth
+    from paper_2108_00529_b200.community import make_schedule
+    monkeypatch.setattr(orc, "make_schedule", make_schedule)
+    e = synth.config_graph("C2")
+    g = cv.from_edge_array(e)
+    n, ee, deg = orc.from_edge_array(e)
+    base = orc.degree_stats(deg)[0]
+    ref = orc.detect_communities(n, ee, deg, base, 10, 3, workers=workers, interleave=inter,
+                                 round_stream=rs)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=3, workers=workers,
+                              interleave=inter, round_stream=rs)
+    assert np.array_equal(a.label, ref[0]) and np.array_equal(a.counter_degree, ref[1])
+    assert len(a.round_history) == len(ref[2])
+    for x, y in zip(a.round_history, ref[2]):
+        assert np.array_equal(x, y)
+
+
 @pytest.mark.parametrize("base", [3, 8, 12, 16, 40, 100, 300])
 def test_detect_thresholds_both_parent_paths(cv, orc, base):
     """Dense graph, every formulation of the deterministic pass: top-b lists
