@@ -1592,7 +1592,13 @@ void scoda_pass_dev(const int2 *E, long long m, long long n, long long T, int ti
             det_pass_topt(E, m, n, T, tie, d0, lab0, deg_out, lab_out, sc, s);
             return;
         }
-        if (T < 255)
+        // per-slot counters fit a byte only for non-negative seeds (a
+        // caller's negative counter stays active below zero, C/community.py
+        // :104-109, and must not wrap)
+        const bool nonneg = seeds_nonneg || !d0;
+        if (!nonneg)
+            det_pass_t<long long>(E, m, n, T, tie, d0, lab0, deg_out, lab_out, sc, s);
+        else if (T < 255)
             det_pass_t<unsigned char>(E, m, n, T, tie, d0, lab0, deg_out, lab_out, sc, s);
         else if (T < (1LL << 30))
             det_pass_t<int>(E, m, n, T, tie, d0, lab0, deg_out, lab_out, sc, s);

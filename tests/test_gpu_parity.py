@@ -134,6 +134,30 @@ def test_scoda_pass_golden(cv):
         assert np.array_equal(lab, d[f"p{i}_lab"]), i
 
 
+@pytest.mark.parametrize("thr", [1, 5, 8, 16, 20])
+def test_scoda_pass_arbitrary_counters_vs_oracle(cv, orc, thr):
+    """_scoda_pass with caller-supplied counters (C/community.py:98-120):
+    random seeds in [-3, thr + 3] -- negative ones force the slot-sort
+    formulation, non-negative ones take the top-b lists (thresholds <= 16) --
+    with self-loops, duplicates and an interleaved order; counters and raw
+    labels bit-exact vs the sequential oracle."""
+    from paper_2108_00529_b200.community import _scoda_pass
+    rng = np.random.default_rng(thr)
+    n = 3000
+    e = rng.integers(0, n, size=(40000, 2))
+    e[::41, 1] = e[::41, 0]
+    order = rng.permutation(len(e))
+    for lo in (-3, 0):
+        deg0 = rng.integers(lo, thr + 4, size=n).astype(np.int64)
+        lab0 = rng.permutation(n).astype(np.int64)
+        deg_g, lab_g = deg0.copy(), lab0.copy()
+        _scoda_pass(e, order, thr, 0, deg_g, lab_g)
+        deg_o, lab_o = deg0.copy(), lab0.copy()
+        orc.scoda_pass(e, order, thr, 0, deg_o, lab_o)
+        assert np.array_equal(deg_g, deg_o), lo
+        assert np.array_equal(lab_g, lab_o), lo
+
+
 def test_resolve_golden(cv, orc):
     from paper_2108_00529_b200.community import _resolve_labels
     d = golden("community")
