@@ -148,14 +148,15 @@ def test_scoda_pass_arbitrary_counters_vs_oracle(cv, orc, thr):
     e[::41, 1] = e[::41, 0]
     order = rng.permutation(len(e))
     for lo in (-3, 0):
-        deg0 = rng.integers(lo, thr + 4, size=n).astype(np.int64)
-        lab0 = rng.permutation(n).astype(np.int64)
-        deg_g, lab_g = deg0.copy(), lab0.copy()
-        _scoda_pass(e, order, thr, 0, deg_g, lab_g)
-        deg_o, lab_o = deg0.copy(), lab0.copy()
-        orc.scoda_pass(e, order, thr, 0, deg_o, lab_o)
-        assert np.array_equal(deg_g, deg_o), lo
-        assert np.array_equal(lab_g, lab_o), lo
+        for tie in (0, 1, 2):
+            deg0 = rng.integers(lo, thr + 4, size=n).astype(np.int64)
+            lab0 = rng.permutation(n).astype(np.int64)
+            deg_g, lab_g = deg0.copy(), lab0.copy()
+            _scoda_pass(e, order, thr, tie, deg_g, lab_g)
+            deg_o, lab_o = deg0.copy(), lab0.copy()
+            orc.scoda_pass(e, order, thr, tie, deg_o, lab_o)
+            assert np.array_equal(deg_g, deg_o), (lo, tie)
+            assert np.array_equal(lab_g, lab_o), (lo, tie)
 
 
 def test_resolve_golden(cv, orc):
