@@ -134,6 +134,38 @@ def test_scoda_pass_golden(cv):
         assert np.array_equal(lab, d[f"p{i}_lab"]), i
 
 
+def _shape_graphs():
+    rng = np.random.default_rng(5)
+    star = np.stack([np.zeros(300, np.int64), np.arange(1, 301)], 1)
+    path = np.stack([np.arange(999), np.arange(1, 1000)], 1)
+    kn = np.array([(i, j) for i in range(30) for j in range(30) if i < j] * 3)
+    kn = kn[rng.permutation(len(kn))]
+    dup = np.repeat(rng.integers(0, 50, (200, 2)), 7, axis=0)
+    return {"one_edge": (np.array([[0, 1]]), None), "star": (star, None),
+            "path": (path, None), "complete_x3": (kn, None), "dup_heavy": (dup, 80),
+            "isolated_tail": (rng.integers(0, 500, (3000, 2)), 650)}
+
+
+@pytest.mark.parametrize("name", list(_shape_graphs()))
+@pytest.mark.parametrize("base", [1, 2, 5, 16])
+def test_detect_graph_shapes_vs_oracle(cv, orc, name, base):
+    """Degenerate shapes through every round of the deterministic pass (one
+    edge, a 300-leaf star, a 1000-node path, a triple complete graph, heavy
+    duplicate edges, isolated trailing nodes): labels, counters and per-round
+    history bit-exact vs the oracle."""
+    e, nc = _shape_graphs()[name]
+    g = cv.from_edge_array(e, node_count=nc)
+    n, ee, deg = orc.from_edge_array(e, node_count=nc)
+    if len(ee) == 0:
+        pytest.skip("only self-loops")
+    ref = orc.detect_communities(n, ee, deg, base, 10, 0, workers=1)
+    a = cv.detect_communities(g, cv.ThresholdSchedule(base=base), seed=0, workers=1)
+    assert np.array_equal(a.label, ref[0]) and np.array_equal(a.counter_degree, ref[1])
+    assert len(a.round_history) == len(ref[2])
+    for x, y in zip(a.round_history, ref[2]):
+        assert np.array_equal(x, y)
+
+
 @pytest.mark.parametrize("thr", [1, 5, 8, 16, 20])
 def test_scoda_pass_arbitrary_counters_vs_oracle(cv, orc, thr):
     """_scoda_pass with caller-supplied counters (C/community.py:98-120):
