@@ -557,6 +557,42 @@ def test_contract_at_scale(cv, orc):
     assert np.all(sg.edges[:, 0] < sg.edges[:, 1])
 
 
+@pytest.mark.parametrize("kind", ["one_community", "wide_int64_labels", "singletons", "tiny_sketch"])
+def test_contract_label_shapes_vs_oracle(cv, orc, kind):
+    """contract() on label shapes the detect output never produces: one
+    community (no superedges), arbitrary int64 labels including negatives
+    (the (label, node) radix-sort path for dense ids), every node its own
+    community, and a 1 x 1 sketch -- all arrays bit-exact vs the oracle."""
+    rng = np.random.default_rng(12)
+    n = 2000
+    e = rng.integers(0, n, (12000, 2))
+    g = cv.from_edge_array(e, node_count=n)
+    n_, ee, deg = orc.from_edge_array(e, node_count=n)
+    rows, cols = 3, 700
+    if kind == "one_community":
+        lab = np.full(n, 17, np.int64)
+    elif kind == "wide_int64_labels":
+        pool = rng.integers(-10**12, 10**12, 90)
+        lab = pool[rng.integers(0, 90, n)]
+    elif kind == "singletons":
+        lab = rng.permutation(n).astype(np.int64) * 3
+    else:
+        lab = rng.integers(0, 40, n).astype(np.int64)
+        rows, cols = 1, 1
+    s = cv.sketch_new(rows, cols, seed=4)
+    cv.accumulate_sizes(s, lab, g.degree)
+    sg = cv.contract(g, lab, s)
+    A, B = orc.sketch_params(rows, 4)
+    t = np.zeros((rows, cols), np.int64)
+    orc.sketch_add_many(t, A, B, lab, deg)
+    assert np.array_equal(s.table, t)
+    k, se, w, mult, comm = orc.contract(ee, lab, t, A, B)
+    assert sg.node_count == k and sg.edge_count == len(se)
+    assert np.array_equal(sg.edges.reshape(-1, 2), se.reshape(-1, 2))
+    assert np.array_equal(sg.multiplicity, mult) and np.array_equal(sg.weight, w)
+    assert np.array_equal(sg.community_id, comm)
+
+
 def test_contract_results_are_views_released_with_the_supergraph(cv, monkeypatch):
     """contract() hands out zero-copy views of the library's result buffers;
     they stay valid while any view is alive and are released once, when the
