@@ -848,6 +848,50 @@ def test_layout_step_teacher_forced(cv, orc):
         assert np.max(np.abs(new_g - new_r)) <= 1e-9 * diam
 
 
+@pytest.mark.parametrize("case", ["two", "three_collinear", "coincident_pair", "all_coincident",
+                                  "far_apart", "weighted_forms"])
+def test_layout_tiny_and_degenerate_vs_oracle(cv, orc, case):
+    """Layouts of 2-12 bodies with collinear, coincident and extreme start
+    positions, both speed / attraction forms and theta in {0, 0.5}: every
+    iteration's positions within 1e-7 of the oracle's diameter."""
+    from paper_2108_00529_b200.supergraph import SuperGraph
+    rng = np.random.default_rng(3)
+    params = {}
+    if case == "two":
+        pos, edges, w = np.array([[0.0, 0.0], [1.0, 0.5]]), np.array([[0, 1]]), [5]
+    elif case == "three_collinear":
+        pos = np.array([[0.0, 0.0], [1.0, 0.0], [2.0, 0.0]])
+        edges, w = np.array([[0, 1], [1, 2]]), [1, 2]
+    elif case == "coincident_pair":
+        pos = np.array([[0.3, 0.3], [0.3, 0.3], [2.0, -1.0], [-1.0, 2.0]])
+        edges, w = np.array([[0, 2], [1, 3], [2, 3]]), [1, 1, 4]
+    elif case == "all_coincident":
+        pos = np.zeros((6, 2))
+        edges, w = np.array([[0, 1], [2, 3], [4, 5], [0, 5]]), [1, 2, 3, 4]
+    elif case == "far_apart":
+        pos = rng.uniform(-1e6, 1e6, (12, 2))
+        edges, w = np.array([[i, (i + 1) % 12] for i in range(12)]), list(range(1, 13))
+    else:
+        pos = rng.uniform(-3, 3, (10, 2))
+        edges, w = np.array([[i, j] for i in range(10) for j in range(i + 1, 10) if (i + j) % 3 == 0]), None
+        params = dict(speed_form="sum", attraction_form="reversed")
+    k = len(pos)
+    w = np.asarray(w if w is not None else np.arange(1, len(edges) + 1), np.int64)
+    weight = rng.integers(1, 9, k).astype(np.int64)
+    sg = SuperGraph(node_count=k, community_id=np.arange(k), weight=weight,
+                    edges=edges, multiplicity=w)
+    mass, ew = orc.masses_supergraph(weight, w)
+    for theta in (0.0, 0.5):
+        for iters in (1, 7):
+            res = cv.layout(sg, cv.LayoutParams(iterations=iters, theta=theta, **params),
+                            positions=pos)
+            ref, hist = orc.layout(k, mass, edges, ew, iterations=iters, positions=pos,
+                                   theta=theta, **params)
+            diam = max(np.hypot(*(ref.max(0) - ref.min(0))), 1e-12)
+            assert np.max(np.abs(res.positions - ref)) <= 1e-7 * diam, (theta, iters)
+            np.testing.assert_allclose(res.displacement, hist, rtol=1e-7, atol=1e-12)
+
+
 def test_reference_layout_kats(cv):
     # /root/reference/pkg/tests/test_layout.py:47-187 + criterion 6
     f = cv.repulsion_forces(np.array([[0.0, 0.0], [2.0, 0.0]]), np.ones(2), 80.0, theta=0.0)
