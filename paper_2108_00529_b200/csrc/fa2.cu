@@ -1394,22 +1394,34 @@ __global__ void classify_rows_kernel(const long long *__restrict__ rowptr, int l
     }
 }
 
+// Rows longer than HEAVY_SPLIT half-edges (R-MAT hubs: up to millions) are
+// cut into chunks of HEAVY_SPLIT, each summed by its own warp into `part`;
+// springs_combine_kernel adds a row's chunks in chunk order (deterministic).
+// A warp per whole row left one warp streaming a hub's million half-edges
+// while the rest of the GPU idled (R-MAT-26: 42.7 ms of a 140 ms iteration).
+constexpr long long HEAVY_SPLIT = 65536;
+
 template <bool UNIT>
 __global__ void __launch_bounds__(FB) springs_heavy_kernel(
     const double2 *__restrict__ pos, const long long *__restrict__ rowptr,
     const int *__restrict__ col, const double *__restrict__ cw, double unit,
     const int *__restrict__ heavy, int nheavy, double2 *__restrict__ hsum,
-    const StepScalars *__restrict__ sc) {
+    const StepScalars *__restrict__ sc, const int *__restrict__ ch_h,
+    const long long *__restrict__ ch_lo, int nchunk, double2 *__restrict__ part) {
     griddep_wait();
     if (sc && sc->bad) return;
     const int lane = lane_id();
-    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nheavy;
+    // work items: heavy rows (ch_h == nullptr) or chunks of heavy rows
+    const int items = ch_h ? nchunk : nheavy;
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items;
          w += (gridDim.x * blockDim.x) >> 5) {
-        int u = heavy[w];
+        const int h = ch_h ? ch_h[w] : w;
+        const int u = heavy[h];
         double2 pu = pos[u];
         double fx = 0.0, fy = 0.0;
-        const long long end = rowptr[u + 1];
-        long long j = rowptr[u] + lane;
+        const long long r0 = ch_h ? ch_lo[w] : rowptr[u];
+        const long long end = ch_h ? min(rowptr[u + 1], r0 + HEAVY_SPLIT) : rowptr[u + 1];
+        long long j = r0 + lane;
         // four lane-strided terms per step: loads batched ahead of the
         // (unchanged, in-order) accumulation, so the col -> pos chains overlap
         for (; j + 96 < end; j += 128) {
@@ -1438,7 +1450,45 @@ __global__ void __launch_bounds__(FB) springs_heavy_kernel(
             fx = add(fx, __shfl_xor_sync(0xffffffffu, fx, o));
             fy = add(fy, __shfl_xor_sync(0xffffffffu, fy, o));
         }
-        if (lane == 0) hsum[w] = make_double2(fx, fy);
+        if (lane == 0) (ch_h ? part : hsum)[w] = make_double2(fx, fy);
+    }
+}
+
+// hsum[h] = sum of row h's chunk partials in chunk order
+__global__ void springs_combine_kernel(const int *__restrict__ choff, int nheavy,
+                                       const double2 *__restrict__ part,
+                                       double2 *__restrict__ hsum) {
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < nheavy; h += gridDim.x * blockDim.x) {
+        double fx = 0.0, fy = 0.0;
+        for (int q = choff[h]; q < choff[h + 1]; ++q) {
+            fx = add(fx, part[q].x);
+            fy = add(fy, part[q].y);
+        }
+        hsum[h] = make_double2(fx, fy);
+    }
+}
+
+// chunk list of the heavy rows: nchunks per row (for the scan), then the fill
+__global__ void heavy_chunks_count_kernel(const long long *__restrict__ rowptr,
+                                          const int *__restrict__ heavy, int nheavy,
+                                          int *__restrict__ nch) {
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < nheavy; h += gridDim.x * blockDim.x) {
+        const int u = heavy[h];
+        const long long len = rowptr[u + 1] - rowptr[u];
+        nch[h] = (int)((len + HEAVY_SPLIT - 1) / HEAVY_SPLIT);
+    }
+}
+
+__global__ void heavy_chunks_fill_kernel(const long long *__restrict__ rowptr,
+                                         const int *__restrict__ heavy, int nheavy,
+                                         const int *__restrict__ choff, int *__restrict__ ch_h,
+                                         long long *__restrict__ ch_lo) {
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < nheavy; h += gridDim.x * blockDim.x) {
+        const long long r0 = rowptr[heavy[h]];
+        for (int q = choff[h]; q < choff[h + 1]; ++q) {
+            ch_h[q] = h;
+            ch_lo[q] = r0 + (long long)(q - choff[h]) * HEAVY_SPLIT;
+        }
     }
 }
 
@@ -2183,6 +2233,11 @@ struct Csr {
     int *heavy;     // [nheavy] heavy row ids
     int nheavy = 0;
     double2 *hsum;  // [nheavy] warp-summed springs
+    // rows beyond HEAVY_SPLIT half-edges: chunk list (nchunk == 0: none)
+    int nchunk = 0;
+    int *ch_h = nullptr, *choff = nullptr;
+    long long *ch_lo = nullptr;
+    double2 *part = nullptr;
 };
 
 // CSR over the rows [row_lo, row_hi) (row_hi < 0: all n).  A node-sharded
@@ -2269,6 +2324,30 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
     CVZ_CUDA(cudaStreamSynchronize(s));
     c.nheavy = (int)nh_h;
     c.hsum = sc.alloc<double2>(c.nheavy > 0 ? c.nheavy : 1);
+    if (c.nheavy > 0) {
+        int *nch = tmp_sc.alloc<int>(c.nheavy + 1);
+        c.choff = sc.alloc<int>(c.nheavy + 1);
+        CVZ_CUDA(cudaMemsetAsync(nch + c.nheavy, 0, sizeof(int), s));
+        CVZ_LAUNCH(heavy_chunks_count_kernel, grid_for(c.nheavy, FB, 1, 8), FB, 0, s, c.rowptr,
+                   c.heavy, c.nheavy, nch);
+        size_t tb = 0;
+        CVZ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, nch, c.choff, c.nheavy + 1, s));
+        void *tmp = tmp_sc.alloc<char>(tb);
+        CVZ_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nch, c.choff, c.nheavy + 1, s));
+        count_launches(2);
+        int total = 0;
+        CVZ_CUDA(cudaMemcpyAsync(&total, c.choff + c.nheavy, sizeof(int), cudaMemcpyDeviceToHost,
+                                 s));
+        CVZ_CUDA(cudaStreamSynchronize(s));
+        if (total > c.nheavy) {  // some row is longer than HEAVY_SPLIT
+            c.nchunk = total;
+            c.ch_h = sc.alloc<int>(total);
+            c.ch_lo = sc.alloc<long long>(total);
+            c.part = sc.alloc<double2>(total);
+            CVZ_LAUNCH(heavy_chunks_fill_kernel, grid_for(c.nheavy, FB, 1, 8), FB, 0, s, c.rowptr,
+                       c.heavy, c.nheavy, c.choff, c.ch_h, c.ch_lo);
+        }
+    }
     return c;
 }
 
@@ -2288,14 +2367,18 @@ static void springs(const double2 *pos, const Csr &c, const StepScalars *sc, int
     static const char *cenv = getenv("CVZ_SPRINGS_CAP");
     const int cap = cenv ? atoi(cenv) : (hi - lo < (1 << 21) ? 1 : 0);
     if (c.nheavy > 0) {
-        unsigned hb = blocks_for((long long)c.nheavy * 32, FB);
+        const int items = c.nchunk > 0 ? c.nchunk : c.nheavy;
+        unsigned hb = blocks_for((long long)items * 32, FB);
         if (cap > 0) hb = std::min<unsigned>(hb, (unsigned)(cap * num_sms()));
         if (c.w)
-            CVZ_LAUNCH(springs_heavy_kernel<false>, hb, FB, 0,
-                       s, pos, c.rowptr, c.col, c.w, c.unit, c.heavy, c.nheavy, c.hsum, sc);
+            CVZ_LAUNCH(springs_heavy_kernel<false>, hb, FB, 0, s, pos, c.rowptr, c.col, c.w,
+                       c.unit, c.heavy, c.nheavy, c.hsum, sc, c.ch_h, c.ch_lo, c.nchunk, c.part);
         else
-            CVZ_LAUNCH(springs_heavy_kernel<true>, hb, FB, 0,
-                       s, pos, c.rowptr, c.col, c.w, c.unit, c.heavy, c.nheavy, c.hsum, sc);
+            CVZ_LAUNCH(springs_heavy_kernel<true>, hb, FB, 0, s, pos, c.rowptr, c.col, c.w,
+                       c.unit, c.heavy, c.nheavy, c.hsum, sc, c.ch_h, c.ch_lo, c.nchunk, c.part);
+        if (c.nchunk > 0)
+            CVZ_LAUNCH(springs_combine_kernel, grid_for(c.nheavy, FB, 1, 8), FB, 0, s, c.choff,
+                       c.nheavy, c.part, c.hsum);
     }
     if (hi > lo) {
         const unsigned lb = blocks_for(hi - lo, FB);

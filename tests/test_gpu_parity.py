@@ -848,6 +848,28 @@ def test_layout_step_teacher_forced(cv, orc):
         assert np.max(np.abs(new_g - new_r)) <= 1e-9 * diam
 
 
+def test_layout_giant_hub_rows_vs_oracle(cv, orc):
+    """Full-graph layout where two hubs have 150K / 70K half-edges: their
+    spring rows are split into 64K-half-edge chunks summed by separate warps
+    and combined in chunk order (fa2.cu HEAVY_SPLIT); positions within 1e-7
+    of the diameter of the oracle's after 3 iterations."""
+    rng = np.random.default_rng(21)
+    n = 160_000
+    hub_a = np.stack([np.zeros(150_000, np.int64), rng.integers(1, n, 150_000)], 1)
+    hub_b = np.stack([np.ones(70_000, np.int64), rng.integers(2, n, 70_000)], 1)
+    rest = rng.integers(2, n, (60_000, 2))
+    e = np.concatenate([hub_a, hub_b, rest])
+    e = e[rng.permutation(len(e))]
+    g = cv.from_edge_array(e, node_count=n)
+    n_, ee, deg = orc.from_edge_array(e, node_count=n)
+    res = cv.layout(g, cv.LayoutParams(iterations=3))
+    mass, ew = orc.masses_graph(deg, len(ee))
+    ref, hist = orc.layout(n, mass, ee, ew, iterations=3)
+    diam = np.hypot(*(ref.max(0) - ref.min(0)))
+    assert np.max(np.abs(res.positions - ref)) <= 1e-7 * diam
+    np.testing.assert_allclose(res.displacement, hist, rtol=1e-7, atol=1e-12)
+
+
 @pytest.mark.parametrize("case", ["two", "three_collinear", "coincident_pair", "all_coincident",
                                   "far_apart", "weighted_forms"])
 def test_layout_tiny_and_degenerate_vs_oracle(cv, orc, case):
