@@ -848,6 +848,22 @@ def test_layout_step_teacher_forced(cv, orc):
         assert np.max(np.abs(new_g - new_r)) <= 1e-9 * diam
 
 
+def test_full_graph_layout_c3_vs_oracle(cv, orc):
+    """C3's full graph (685K bodies: beyond the cooperative tree-key sort's
+    resident tiles, so the CUB key sort and the large-tree paths run); 2
+    iterations within 1e-7 of the diameter of the oracle's."""
+    from paper_2108_00529_b200 import synth
+    e = synth.config_graph("C3")
+    g = cv.from_edge_array(e)
+    n, ee, deg = orc.from_edge_array(e)
+    res = cv.layout(g, cv.LayoutParams(iterations=2))
+    mass, ew = orc.masses_graph(deg, len(ee))
+    ref, hist = orc.layout(n, mass, ee, ew, iterations=2)
+    diam = np.hypot(*(ref.max(0) - ref.min(0)))
+    assert np.max(np.abs(res.positions - ref)) <= 1e-7 * diam
+    np.testing.assert_allclose(res.displacement, hist, rtol=1e-7, atol=1e-12)
+
+
 def test_layout_giant_hub_rows_vs_oracle(cv, orc):
     """Full-graph layout where two hubs have 150K / 70K half-edges: their
     spring rows are split into 64K-half-edge chunks summed by separate warps
