@@ -45,6 +45,12 @@ int cvz_version(void);
 const char *cvz_last_error(void);
 /* Number of kernels this library has launched so far (process-wide).     */
 long long cvz_launch_count(void);
+/* Copy bytes (<= 256) of device memory to host memory after all work queued
+ * on `stream`, without the copy engines (a one-CTA kernel writes mapped
+ * pinned memory): small control reads (counts, flags) do not queue behind a
+ * bulk transfer in flight on another stream.  No reference counterpart
+ * (numpy scalars are host values). */
+int cvz_read_small(void *host, const void *dev, int64_t bytes, void *stream);
 
 /* Per-kernel device timing.  Between begin and end every library kernel
  * (and every CUB primitive, by region name) launched on a stream that is not

@@ -42,6 +42,7 @@ SIGNATURES = {
     "cvz_version": [],
     "cvz_last_error": [],
     "cvz_launch_count": [],
+    "cvz_read_small": [_P, _P, _I64, _P],
     "cvz_profile_begin": [],
     "cvz_profile_end": [],
     "cvz_profile_report": [],
@@ -208,6 +209,21 @@ def to_dev(a, dtype):
         arr = np.ascontiguousarray(np.asarray(a))
         t = T.from_numpy(arr).to(device=device(), dtype=dtype, non_blocking=False)
     return t.contiguous()
+
+
+def read_ints(t):
+    """Small int64 CUDA tensor (<= 32 values) -> list of Python ints after
+    the current stream's work, without the copy engines (cvz_read_small):
+    a control read does not wait behind a bulk prefetch on another stream."""
+    import numpy as np
+    t = t.detach()
+    T = torch()
+    if not t.is_cuda:
+        return [int(v) for v in t.tolist()]
+    t = t.to(T.int64).contiguous()
+    out = np.empty(int(t.numel()), dtype=np.int64)
+    call("cvz_read_small", out.ctypes.data, ptr(t), out.nbytes, stream())
+    return [int(v) for v in out]
 
 
 def to_host(t):

@@ -205,6 +205,13 @@ struct DeviceCache {
 
 void init_pool_once();
 
+// Small device -> host readback (counts, flags) that bypasses the copy
+// engines: a one-CTA kernel stores the bytes into mapped pinned memory and
+// the stream is synchronised.  A cudaMemcpyAsync of four bytes queues behind
+// any bulk copy in flight on the same engine (the label prefetch: ~0.5 ms of
+// D2H at C4) and would stall the caller that long.  bytes <= 256.
+void read_small(void *host, const void *dev, size_t bytes, cudaStream_t s);
+
 // Stream-ordered scratch arena: every allocation is released (stream-ordered)
 // when the arena goes out of scope, so kernels queued before the free still
 // see valid memory.

@@ -252,8 +252,7 @@ void superedges(const int2 *e, long long m, const int *dense, long long k, int B
         CVZ_LAUNCH(cross_keys_kernel<K>, grid_for(m, 256, 1, 16), 256, 0, s, e, m, dense, B, keys,
                    cnt);
     unsigned long long hc = 0;
-    CVZ_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
-    CVZ_CUDA(cudaStreamSynchronize(s));
+    read_small(&hc, cnt, sizeof(hc), s);
     long long c = (long long)hc;
     res->se = 0;
     if (c == 0) {
@@ -284,8 +283,7 @@ void superedges(const int2 *e, long long m, const int *dense, long long k, int B
     }
     count_launches(2);
     long long hr = 0;
-    CVZ_CUDA(cudaMemcpyAsync(&hr, nruns, sizeof(hr), cudaMemcpyDeviceToHost, s));
-    CVZ_CUDA(cudaStreamSynchronize(s));
+    read_small(&hr, nruns, sizeof(hr), s);
     res->se = hr;
     res->se_edges = device_alloc<int64_t>(2 * hr, s);
     res->mult = device_alloc<int64_t>(hr, s);
@@ -305,8 +303,7 @@ long long dense_ids(const int64_t *labels, int64_t n, int *dense, int64_t **comm
     auto *lab = reinterpret_cast<const long long *>(labels);
     CVZ_LAUNCH(minmax_kernel, grid_for(n, 256, 4, 4), 256, 0, s, lab, (long long)n, mm, mm + 1);
     long long h[2];
-    CVZ_CUDA(cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CVZ_CUDA(cudaStreamSynchronize(s));
+    read_small(h, mm, sizeof(h), s);
     long long k;
     long long range = h[1] + 1;
     if (h[0] >= 0 && h[1] < (1LL << 31) && range <= std::max<long long>(4 * n, 1 << 20)) {
@@ -324,9 +321,8 @@ long long dense_ids(const int64_t *labels, int64_t n, int *dense, int64_t **comm
         }
         count_launches(2);
         int last[2];
-        CVZ_CUDA(cudaMemcpyAsync(&last[0], rank + range - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaMemcpyAsync(&last[1], present + range - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(&last[0], rank + range - 1, sizeof(int), s);
+        read_small(&last[1], present + range - 1, sizeof(int), s);
         k = (long long)last[0] + last[1];
         int64_t *comm = device_alloc<int64_t>(k, s);
         CVZ_LAUNCH(comm_from_present_kernel, grid_for(range, 256, 1, 8), 256, 0, s, present, rank,
@@ -355,8 +351,7 @@ long long dense_ids(const int64_t *labels, int64_t n, int *dense, int64_t **comm
         CVZ_CUDA(cub::DeviceScan::InclusiveSum(tmp2, tb2, flags, incl, (int)n, s));
         count_launches(2);
         int hk = 0;
-        CVZ_CUDA(cudaMemcpyAsync(&hk, incl + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(&hk, incl + n - 1, sizeof(int), s);
         k = hk;
         int64_t *comm = device_alloc<int64_t>(k, s);
         CVZ_LAUNCH(dense_from_sorted_kernel, grid_for(n, 256, 1, 8), 256, 0, s, sorted, node, incl,

@@ -2181,8 +2181,7 @@ struct Tree {
     }
     bool jitter_seen(cudaStream_t s) {
         unsigned h = 0;
-        CVZ_CUDA(cudaMemcpyAsync(&h, jflag, sizeof(h), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(&h, jflag, sizeof(h), s);
         return h != 0;
     }
 };
@@ -2278,8 +2277,7 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
                                            cnt_d, 2 * m, pred, s));
             count_launches(2);
         }
-        CVZ_CUDA(cudaMemcpyAsync(&nh, cnt_d, sizeof(nh), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(&nh, cnt_d, sizeof(nh), s);
         val = sel;
         key = tmp_sc.alloc<unsigned>(nh > 0 ? nh : 1);
         if (nh > 0)
@@ -2320,8 +2318,7 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
     CVZ_LAUNCH(classify_rows_kernel, grid_for(rows, FB, 1, 8), FB, 0, s, c.rowptr,
                (int)row_lo, (int)row_hi, c.hidx, c.heavy, nh_d);
     unsigned nh_h = 0;
-    CVZ_CUDA(cudaMemcpyAsync(&nh_h, nh_d, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-    CVZ_CUDA(cudaStreamSynchronize(s));
+    read_small(&nh_h, nh_d, sizeof(unsigned), s);
     c.nheavy = (int)nh_h;
     c.hsum = sc.alloc<double2>(c.nheavy > 0 ? c.nheavy : 1);
     if (c.nheavy > 0) {
@@ -2336,9 +2333,7 @@ static Csr build_csr(const int2 *e, long long m, long long n, const double *weig
         CVZ_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nch, c.choff, c.nheavy + 1, s));
         count_launches(2);
         int total = 0;
-        CVZ_CUDA(cudaMemcpyAsync(&total, c.choff + c.nheavy, sizeof(int), cudaMemcpyDeviceToHost,
-                                 s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(&total, c.choff + c.nheavy, sizeof(int), s);
         if (total > c.nheavy) {  // some row is longer than HEAVY_SPLIT
             c.nchunk = total;
             c.ch_h = sc.alloc<int>(total);
@@ -2589,10 +2584,9 @@ int cvz_fa2_shard_finish(cvz_fa2_shard *h, double *speed_out, int64_t *bad_itera
         cudaStream_t s = as_stream(stream);
         StepScalars out;
         unsigned jf = 0;
-        CVZ_CUDA(cudaMemcpyAsync(&out, h->scal, sizeof(out), cudaMemcpyDeviceToHost, s));
+        read_small(&out, h->scal, sizeof(out), s);
         if (!h->exact)
-            CVZ_CUDA(cudaMemcpyAsync(&jf, h->tree.jflag, sizeof(jf), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+            read_small(&jf, h->tree.jflag, sizeof(jf), s);
         if (speed_out) *speed_out = out.speed;
         *bad_iteration = out.bad;
         *jitter_seen = jf != 0;
@@ -2841,15 +2835,14 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
             run_all(true);
         }
         StepScalars out;
-        CVZ_CUDA(cudaMemcpyAsync(&out, scal, sizeof(out), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
-        CVZ_CUDA(cudaMemcpyAsync(speed, &out.speed, sizeof(double), cudaMemcpyHostToDevice, s));
+        read_small(&out, scal, sizeof(out), s);
+        CVZ_CUDA(cudaMemcpyAsync(speed, &scal->speed, sizeof(double), cudaMemcpyDeviceToDevice,
+                                 s));
         *bad_iteration = out.bad;
         if (out.bad)
             throw Error(CVZ_ERR_LAYOUT, "non-finite positions at iteration " +
                                             std::to_string(out.bad) +
                                             "; reduce speed or check input weights");
-        CVZ_CUDA(cudaStreamSynchronize(s));
     });
 }
 

@@ -11,6 +11,8 @@
 #include <mutex>
 #include <sstream>
 
+#include <cstring>
+
 #include "common.cuh"
 
 namespace cvz {
@@ -61,6 +63,31 @@ void init_pool_once() {  // per device: the release threshold is a pool attribut
         }
         return 1;
     });
+}
+
+namespace {
+__global__ void read_small_kernel(const unsigned char *__restrict__ src,
+                                  volatile unsigned char *__restrict__ dst, int bytes) {
+    for (int i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+
+void read_small(void *host, const void *dev, size_t bytes, cudaStream_t s) {
+    constexpr size_t kSlot = 256;
+    CVZ_REQUIRE(bytes <= kSlot, CVZ_ERR_VALUE, "read_small: at most 256 bytes");
+    // one mapped pinned slot per host thread (portable: any device can
+    // write it through UVA); the synchronise below serialises its reuse
+    static thread_local unsigned char *slot = nullptr;
+    if (!slot) {
+        void *p = nullptr;
+        CVZ_CUDA(cudaHostAlloc(&p, kSlot, cudaHostAllocMapped | cudaHostAllocPortable));
+        slot = static_cast<unsigned char *>(p);
+    }
+    if (bytes == 0) return;
+    CVZ_LAUNCH(read_small_kernel, 1, 32, 0, s, static_cast<const unsigned char *>(dev), slot,
+               (int)bytes);
+    CVZ_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(host, slot, bytes);
 }
 
 namespace {
@@ -367,8 +394,7 @@ void degree_stats(const int64_t *degree, int64_t n, int64_t *out3, cudaStream_t 
                (long long)n, acc, acc + 1);
     // bins sized by the max degree: read it back (tiny sync, host API is sync)
     unsigned long long mx = 0;
-    CVZ_CUDA(cudaMemcpyAsync(&mx, acc + 1, sizeof(mx), cudaMemcpyDeviceToHost, s));
-    CVZ_CUDA(cudaStreamSynchronize(s));
+    read_small(&mx, acc + 1, sizeof(mx), s);
     long long nbins = (long long)mx + 1;
     auto *hist = sc.alloc<unsigned int>(nbins > SMEM_BINS ? nbins : SMEM_BINS);
     CVZ_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned) * (nbins > SMEM_BINS ? nbins : SMEM_BINS), s));
@@ -388,6 +414,14 @@ extern "C" {
 int cvz_version(void) { return 1; }
 const char *cvz_last_error(void) { return t_last_error.c_str(); }
 long long cvz_launch_count(void) { return g_launches.load(); }
+
+int cvz_read_small(void *host, const void *dev, int64_t bytes, void *stream) {
+    return guard([&] {
+        CVZ_REQUIRE(bytes >= 0 && bytes <= 256, CVZ_ERR_VALUE, "read_small: 0..256 bytes");
+        CVZ_REQUIRE(host && (dev || bytes == 0), CVZ_ERR_VALUE, "null pointer");
+        read_small(host, dev, (size_t)bytes, as_stream(stream));
+    });
+}
 
 int cvz_profile_begin(void) {
     return guard([&] {
@@ -438,8 +472,7 @@ int cvz_edges_compact(const void *edges, int in_is_int32, int64_t m, int32_t *ed
         edges_compact(edges, in_is_int32 != 0, m, edges_out, d_m_out, d_max_id, bad, s);
         if (check_range) {
             int hbad = 0;
-            CVZ_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-            CVZ_CUDA(cudaStreamSynchronize(s));
+            read_small(&hbad, bad, sizeof(int), s);
             CVZ_REQUIRE(!hbad, CVZ_ERR_RANGE, "node ids must lie in [0, 2^31)");
         }
     });

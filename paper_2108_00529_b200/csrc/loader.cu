@@ -102,8 +102,7 @@ int cvz_first_seen_remap(const int64_t *ext, int64_t count, int32_t *dense, int6
         CVZ_LAUNCH(minmax_i64_kernel, grid_for(count, RB, 4, 4), RB, 0, s, x, (long long)count,
                    mm);
         unsigned long long hm[2];
-        CVZ_CUDA(cudaMemcpyAsync(hm, mm, sizeof(hm), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(hm, mm, sizeof(hm), s);
         unsigned long long range = hm[1] - hm[0];
         int bits = 1;
         while (bits < 64 && (range >> bits) != 0) ++bits;
@@ -142,9 +141,8 @@ int cvz_first_seen_remap(const int64_t *ext, int64_t count, int32_t *dense, int6
         CVZ_LAUNCH(dense_ids_kernel, grid_for(count, RB, 1, 8), RB, 0, s, sval, hidx, rank,
                    (long long)count, reinterpret_cast<int *>(dense));
         unsigned tail[2];
-        CVZ_CUDA(cudaMemcpyAsync(&tail[0], rank + count - 1, 4, cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaMemcpyAsync(&tail[1], first + count - 1, 4, cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(&tail[0], rank + count - 1, 4, s);
+        read_small(&tail[1], first + count - 1, 4, s);
         *n_out = (int64_t)tail[0] + tail[1];
     });
 }

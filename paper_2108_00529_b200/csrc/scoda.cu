@@ -1425,8 +1425,7 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
             CVZ_LAUNCH(slot_keys_kernel, tiles, TB, 0, s, E, m, d0p, T, keys, vals,
                        LookbackState{status, ctr}, dcount, tiles);
             unsigned long long hns = 0;
-            CVZ_CUDA(cudaMemcpyAsync(&hns, dcount, sizeof(hns), cudaMemcpyDeviceToHost, s));
-            CVZ_CUDA(cudaStreamSynchronize(s));
+            read_small(&hns, dcount, sizeof(hns), s);
             ns = (long long)hns;
         }
         // 2. stable sort by node: each node's slots in stream order
@@ -1490,9 +1489,7 @@ static void det_pass_t(const int2 *E, long long m, long long n, long long T, int
         CVZ_COOP(events_coop_kernel, CB, s, wa, wb, cnt, R, origin, ptr);
         if (getenv("CVZ_DEBUG_RESOLVE")) {  // development aid: event worklist per sweep
             std::vector<unsigned> h(R + 1);
-            CVZ_CUDA(cudaMemcpyAsync(h.data(), cnt, (R + 1) * sizeof(unsigned),
-                                     cudaMemcpyDeviceToHost, s));
-            CVZ_CUDA(cudaStreamSynchronize(s));
+            read_small(h.data(), cnt, (R + 1) * sizeof(unsigned), s);
             fprintf(stderr, "events m=%lld live slots=%lld counts:", m, ns);
             for (unsigned v : h) fprintf(stderr, " %u", v);
             fprintf(stderr, "\n");
@@ -1663,17 +1660,14 @@ void resolve_dev(const int64_t *lab, long long n, int64_t *rep_out, bool check, 
              bad);
     if (getenv("CVZ_DEBUG_RESOLVE")) {  // development aid: worklist length per sweep
         std::vector<unsigned> h(R + 1);
-        CVZ_CUDA(cudaMemcpyAsync(h.data(), cnt, (R + 1) * sizeof(unsigned),
-                                 cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(h.data(), cnt, (R + 1) * sizeof(unsigned), s);
         fprintf(stderr, "resolve n=%lld counts:", n);
         for (unsigned v : h) fprintf(stderr, " %u", v);
         fprintf(stderr, "\n");
     }
     if (check) {
         int hbad = 0;
-        CVZ_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(&hbad, bad, sizeof(int), s);
         CVZ_REQUIRE(!hbad, CVZ_ERR_RANGE, "labels must lie in [0, n)");
     }
 }
@@ -1710,8 +1704,7 @@ int cvz_scoda_pass(const int32_t *edges, int64_t m, const int64_t *order, int64_
         CVZ_LAUNCH(any_negative_kernel, grid_for(n, TB, 1, 4), TB, 0, s,
                    reinterpret_cast<const long long *>(d0), (long long)n, neg);
         int hneg = 0;
-        CVZ_CUDA(cudaMemcpyAsync(&hneg, neg, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(&hneg, neg, sizeof(int), s);
         scoda_pass_dev(E, m, n, threshold, tie_code, mode, d0, l0, deg, raw, sc, s, hneg == 0);
         resolve_dev(raw, n, lab, true, sc, s);
     });
@@ -1770,8 +1763,7 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
                    reinterpret_cast<long long *>(history_out), round_index > 1 ? 1 : 0, dchg);
         int hchg = 1;
         if (round_index > 1) {
-            CVZ_CUDA(cudaMemcpyAsync(&hchg, dchg, sizeof(int), cudaMemcpyDeviceToHost, s));
-            CVZ_CUDA(cudaStreamSynchronize(s));
+            read_small(&hchg, dchg, sizeof(int), s);
         }
         *changed = hchg;
         *next_m = 0;
@@ -1806,8 +1798,7 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
                    reinterpret_cast<int2 *>(next_edges), LookbackState{status, ctr}, dcount, tiles,
                    nsize != nullptr, dcount + 1);
         unsigned long long hm[2] = {0, 0};
-        CVZ_CUDA(cudaMemcpyAsync(hm, dcount, sizeof(hm), cudaMemcpyDeviceToHost, s));
-        CVZ_CUDA(cudaStreamSynchronize(s));
+        read_small(hm, dcount, sizeof(hm), s);
         *next_m = (int64_t)hm[0];
         if (next_dead) *next_dead = (int64_t)hm[1];
     });

@@ -316,8 +316,7 @@ int cvz_sketch_add(int64_t *table, int rows, int64_t cols, const int64_t *hash_a
             CVZ_LAUNCH(negative_check_kernel, grid_for(n_amounts, 256, 4, 4), 256, 0, s,
                        reinterpret_cast<const long long *>(amounts), (long long)n_amounts, flag);
             int h = 0;
-            CVZ_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-            CVZ_CUDA(cudaStreamSynchronize(s));
+            read_small(&h, flag, sizeof(int), s);
             CVZ_REQUIRE(!h, CVZ_ERR_VALUE, "amounts must be non-negative");
         }
         sketch_add(table, rows, cols, hash_a, hash_b, keys, amounts, k, n_amounts, d_saturated, s);

@@ -291,7 +291,7 @@ def from_edge_array(edges, node_count=None) -> Graph:
     scal = T.zeros(2, dtype=T.int64, device=nat.device())
     nat.call("cvz_edges_compact", nat.ptr(src), int(src.dtype == T.int32), m_in,
              nat.ptr(out), nat.ptr(scal), nat.ptr(scal[1:]), 1, nat.stream())
-    m, mx = (int(v) for v in scal.cpu().tolist())
+    m, mx = nat.read_ints(scal)
     if node_count is None:
         n = mx + 1 if m else 0
     else:
@@ -307,7 +307,7 @@ def _stats_dev(degree_dev, n):
     out = T.empty(3, dtype=T.int64, device=nat.device())
     nat.call("cvz_degree_stats", nat.ptr(degree_dev), int(degree_dev.shape[0]),
              nat.ptr(out), nat.stream())
-    return [int(v) for v in out.cpu().tolist()]
+    return nat.read_ints(out)
 
 
 def _graph_stats(g: Graph):

@@ -150,7 +150,9 @@ def _masses_and_edges(obj):
 def _device_model(obj):
     """mass (f64), edges (int32), edge weight (f64 or None) as CUDA tensors."""
     T = nat.torch()
-    if hasattr(obj, "weight"):
+    # our SuperGraph first: hasattr(obj, "weight") would evaluate the host
+    # property (a device -> host copy of the weights, then a re-upload)
+    if hasattr(obj, "weight_dev") or hasattr(obj, "weight"):
         if hasattr(obj, "weight_dev"):
             w = obj.weight_dev()
             mass = T.clamp(w, min=1).to(T.float64)

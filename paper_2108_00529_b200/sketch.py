@@ -7,6 +7,7 @@ saturation and estimation run in cvz_sketch_* kernels.
 
 from __future__ import annotations
 
+import functools
 import math
 import warnings
 
@@ -45,8 +46,8 @@ class CountMinSketch:
 
     def _hash_dev(self):
         if self._ab_dev is None:
-            T = nat.torch()
-            self._ab_dev = (nat.to_dev(self.hash_a, T.int64), nat.to_dev(self.hash_b, T.int64))
+            self._ab_dev = _hash_params_dev(self.hash_a.tobytes(), self.hash_b.tobytes(),
+                                            nat.device().index)
         return self._ab_dev
 
     def _indices(self, keys) -> np.ndarray:
@@ -60,13 +61,40 @@ class CountMinSketch:
         return nat.to_host(out)
 
 
+@functools.lru_cache(maxsize=64)
+def _hash_params_dev(a_bytes: bytes, b_bytes: bytes, device_index):
+    """Device copies of one sketch's hash parameters, shared by every sketch
+    with the same parameters (read-only in the kernels); uploaded once from
+    pinned memory without a host sync."""
+    T = nat.torch()
+    out = []
+    for raw in (a_bytes, b_bytes):
+        h = T.from_numpy(np.frombuffer(raw, dtype=np.int64).copy()).pin_memory()
+        out.append(h.to(device=nat.device(), non_blocking=True))
+    return tuple(out)
+
+
+@functools.lru_cache(maxsize=64)
+def _hash_params(rows: int, seed):
+    """numpy's seeded draws (C/sketch.py:50-52), memoised per (rows, seed)."""
+    rng = np.random.default_rng(seed)
+    a = rng.integers(1, int(MERSENNE_P), size=rows, dtype=np.int64)
+    b = rng.integers(0, int(MERSENNE_P), size=rows, dtype=np.int64)
+    a.flags.writeable = False
+    b.flags.writeable = False
+    return a, b
+
+
 def sketch_new(rows: int, cols: int, seed: int) -> CountMinSketch:
     """C/sketch.py:47-55."""
     if rows < 1 or cols < 1:
         raise ValueError("sketch needs at least one row and one column")
-    rng = np.random.default_rng(seed)
-    a = rng.integers(1, int(MERSENNE_P), size=rows, dtype=np.int64)
-    b = rng.integers(0, int(MERSENNE_P), size=rows, dtype=np.int64)
+    if isinstance(seed, (int, np.integer)):
+        a, b = (x.copy() for x in _hash_params(int(rows), int(seed)))
+    else:  # SeedSequence / Generator seeds: not hashable for the memo
+        rng = np.random.default_rng(seed)
+        a = rng.integers(1, int(MERSENNE_P), size=rows, dtype=np.int64)
+        b = rng.integers(0, int(MERSENNE_P), size=rows, dtype=np.int64)
     T = nat.torch()
     table = T.zeros((rows, cols), dtype=T.int64, device=nat.device())
     return CountMinSketch(rows=rows, cols=cols, table=Dual(dev=table), hash_a=a, hash_b=b)
@@ -93,9 +121,10 @@ def _dev64(x):
     return nat.to_dev(h, T.int64), h
 
 
-def sketch_add_many(s: CountMinSketch, keys, amounts) -> None:
+def sketch_add_many(s: CountMinSketch, keys, amounts, _nonneg: bool = False) -> None:
     """Bulk weighted increments (C/sketch.py:71-86) -- GPU, staged in shared
-    memory; keys/amounts may be numpy arrays or CUDA tensors."""
+    memory; keys/amounts may be numpy arrays or CUDA tensors (`_nonneg`:
+    internal, the amounts are known non-negative)."""
     T = nat.torch()
     kd, _ = _dev64(keys)
     ndim = amounts.dim() if isinstance(amounts, T.Tensor) else np.ndim(amounts)
@@ -105,7 +134,7 @@ def sketch_add_many(s: CountMinSketch, keys, amounts) -> None:
             raise ValueError("amounts must be non-negative")
         validate = 0
     else:
-        validate = 1
+        validate = 0 if _nonneg else 1
     # np.add.at(table[r], idx[r], amounts) broadcasting: a scalar or one
     # amount applies to every key; any other length mismatch is an error
     k, na = int(kd.shape[0]), int(ad.shape[0])
@@ -117,7 +146,7 @@ def sketch_add_many(s: CountMinSketch, keys, amounts) -> None:
     nat.call("cvz_sketch_add", nat.ptr(table), s.rows, s.cols, nat.ptr(a), nat.ptr(b),
              nat.ptr(kd), nat.ptr(ad), k, na, validate, nat.ptr(sat), nat.stream())
     s._table.set_dev(table)
-    if int(sat.item()) and not s.saturated:
+    if nat.read_ints(sat)[0] and not s.saturated:
         s.saturated = True
         warnings.warn("sketch counter overflow, counts saturated", RuntimeWarning, stacklevel=2)
 

@@ -73,10 +73,13 @@ def _labels_dev(labels):
 def accumulate_sizes(sketch: CountMinSketch, labels, degrees) -> None:
     """Add each node's degree to its community's counter (C/supergraph.py:42-46)."""
     T = nat.torch()
+    # degrees our kernels computed (a Graph whose degrees never left the
+    # device) are non-negative by construction: no validation pass + sync
+    trusted = getattr(getattr(degrees, "_degree", None), "on_device", False)
     if hasattr(degrees, "degree_dev"):
         degrees = degrees.degree_dev()
     sketch_add_many(sketch, _labels_dev(labels), degrees if isinstance(degrees, T.Tensor)
-                    else np.asarray(degrees, dtype=np.int64))
+                    else np.asarray(degrees, dtype=np.int64), _nonneg=trusted)
 
 
 def contract(g, labels, sketch: CountMinSketch) -> SuperGraph:

@@ -32,7 +32,8 @@ dev = torch.from_numpy(synth.config_graph(a.config)).to("cuda")
 for _ in range(2):
     bench.pipeline(cv, dev, mode=a.mode)
 torch.cuda.synchronize()
-with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA],
+             with_stack=bool(os.environ.get("TL_STACK"))) as prof:
     with torch.profiler.record_function("step"):
         bench.pipeline(cv, dev, mode=a.mode)
     torch.cuda.synchronize()
@@ -55,13 +56,28 @@ for e in rt:
 print("host runtime calls (count, total ms):")
 for k, (c, d) in sorted(rtagg.items(), key=lambda kv: -kv[1][1])[:15]:
     print(f"  {c:6d} {d / 1000:9.3f}  {k}")
+# true idle intervals: no kernel running on any stream (kernels of the
+# side streams overlap the main stream's, so consecutive-start gaps mislead)
 gaps = []
-for x, y in zip(kern, kern[1:]):
-    g = y["ts"] - (x["ts"] + x["dur"])
+end, last = kern[0]["ts"] + kern[0]["dur"], kern[0]
+for y in kern[1:]:
+    g = y["ts"] - end
     if g > 20:
-        gaps.append((g, x["name"][:60], y["name"][:60], x["ts"] + x["dur"], y["ts"]))
+        gaps.append((g, last["name"][:60], y["name"][:60], end, y["ts"]))
+    if y["ts"] + y["dur"] > end:
+        end, last = y["ts"] + y["dur"], y
 tot_gap = sum(g[0] for g in gaps)
 print(f"gaps > 20us: {len(gaps)}  total {tot_gap / 1000:.3f} ms")
 for g, a1, b1, s, e in sorted(gaps, reverse=True)[:25]:
     inside = collections.Counter(r["name"] for r in rt if r["ts"] >= s and r["ts"] < e)
     print(f"  {g / 1000:7.3f} ms after {a1!r} before {b1!r}  host: {dict(inside.most_common(4))}")
+# the host calls inside the three largest idle intervals, in order
+cpu = sorted([e for e in ev if e.get("cat") in ("cuda_runtime", "cuda_driver", "cpu_op",
+                                                 "user_annotation", "python_function")],
+             key=lambda e: e["ts"])
+for g, a1, b1, s, e in sorted(gaps, reverse=True)[:3]:
+    print(f"-- idle {g / 1000:.3f} ms after {a1!r}")
+    for r in cpu:
+        if r["ts"] >= s - 50 and r["ts"] < e and r.get("dur", 0) >= 5:
+            print(f"   +{(r['ts'] - s) / 1000:7.3f} ms {r.get('dur', 0) / 1000:7.3f} ms "
+                  f"{r.get('cat')}: {r['name'][:80]}")
