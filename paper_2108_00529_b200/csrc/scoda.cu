@@ -1199,7 +1199,8 @@ __global__ void init_labels_kernel(long long n, const long long *__restrict__ la
 // ---- round driver helpers --------------------------------------------------
 
 __global__ void size_hist_kernel(const long long *__restrict__ node_lab, long long n,
-                                 unsigned *__restrict__ size) {
+                                 unsigned *__restrict__ size, const int *__restrict__ gate = nullptr) {
+    if (gate && !*gate) return;  // detect round: labels unchanged, nothing follows
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
          x += (long long)gridDim.x * blockDim.x) {
         int l = (int)node_lab[x];
@@ -1266,7 +1267,8 @@ constexpr unsigned SAT_MASK = SAT_BIT - 1;
 // (size == nullptr: no flag)
 __global__ void pack_map_kernel(const long long *__restrict__ rep, long long n,
                                 const unsigned *__restrict__ size, long long Tn,
-                                unsigned *__restrict__ out) {
+                                unsigned *__restrict__ out, const int *__restrict__ gate = nullptr) {
+    if (gate && !*gate) return;
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < n;
          x += (long long)gridDim.x * blockDim.x) {
         const unsigned r = (unsigned)rep[x];
@@ -1283,7 +1285,9 @@ __global__ void pack_map_kernel(const long long *__restrict__ rep, long long n,
 __global__ void __launch_bounds__(TB) relabel_compact_kernel(
     const int2 *__restrict__ in, long long m, const unsigned *__restrict__ map,
     int2 *__restrict__ out, LookbackState st, unsigned long long *__restrict__ d_count,
-    unsigned num_tiles, bool drop, unsigned long long *__restrict__ d_dead) {
+    unsigned num_tiles, bool drop, unsigned long long *__restrict__ d_dead,
+    const int *__restrict__ gate = nullptr) {
+    if (gate && !*gate) return;  // every CTA leaves: no tile waits on a predecessor
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_prefix;
     const unsigned tile = acquire_tile(st, &s_tile);
@@ -1754,21 +1758,20 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
         int64_t *raw = sc.alloc<int64_t>(n), *rep = sc.alloc<int64_t>(n);
         scoda_pass_dev(E, m_cur, n, T, tie_code, mode, d0, nullptr, deg_out, raw, sc, s, true);
         resolve_dev(raw, n, rep, false, sc, s);
-        // 4. compose + history + early-stop test (:266-269)
-        int *dchg = sc.alloc<int>(1);
-        CVZ_CUDA(cudaMemsetAsync(dchg, 0, sizeof(int), s));
+        // 4. compose + history + early-stop test (:266-269).  The next
+        //    stream is built right behind it, gated on the device by the
+        //    changed flag (an unchanged round's kernels exit at once), so
+        //    the round ends with ONE host read of {kept, dead, changed}.
+        //    ctl: [0] kept edges, [1] dead edges, [2] changed (int)
+        auto *ctl = sc.alloc<unsigned long long>(3);
+        CVZ_CUDA(cudaMemsetAsync(ctl, 0, 3 * sizeof(unsigned long long), s));
+        int *dchg = reinterpret_cast<int *>(ctl + 2);
+        if (round_index == 1) CVZ_CUDA(cudaMemsetAsync(dchg, 1, 1, s));  // first round: changed
         CVZ_LAUNCH(compose_kernel, grid_for(n, TB, CITEMS, 8), TB, 0, s, (long long)n,
                    reinterpret_cast<const long long *>(rep), reinterpret_cast<long long *>(node_lab),
                    reinterpret_cast<long long *>(prev_lab),
                    reinterpret_cast<long long *>(history_out), round_index > 1 ? 1 : 0, dchg);
-        int hchg = 1;
-        if (round_index > 1) {
-            read_small(&hchg, dchg, sizeof(int), s);
-        }
-        *changed = hchg;
-        *next_m = 0;
-        if (next_dead) *next_dead = 0;
-        if (!hchg) return;
+        const int *gate = round_index > 1 ? dchg : nullptr;
         // 5. next stream: contract (:272-278) or restream (:274-276)
         const int2 *src = round_stream == 0 ? cur : reinterpret_cast<const int2 *>(orig_edges);
         long long msrc = round_stream == 0 ? m_cur : m_orig;
@@ -1777,10 +1780,9 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
         if (tiles == 0) tiles = 1;
         auto *status = sc.alloc<unsigned long long>(tiles);
         auto *ctr = sc.alloc<unsigned>(1);
-        auto *dcount = sc.alloc<unsigned long long>(2);
+        unsigned long long *dcount = ctl;
         CVZ_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * tiles, s));
         CVZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
-        CVZ_CUDA(cudaMemsetAsync(dcount, 0, 2 * sizeof(unsigned long long), s));
         // next round's community sizes (what its seeding computes) for the
         // dead-edge drop; contract streams only (restream rebuilds each round)
         unsigned *nsize = nullptr;
@@ -1788,19 +1790,21 @@ int cvz_detect_round(const int32_t *cur_edges, int64_t m_cur, const int64_t *ord
             nsize = sc.alloc<unsigned>(n);
             CVZ_CUDA(cudaMemsetAsync(nsize, 0, sizeof(unsigned) * n, s));
             CVZ_LAUNCH(size_hist_kernel, grid_for(n, TB, 1, 8), TB, 0, s,
-                       reinterpret_cast<const long long *>(node_lab), (long long)n, nsize);
+                       reinterpret_cast<const long long *>(node_lab), (long long)n, nsize, gate);
         }
         unsigned *map = sc.alloc<unsigned>(n);
         CVZ_LAUNCH(pack_map_kernel, grid_for(n, TB, 1, 8), TB, 0, s,
                    reinterpret_cast<const long long *>(map64), (long long)n, nsize,
-                   (long long)next_threshold, map);
+                   (long long)next_threshold, map, gate);
         CVZ_LAUNCH(relabel_compact_kernel, tiles, TB, 0, s, src, msrc, map,
                    reinterpret_cast<int2 *>(next_edges), LookbackState{status, ctr}, dcount, tiles,
-                   nsize != nullptr, dcount + 1);
-        unsigned long long hm[2] = {0, 0};
-        read_small(hm, dcount, sizeof(hm), s);
-        *next_m = (int64_t)hm[0];
-        if (next_dead) *next_dead = (int64_t)hm[1];
+                   nsize != nullptr, dcount + 1, gate);
+        unsigned long long hm[3] = {0, 0, 0};
+        read_small(hm, ctl, sizeof(hm), s);
+        const int hchg = (int)(unsigned)hm[2];  // the int in ctl[2]'s low word
+        *changed = hchg != 0;
+        *next_m = hchg ? (int64_t)hm[0] : 0;
+        if (next_dead) *next_dead = hchg ? (int64_t)hm[1] : 0;
     });
 }
 

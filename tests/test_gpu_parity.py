@@ -1153,3 +1153,34 @@ def test_pipeline_edge_cases(cv, orc):
     assert g.edge_count == 0 and g.node_count == 4 and g.degree.tolist() == [0, 0, 0, 0]
     with pytest.raises(ValueError):
         cv.detect_communities(g, cv.ThresholdSchedule(base=2))
+
+
+def test_read_small_and_memoised_sketch_params(cv):
+    """cvz_read_small (control reads that bypass the copy engines) returns the
+    device bytes after the stream's work, refuses > 256 bytes; memoised sketch
+    hash parameters are fresh arrays per sketch (mutating one sketch's
+    parameters does not leak into the next) and equal numpy's draws
+    (C/sketch.py:50-52)."""
+    import torch
+
+    from paper_2108_00529_b200 import _native as nat
+    t = torch.arange(-5, 27, dtype=torch.int64, device="cuda") * 3
+    t.mul_(7)  # queued work the read must wait for
+    assert nat.read_ints(t) == [v * 21 for v in range(-5, 27)]
+    assert nat.read_ints(torch.tensor([2 ** 40 + 1], device="cuda")) == [2 ** 40 + 1]
+    big = torch.zeros(33, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):
+        nat.read_ints(big)
+    s1 = cv.sketch_new(4, 6500, seed=11)
+    rng = np.random.default_rng(11)
+    a = rng.integers(1, (1 << 31) - 1, size=4, dtype=np.int64)
+    b = rng.integers(0, (1 << 31) - 1, size=4, dtype=np.int64)
+    assert np.array_equal(s1.hash_a, a) and np.array_equal(s1.hash_b, b)
+    s1.hash_a[0] = 12345
+    s2 = cv.sketch_new(4, 6500, seed=11)
+    assert np.array_equal(s2.hash_a, a)
+    # generator seeds are not memoised: they advance the caller's generator
+    g = np.random.default_rng(5)
+    s3 = cv.sketch_new(2, 100, seed=g)
+    s4 = cv.sketch_new(2, 100, seed=g)
+    assert not np.array_equal(s3.hash_a, s4.hash_a)
