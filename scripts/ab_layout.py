@@ -9,6 +9,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import hashlib  # noqa: E402
+
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2108_00529_b200 as cv  # noqa: E402
@@ -41,7 +44,8 @@ for _ in range(3):
 env = {k: v for k, v in os.environ.items() if k.startswith("CVZ_")}
 print(f"{a.config} {'full' if a.full else 'super'} n={obj.node_count} m={obj.edge_count} "
       f"env={env} ms/iter={min(ts):.4f} disp[-1]={r.displacement[-1]:.6g} "
-      f"pos0={r.positions[0].tolist()}")
+      f"pos0={r.positions[0].tolist()} "
+      f"hash={hashlib.sha1(np.ascontiguousarray(r.positions).tobytes()).hexdigest()[:12]}")
 with cv._native.profile() as prof:
     cv.layout(obj, cv.LayoutParams(iterations=10))
 for name, (c, ms) in sorted(prof.kernels.items(), key=lambda kv: -kv[1][1])[:int(os.environ.get("AB_TOP", "40"))]:
