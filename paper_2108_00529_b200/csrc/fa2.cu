@@ -894,9 +894,14 @@ __global__ void __launch_bounds__(FB) bh_kernel(const Body *__restrict__ bodies,
 // written into one array in DFS preorder (children in key order = the
 // reference's pop order), so a node's first child is the next node and its
 // subtree is a contiguous index range ending before `skip`.  A node is one
-// 32-byte sector: COM (body position for a leaf), mass, skip, and meta =
-// kind | level << 2; a cell's side^2 is a per-level table (the reference
-// halves the root side exactly, C/layout.py:171-208).  Rarely needed ids
+// 32-byte sector: COM (body position for a leaf), mass, skip, and meta.  A
+// cell at depth L stores meta = -(L << 21): the reference halves the root
+// side exactly (C/layout.py:171-208), so side^2 at depth L is side0^2 with
+// 2L subtracted from its exponent, and the walk forms it with ONE integer
+// add into the high word of side0^2.  Leaves and aggregates (always
+// approximated) store INT_MIN / INT_MIN + 1: the same add flips the sign of
+// side0^2, and a negative side^2 passes `side^2 < theta^2 d^2` for every
+// d^2 >= 0, so the hot loop needs no kind test before the opening test.  Rarely needed ids
 // (binary node / sorted body) live in a parallel aux[] array.
 //
 // Preorder index without a sort: with C_le(f) = #cells whose first body is
@@ -906,8 +911,23 @@ __global__ void __launch_bounds__(FB) bh_kernel(const Body *__restrict__ bodies,
 struct __align__(32) PNode {
     double x, y, m;
     int skip;  // preorder index of the DFS successor, -1 = end
-    int meta;  // kind (1 cell, 2 depth-40 aggregate, 3 body leaf) | level << 2
+    int meta;  // cell: -(level << 21); PN_LEAF / PN_AGG
 };
+
+constexpr int PN_LEAF = INT_MIN;
+constexpr int PN_AGG = INT_MIN + 1;
+// kind (1 cell, 2 depth-40 aggregate, 3 body leaf) and cell depth from meta
+__device__ __forceinline__ int pn_kind(int meta) {
+    return meta == PN_LEAF ? 3 : meta == PN_AGG ? 2 : 1;
+}
+__device__ __forceinline__ int pn_level(int meta) { return (-meta) >> 21; }
+// side^2 of a node (negative for leaves / aggregates): the exponent form when
+// side0^2 is comfortably normal, else the per-level table
+template <bool S2EXP>
+__device__ __forceinline__ double pn_side2(int meta, int s20_hi, int s20_lo, const double *s2tab) {
+    if (S2EXP) return __hiloint2double(s20_hi + meta, s20_lo);
+    return meta <= PN_AGG ? -1.0 : s2tab[pn_level(meta)];
+}
 
 __device__ __forceinline__ void preorder_cells_body(int tid, int nthr, int n, const TNode *__restrict__ nodes,
                                       const int *__restrict__ first, const int *__restrict__ last,
@@ -932,7 +952,7 @@ __device__ __forceinline__ void preorder_cells_body(int tid, int nthr, int n, co
         t.y = c.comy;
         t.m = c.mass;
         t.skip = nxt >= total ? -1 : nxt;
-        t.meta = c.kind | ((c.kind == 1 ? (delta[b] >> 1) : 0) << 2);
+        t.meta = c.kind == 1 ? -((delta[b] >> 1) << 21) : PN_AGG;
         pn[idx] = t;
         aux[idx] = b;
     }
@@ -950,7 +970,7 @@ __device__ __forceinline__ void preorder_leaves_body(int tid, int nthr, int n, c
         t.y = b.y;
         t.m = b.m;
         t.skip = idx + 1 >= total ? -1 : idx + 1;
-        t.meta = 3;
+        t.meta = PN_LEAF;
         pn[idx] = t;
         aux[idx] = q;
     }
@@ -1002,7 +1022,7 @@ struct Walker {
     __device__ __forceinline__ bool visit(const PNode &t, int c, int p, int self, long long i,
                                           double xi, double yi, double mi, double kmi, double &fx,
                                           double &fy) const {
-        const int kind = t.meta & 3;
+        const int kind = pn_kind(t.meta);
         double mc = t.m, dx = sub(xi, t.x), dy = sub(yi, t.y);
         double d2 = add(mul(dx, dx), mul(dy, dy));
         bool self_out = false;
@@ -1028,7 +1048,7 @@ struct Walker {
             }
         }
         // leaves and aggregates are always approximated (C/layout.py:256-261)
-        if (kind == 1 && !(s2tab[t.meta >> 2] < mul(th2, d2))) return false;
+        if (kind == 1 && !(s2tab[pn_level(t.meta)] < mul(th2, d2))) return false;
         if (c == self) return true;  // j == i skipped (:237-238)
         double f;
         if (d2 >= EPS * EPS) {
@@ -1156,20 +1176,21 @@ __global__ void __launch_bounds__(NT, MINB) bh_flat_kernel(Walker w, const PNode
         // (-1.3 % against testing the kind first)
         while (c >= 0) {
             const PNode t = pn[c];
-            const int kind = t.meta & 3;
             if (COUNT) ++n_visit;
             const double dx = sub(xi, t.x), dy = sub(yi, t.y);
             const double d2 = add(mul(dx, dx), mul(dy, dy));
             // cells open unless side^2 < theta^2 d^2; leaves and aggregates
-            // are always approximated (C/layout.py:256-261)
-            const bool open =
-                kind == 1 && !((s2exp ? __hiloint2double(s20_hi - ((t.meta >> 2) << 21), s20_lo)
-                                      : s2tab[t.meta >> 2]) < mul(th2, d2));
+            // are always approximated (C/layout.py:256-261): their side^2 is
+            // negative
+            const bool open = !((s2exp ? pn_side2<true>(t.meta, s20_hi, s20_lo, s2tab)
+                                       : pn_side2<false>(t.meta, s20_hi, s20_lo, s2tab)) <
+                                mul(th2, d2));
             if (open) {
                 ++c;
                 continue;
             }
-            if (kind == 2 || !(d2 >= eps2)) {
+            if (t.meta == PN_AGG || !(d2 >= eps2)) {
+                const int kind = pn_kind(t.meta);
                 if (kind == 2) {
                     if (COUNT) ++n_acc;
                     const double2 r = aggregate_add(w, t, c, p, i, xi, yi, mi, kmi, fx, fy);
