@@ -380,67 +380,154 @@ __device__ __forceinline__ void karras_body(int bid, int nblk, Keys K, int *__re
     if (bid == 0 && threadIdx.x == 0) pdelta[0] = -2;  // root
 }
 
-// ---- cell sums from double-double prefix sums ----------------------------------
+// ---- cell sums from fixed-point prefix sums -------------------------------------
 // Every radix-tree node covers a contiguous range [first, last] of the
-// key-sorted bodies, so its mass and moments are differences of prefix sums.
-// The prefixes are double-double (error-free TwoSum), so a difference is
-// exact to ~n * 2^-106 of the prefix magnitude -- as accurate as summing the
-// cell directly -- and every node is computed independently: no bottom-up
-// pass, no atomics, no depth-serial chain.
-struct DD {
-    double h, l;
+// key-sorted bodies, so its mass and moments are differences of prefix sums,
+// and every node is computed independently: no bottom-up pass, no atomics,
+// no depth-serial chain.  The prefixes are 128-bit two's-complement fixed
+// point: a body's m, m*x, m*y (the same fp64 products as before) scaled by
+// 2^S and truncated, with S chosen per tree so that n * max m * max|coord|
+// stays below 2^125 -- integer adds are exact and associative, so a
+// difference is the cell's exact sum up to one truncation per body
+// (<= n * 2^-125 of that bound, finer than a double-double's 2^-106), and
+// the scan's dependent chains are two-instruction adds instead of the
+// twelve-flop TwoSum (the scan was bound by those fp64 latencies).
+struct FX {
+    unsigned long long lo;
+    long long hi;
 };
-struct DD3 {
-    DD m, x, y;
+struct FX3 {
+    FX m, x, y;
 };
 
-__device__ __forceinline__ DD dd_add(DD a, DD b) {
-    double s = __dadd_rn(a.h, b.h);
-    double bb = __dsub_rn(s, a.h);
-    double e = __dadd_rn(__dsub_rn(a.h, __dsub_rn(s, bb)), __dsub_rn(b.h, bb));
-    e = __dadd_rn(e, __dadd_rn(a.l, b.l));
-    double h = __dadd_rn(s, e);
-    return DD{h, __dsub_rn(e, __dsub_rn(h, s))};
+__device__ __forceinline__ FX fx_add(FX a, FX b) {
+    FX r;
+    asm("add.cc.u64 %0, %2, %4;\n\taddc.s64 %1, %3, %5;"
+        : "=l"(r.lo), "=l"(r.hi)
+        : "l"(a.lo), "l"(a.hi), "l"(b.lo), "l"(b.hi));
+    return r;
 }
 
-__device__ __forceinline__ DD dd_neg(DD a) { return DD{-a.h, -a.l}; }
+__device__ __forceinline__ FX fx_neg(FX a) {
+    FX r;
+    asm("sub.cc.u64 %0, 0, %2;\n\tsubc.s64 %1, 0, %3;"
+        : "=l"(r.lo), "=l"(r.hi)
+        : "l"(a.lo), "l"(a.hi));
+    return r;
+}
 
-// Two-level double-double prefix: tile-local inclusive prefixes (TILE_DD
+// v * 2^S truncated toward zero (|v| * 2^S < 2^127 by the choice of S)
+__device__ __forceinline__ FX to_fx(double v, int S) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    int ex = (int)((bits >> 52) & 0x7ff);
+    unsigned long long mant = bits & ((1ull << 52) - 1);
+    if (ex == 0)
+        ex = 1;  // subnormal
+    else
+        mant |= 1ull << 52;
+    const int sh = ex - 1075 + S;  // |v| = mant * 2^(ex - 1075)
+    FX r{0ull, 0ll};
+    if (sh >= 0) {
+        if (sh < 64) {
+            r.lo = mant << sh;
+            r.hi = sh ? (long long)(mant >> (64 - sh)) : 0ll;
+        } else {
+            r.hi = (long long)(mant << (sh - 64));
+        }
+    } else if (sh > -64) {
+        r.lo = mant >> (-sh);
+    }
+    return (bits >> 63) ? fx_neg(r) : r;
+}
+
+// x * 2^-S correctly rounded to the nearest double
+__device__ __forceinline__ double from_fx(FX x, int S) {
+    const bool neg = x.hi < 0;
+    if (neg) x = fx_neg(x);
+    const unsigned long long hi = (unsigned long long)x.hi;
+    double d;
+    if (hi == 0) {
+        d = __ull2double_rn(x.lo);
+    } else {
+        const int lz = __clzll(hi);
+        unsigned long long w = lz ? (hi << lz) | (x.lo >> (64 - lz)) : hi;
+        const unsigned long long rest = lz ? (x.lo << lz) : x.lo;
+        w |= rest != 0;  // sticky: the top 64 bits round like the whole value
+        d = ldexp(__ull2double_rn(w), 64 - lz);
+    }
+    d = ldexp(d, -S);
+    return neg ? -d : d;
+}
+
+// Scales of one tree: prefixes of m stay below n * max m, of m*x / m*y
+// below n * max m * max|coord| (bbox of the current positions).  mmax:
+// max |m| as non-negative double bits (Tree::set_mass).
+struct FxScale {
+    int sm, sxy;
+};
+
+__device__ __forceinline__ int fx_shift(double bound) {
+    // smallest e with 2^e > bound (with margin), S = 125 - e, clamped
+    if (!(bound > 0.0)) return 0;
+    const int e = ilogb(bound * (1.0 + 0x1p-40)) + 1;
+    return max(-1000, min(1000, 125 - e));
+}
+
+__device__ __forceinline__ FxScale fx_scale(int n, const unsigned long long *mmax,
+                                            const double *bbox) {
+    const double mm = __longlong_as_double((long long)*mmax);
+    const double c = fmax(fmax(fabs(bbox[0]), fabs(bbox[1])), fmax(fabs(bbox[2]), fabs(bbox[3])));
+    const double bm = (double)n * mm;
+    return FxScale{fx_shift(bm), fx_shift(bm * c)};
+}
+
+// max |mass| (non-negative doubles order like their bit patterns)
+__global__ void mass_max_kernel(const double *__restrict__ mass, long long n,
+                                unsigned long long *__restrict__ out) {
+    unsigned long long m = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        m = max(m, (unsigned long long)__double_as_longlong(fabs(mass[i])));
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// Two-level fixed-point prefix: tile-local inclusive prefixes (TILE_FX
 // bodies per CTA, 8 per thread) + one small scan of the tile totals.
-constexpr int DD_ITEMS = 2;
-constexpr int TILE_DD = FB * DD_ITEMS;
+constexpr int FX_ITEMS = 2;
+constexpr int TILE_FX = FB * FX_ITEMS;
 
-__device__ __forceinline__ DD dd_shfl_up(DD v, int o) {
-    return DD{__shfl_up_sync(0xffffffffu, v.h, o), __shfl_up_sync(0xffffffffu, v.l, o)};
+__device__ __forceinline__ FX fx_shfl_up(FX v, int o) {
+    return FX{__shfl_up_sync(0xffffffffu, v.lo, o), __shfl_up_sync(0xffffffffu, v.hi, o)};
 }
 
-__device__ __forceinline__ DD3 dd3_add(const DD3 &a, const DD3 &b) {
-    return DD3{dd_add(a.m, b.m), dd_add(a.x, b.x), dd_add(a.y, b.y)};
+__device__ __forceinline__ FX3 fx3_add(const FX3 &a, const FX3 &b) {
+    return FX3{fx_add(a.m, b.m), fx_add(a.x, b.x), fx_add(a.y, b.y)};
 }
 
-// block-wide inclusive scan of one DD3 per thread
-__device__ DD3 block_scan_dd3(DD3 v, DD3 *warp_tot, DD3 &block_total) {
+// block-wide inclusive scan of one FX3 per thread
+__device__ FX3 block_scan_fx3(FX3 v, FX3 *warp_tot, FX3 &block_total) {
     const int lane = lane_id(), wid = threadIdx.x >> 5;
-    DD3 x = v;
+    FX3 x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        DD3 y{dd_shfl_up(x.m, o), dd_shfl_up(x.x, o), dd_shfl_up(x.y, o)};
-        if (lane >= o) x = dd3_add(y, x);
+        FX3 y{fx_shfl_up(x.m, o), fx_shfl_up(x.x, o), fx_shfl_up(x.y, o)};
+        if (lane >= o) x = fx3_add(y, x);
     }
     if (lane == 31) warp_tot[wid] = x;
     __syncthreads();
-    DD3 before{{0, 0}, {0, 0}, {0, 0}};
-    DD3 tot{{0, 0}, {0, 0}, {0, 0}};
+    FX3 before{{0, 0}, {0, 0}, {0, 0}};
+    FX3 tot{{0, 0}, {0, 0}, {0, 0}};
     for (int w = 0; w < FB / 32; ++w) {
-        if (w < wid) before = dd3_add(before, warp_tot[w]);
-        tot = dd3_add(tot, warp_tot[w]);
+        if (w < wid) before = fx3_add(before, warp_tot[w]);
+        tot = fx3_add(tot, warp_tot[w]);
     }
     block_total = tot;
-    return wid ? dd3_add(before, x) : x;
+    return wid ? fx3_add(before, x) : x;
 }
 
 // Gather the key-sorted bodies of one tile (bodies, 80-bit keys for karras)
-// and run the tile-local double-double prefix over them in the same CTA.
+// and run the tile-local fixed-point prefix over them in the same CTA.
 // sorted 80-bit keys only (the split build: karras can start while the
 // bodies are gathered and prefix-summed on the main stream)
 __global__ void __launch_bounds__(FB) gather_keys_kernel(
@@ -455,7 +542,7 @@ __global__ void __launch_bounds__(FB) gather_keys_kernel(
     }
 }
 
-__device__ __forceinline__ void dd_tiles_body(DD3 *__restrict__ tile_tot, int tiles);
+__device__ __forceinline__ void fx_tiles_body(FX3 *__restrict__ tile_tot, int tiles);
 
 // khi == nullptr: keys already gathered (gather_keys_kernel); tile_ctr !=
 // nullptr: the last CTA to finish also scans the tile totals
@@ -463,17 +550,19 @@ __global__ void __launch_bounds__(FB) gather_scan_kernel(
     const double2 *__restrict__ pos, const double *__restrict__ mass,
     const unsigned *__restrict__ idx, const unsigned *__restrict__ k32s,
     const unsigned long long *__restrict__ krest, int n, Body *__restrict__ bodies,
-    unsigned long long *__restrict__ khi, unsigned *__restrict__ klo, DD3 *__restrict__ local,
-    DD3 *__restrict__ tile_tot, int top_digits, unsigned *__restrict__ tile_ctr) {
+    unsigned long long *__restrict__ khi, unsigned *__restrict__ klo, FX3 *__restrict__ local,
+    FX3 *__restrict__ tile_tot, int top_digits, unsigned *__restrict__ tile_ctr,
+    const double *__restrict__ bbox, const unsigned long long *__restrict__ mmax) {
     griddep_wait();
-    __shared__ DD3 warp_tot[FB / 32];
-    const long long base = (long long)blockIdx.x * TILE_DD + (long long)threadIdx.x * DD_ITEMS;
-    DD3 acc{{0, 0}, {0, 0}, {0, 0}};
-    DD3 item[DD_ITEMS];
+    __shared__ FX3 warp_tot[FB / 32];
+    const FxScale S = fx_scale(n, mmax, bbox);
+    const long long base = (long long)blockIdx.x * TILE_FX + (long long)threadIdx.x * FX_ITEMS;
+    FX3 acc{{0, 0}, {0, 0}, {0, 0}};
+    FX3 item[FX_ITEMS];
 #pragma unroll
-    for (int j = 0; j < DD_ITEMS; ++j) {
+    for (int j = 0; j < FX_ITEMS; ++j) {
         long long p = base + j;
-        DD3 v{{0, 0}, {0, 0}, {0, 0}};
+        FX3 v{{0, 0}, {0, 0}, {0, 0}};
         if (p < n) {
             unsigned i = idx[p];
             double2 q = pos[i];
@@ -484,28 +573,28 @@ __global__ void __launch_bounds__(FB) gather_scan_kernel(
                 khi[p] = ((unsigned long long)k32s[p] << (64 - 2 * top_digits)) | (r >> 16);
                 klo[p] = (unsigned)(r & 0xffffu) << 16;  // digits 32..39 on top
             }
-            v = DD3{DD{mi, 0.0}, DD{mul(mi, q.x), 0.0}, DD{mul(mi, q.y), 0.0}};
+            v = FX3{to_fx(mi, S.sm), to_fx(mul(mi, q.x), S.sxy), to_fx(mul(mi, q.y), S.sxy)};
         }
-        acc = dd3_add(acc, v);
+        acc = fx3_add(acc, v);
         item[j] = acc;
     }
-    DD3 total;
-    DD3 incl = block_scan_dd3(acc, warp_tot, total);
-    DD3 excl{{0, 0}, {0, 0}, {0, 0}};
+    FX3 total;
+    FX3 incl = block_scan_fx3(acc, warp_tot, total);
+    FX3 excl{{0, 0}, {0, 0}, {0, 0}};
     // exclusive prefix of this thread = incl - acc, formed as a sum to stay exact
     {
         const int lane = lane_id(), wid = threadIdx.x >> 5;
-        DD3 up{dd_shfl_up(incl.m, 1), dd_shfl_up(incl.x, 1), dd_shfl_up(incl.y, 1)};
+        FX3 up{fx_shfl_up(incl.m, 1), fx_shfl_up(incl.x, 1), fx_shfl_up(incl.y, 1)};
         if (lane > 0) {
             excl = up;
         } else if (wid > 0) {
-            for (int w = 0; w < wid; ++w) excl = dd3_add(excl, warp_tot[w]);
+            for (int w = 0; w < wid; ++w) excl = fx3_add(excl, warp_tot[w]);
         }
     }
 #pragma unroll
-    for (int j = 0; j < DD_ITEMS; ++j) {
+    for (int j = 0; j < FX_ITEMS; ++j) {
         long long i = base + j;
-        if (i < n) local[i] = dd3_add(excl, item[j]);
+        if (i < n) local[i] = fx3_add(excl, item[j]);
     }
     if (threadIdx.x == 0) tile_tot[blockIdx.x] = total;
     if (tile_ctr) {  // last CTA scans the tile totals (threadfence-reduction pattern)
@@ -516,41 +605,41 @@ __global__ void __launch_bounds__(FB) gather_scan_kernel(
         __syncthreads();
         if (last) {
             __threadfence();
-            dd_tiles_body(tile_tot, gridDim.x);
+            fx_tiles_body(tile_tot, gridDim.x);
             if (threadIdx.x == 0) *tile_ctr = 0u;  // ready for the next replay
         }
     }
 }
 
 // exclusive scan of the tile totals, one CTA
-__device__ __forceinline__ void dd_tiles_body(DD3 *__restrict__ tile_tot, int tiles) {
-    __shared__ DD3 warp_tot[FB / 32];
-    DD3 carry{{0, 0}, {0, 0}, {0, 0}};
+__device__ __forceinline__ void fx_tiles_body(FX3 *__restrict__ tile_tot, int tiles) {
+    __shared__ FX3 warp_tot[FB / 32];
+    FX3 carry{{0, 0}, {0, 0}, {0, 0}};
     for (int t0 = 0; t0 < tiles; t0 += FB) {
         int t = t0 + threadIdx.x;
-        DD3 v = t < tiles ? tile_tot[t] : DD3{{0, 0}, {0, 0}, {0, 0}};
-        DD3 total;
-        DD3 incl = block_scan_dd3(v, warp_tot, total);
+        FX3 v = t < tiles ? tile_tot[t] : FX3{{0, 0}, {0, 0}, {0, 0}};
+        FX3 total;
+        FX3 incl = block_scan_fx3(v, warp_tot, total);
         __syncthreads();
         // exclusive = carry + (incl - v): recompute as carry + exclusive sum
-        DD3 excl{{0, 0}, {0, 0}, {0, 0}};
+        FX3 excl{{0, 0}, {0, 0}, {0, 0}};
         const int lane = lane_id(), wid = threadIdx.x >> 5;
-        DD3 up{dd_shfl_up(incl.m, 1), dd_shfl_up(incl.x, 1), dd_shfl_up(incl.y, 1)};
+        FX3 up{fx_shfl_up(incl.m, 1), fx_shfl_up(incl.x, 1), fx_shfl_up(incl.y, 1)};
         if (lane > 0) {
             excl = up;
         } else if (wid > 0) {
-            for (int w = 0; w < wid; ++w) excl = dd3_add(excl, warp_tot[w]);
+            for (int w = 0; w < wid; ++w) excl = fx3_add(excl, warp_tot[w]);
         }
         __syncthreads();
-        if (t < tiles) tile_tot[t] = dd3_add(carry, excl);
-        carry = dd3_add(carry, total);
+        if (t < tiles) tile_tot[t] = fx3_add(carry, excl);
+        carry = fx3_add(carry, total);
         __syncthreads();
     }
 }
 
-__device__ __forceinline__ DD3 dd_prefix_at(const DD3 *__restrict__ local,
-                                            const DD3 *__restrict__ tile_off, int i) {
-    return dd3_add(tile_off[i / TILE_DD], local[i]);
+__device__ __forceinline__ FX3 fx_prefix_at(const FX3 *__restrict__ local,
+                                            const FX3 *__restrict__ tile_off, int i) {
+    return fx3_add(tile_off[i / TILE_FX], local[i]);
 }
 
 
@@ -564,10 +653,10 @@ __global__ void __launch_bounds__(FB) karras_tiles_kernel(Keys K, int *__restric
                                                           int *__restrict__ parent_leaf,
                                                           int *__restrict__ pdelta,
                                                           int *__restrict__ rc_by_split,
-                                                          DD3 *__restrict__ tile_tot, int tiles) {
+                                                          FX3 *__restrict__ tile_tot, int tiles) {
     griddep_wait();
     if (blockIdx.x == gridDim.x - 1) {
-        dd_tiles_body(tile_tot, tiles);
+        fx_tiles_body(tile_tot, tiles);
         return;
     }
     karras_body(blockIdx.x, gridDim.x - 1, K, left, first, last, delta_out, parent_int,
@@ -587,34 +676,30 @@ __global__ void __launch_bounds__(FB) karras_only_kernel(Keys K, int *__restrict
                 pdelta, rc_by_split);
 }
 
-__global__ void node_sums_kernel(int n, const DD3 *__restrict__ local,
-                                 const DD3 *__restrict__ tile_off,
+__global__ void node_sums_kernel(int n, const FX3 *__restrict__ local,
+                                 const FX3 *__restrict__ tile_off,
                                  const int *__restrict__ left, const int *__restrict__ first,
                                  const int *__restrict__ last, const int *__restrict__ delta,
                                  const int *__restrict__ pdelta,
                                  const int *__restrict__ rc_by_split,
                                  const double *__restrict__ bbox, double *__restrict__ smass,
                                  double *__restrict__ sx, double *__restrict__ sy,
-                                 TNode *__restrict__ nodes, unsigned *__restrict__ cnt) {
+                                 TNode *__restrict__ nodes, unsigned *__restrict__ cnt,
+                                 const unsigned long long *__restrict__ mmax) {
     griddep_wait();
     Geo g = root_geo(bbox);
+    const FxScale S = fx_scale(n, mmax, bbox);
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < n - 1;
          node += gridDim.x * blockDim.x) {
         const int f0 = first[node], l0 = last[node];
-        DD3 hi = dd_prefix_at(local, tile_off, l0);
-        double mm, xx, yy;
-        if (f0 == 0) {
-            mm = hi.m.h;
-            xx = hi.x.h;
-            yy = hi.y.h;
-        } else {
-            DD3 lo = dd_prefix_at(local, tile_off, f0 - 1);
-            DD a = dd_add(hi.m, dd_neg(lo.m)), b = dd_add(hi.x, dd_neg(lo.x)),
-               c = dd_add(hi.y, dd_neg(lo.y));
-            mm = __dadd_rn(a.h, a.l);
-            xx = __dadd_rn(b.h, b.l);
-            yy = __dadd_rn(c.h, c.l);
+        FX3 hi = fx_prefix_at(local, tile_off, l0);
+        if (f0 > 0) {
+            const FX3 lo = fx_prefix_at(local, tile_off, f0 - 1);
+            hi = FX3{fx_add(hi.m, fx_neg(lo.m)), fx_add(hi.x, fx_neg(lo.x)),
+                     fx_add(hi.y, fx_neg(lo.y))};
         }
+        const double mm = from_fx(hi.m, S.sm), xx = from_fx(hi.x, S.sxy),
+                     yy = from_fx(hi.y, S.sxy);
         smass[node] = mm;
         sx[node] = xx;
         sy[node] = yy;
@@ -1951,7 +2036,7 @@ struct Tree {
     unsigned *visit;
     double *smass, *sx, *sy;
     TNode *nodes;
-    DD3 *prefix, *tile_tot;
+    FX3 *prefix, *tile_tot;
     int2 *i12;
     PNode *pn;
     int *paux;
@@ -1979,8 +2064,9 @@ struct Tree {
         n = n_;
         scr = &sc;
         i12 = sc.alloc<int2>(n > 1 ? n - 1 : 1);
-        prefix = sc.alloc<DD3>(n);
-        tile_tot = sc.alloc<DD3>((n + TILE_DD - 1) / TILE_DD);
+        prefix = sc.alloc<FX3>(n);
+        mmax = sc.alloc<unsigned long long>(1);
+        tile_tot = sc.alloc<FX3>((n + TILE_FX - 1) / TILE_FX);
         pn = sc.alloc<PNode>(2 * n - 1);
         paux = sc.alloc<int>(2 * n - 1);
         pcnt = sc.alloc<unsigned>(n);
@@ -2029,10 +2115,20 @@ struct Tree {
     // build from pos + bbox (bbox already on device)
     // aux != nullptr: karras runs on `aux` while the bodies are gathered and
     // prefix-summed on `s` (fork ev_a, join ev_b; both captured into the graph)
+    // max |mass| for the fixed-point scales (masses are constant over a
+    // layout: once per layout / repulsion call, before any graph capture)
+    unsigned long long *mmax = nullptr;
+    const double *mass_set = nullptr;
+    void set_mass(const double *mass, cudaStream_t s) {
+        CVZ_CUDA(cudaMemsetAsync(mmax, 0, sizeof(unsigned long long), s));
+        CVZ_LAUNCH(mass_max_kernel, grid_for(n, FB, 1, 8), FB, 0, s, mass, (long long)n, mmax);
+        mass_set = mass;
+    }
     void build(const double2 *pos, const double *mass, const double *bbox_, cudaStream_t s,
                cudaStream_t aux = nullptr, cudaEvent_t ev_a = nullptr,
                cudaEvent_t ev_b = nullptr) {
         bbox = const_cast<double *>(bbox_);
+        CVZ_REQUIRE(mass == mass_set, CVZ_ERR_VALUE, "Tree::set_mass not called for these masses");
         unsigned g = grid_for(n, FB, 1, 8);
         // radix-sorted levels: 12 (3 passes) measured best for supergraph-sized
         // n, 16 for multi-million-body full graphs (denser level-12 cells);
@@ -2058,7 +2154,7 @@ struct Tree {
         CVZ_LAUNCH_PDL(tie_fixup_kernel, g, FB, 0, s, klo2, idx2, khi, n, long_runs, nlong);
         CVZ_LAUNCH_PDL(tie_fixup_long_kernel, num_sms(), 1024, 0, s, klo2, idx2, khi, n, long_runs,
                    nlong, fix_k, fix_i);
-        const int tiles = (n + TILE_DD - 1) / TILE_DD;
+        const int tiles = (n + TILE_FX - 1) / TILE_FX;
         Keys K{khi3, klo3, n};
         if (aux) {
             // the body gather + prefix sums need only the sorted order: they
@@ -2073,20 +2169,21 @@ struct Tree {
             CVZ_CUDA(cudaEventRecord(ev_b, aux));
             CVZ_LAUNCH(gather_scan_kernel, tiles, FB, 0, s, pos, mass, idx2, klo2, khi, n, bodies,
                        (unsigned long long *)nullptr, (unsigned *)nullptr, prefix, tile_tot,
-                       top_digits, tile_ctr);
+                       top_digits, tile_ctr, bbox, mmax);
             CVZ_CUDA(cudaStreamWaitEvent(s, ev_b, 0));
             CVZ_LAUNCH(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix, tile_tot,
                        left, first, last, delta, pdelta, rc_by_split, bbox, smass, sx, sy, nodes,
-                       flat() ? pcnt : nullptr);
+                       flat() ? pcnt : nullptr, mmax);
         } else {
             CVZ_LAUNCH_PDL(gather_scan_kernel, tiles, FB, 0, s, pos, mass, idx2, klo2, khi, n,
-                           bodies, khi3, klo3, prefix, tile_tot, top_digits, (unsigned *)nullptr);
+                           bodies, khi3, klo3, prefix, tile_tot, top_digits, (unsigned *)nullptr,
+                           bbox, mmax);
             CVZ_LAUNCH_PDL(karras_tiles_kernel, grid_for(n - 1, FB, 1, 8) + 1, FB, 0, s, K, left,
                            first, last, delta, parent_int, parent_leaf, pdelta, rc_by_split,
                            tile_tot, tiles);
             CVZ_LAUNCH_PDL(node_sums_kernel, grid_for(n - 1, FB, 1, 8), FB, 0, s, n, prefix,
                            tile_tot, left, first, last, delta, pdelta, rc_by_split, bbox, smass, sx,
-                           sy, nodes, flat() ? pcnt : nullptr);
+                           sy, nodes, flat() ? pcnt : nullptr, mmax);
         }
         if (flat()) {
             {
@@ -2235,6 +2332,7 @@ void repulsion_dev(const double *pos, const double *mass, long long n, double kr
     bbox_dev(p2, (int)n, bbox, sc, s);
     Tree t;
     t.alloc((int)n, sc);
+    t.set_mass(mass, s);
     t.build(p2, mass, bbox, s);
     t.repulse(kr, theta, o2, nullptr, false, s);
     if (t.jitter_seen(s)) {  // a cell jitter needs the reference's cell numbering
@@ -2530,6 +2628,7 @@ int cvz_fa2_shard_create(const double *pos, const double *mass, int64_t n, const
             bbox_dev(reinterpret_cast<const double2 *>(pos), (int)n, h->bbox, sc, s);
             if (!h->exact) {
                 h->tree.alloc((int)n, sc);
+                h->tree.set_mass(h->mass, s);
                 h->tree.force_flat = true;
                 h->work = sc.alloc<int>(hi > lo ? hi - lo : 1);
                 h->nwork = sc.alloc<int>(1);
@@ -2703,7 +2802,10 @@ int cvz_layout_run(double *pos, const double *mass, int64_t n, const int32_t *ed
         reset_scalars();
         const bool exact = P->theta <= 0;
         Tree tree;
-        if (!exact) tree.alloc(N, sc);
+        if (!exact) {
+            tree.alloc(N, sc);
+            tree.set_mass(mass, s);
+        }
         long long *badp = &scal->bad;
         // snapshot for the (rare) rerun with the reference's cell numbering
         double2 *pos0 = sc.alloc<double2>(n), *prev0 = sc.alloc<double2>(n);
