@@ -236,8 +236,9 @@ def roofline(prof, st, peak_gbs):
     if name.startswith("bh_"):
         # the tree walk is not HBM-bound: its node array is L1/L2-resident and
         # every visit is a dependent fp64 chain (profiles/r1g_ncu_full_c4_fa2.md)
-        roof["limiter"] = ("issue-bound fp64 tree walk (ncu: DRAM ~1%, L1 hit ~96%); "
-                           "see walk.fp64_frac")
+        roof["limiter"] = ("L1TEX-throughput-bound fp64 tree walk (ncu: LSU wavefronts "
+                           "~70% of peak elapsed, ~78% while active; L1 hit ~96%, DRAM ~1%); "
+                           "see roofline.l1 and walk.fp64_frac")
     return roof, top
 
 
@@ -763,6 +764,19 @@ def main():
     try:  # DRAM bytes per launch from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             roof["traffic"] = json.load(fh).get(roof["kernel"])
+    except (OSError, ValueError):
+        pass
+    try:  # the roof the walk actually sits under: L1TEX throughput (ncu)
+        with open(os.path.join(ROOT, "profiles", "ncu_limits.json")) as fh:
+            lim = json.load(fh).get(roof["kernel"])
+        if lim:
+            roof["l1"] = {
+                "frac_elapsed": lim.get("l1tex__throughput.avg.pct_of_peak_sustained_elapsed"),
+                "frac_active": lim.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                "issue_active": lim.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "fp64_pipe_active": lim.get(
+                    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                "source": "profiles/ncu_limits.json (ncu --set full of this kernel)"}
     except (OSError, ValueError):
         pass
     value = r["m_in"] * ws / (r["ms_step"] / 1000.0)
