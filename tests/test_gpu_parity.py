@@ -703,6 +703,31 @@ def test_repulsion_clusters_vs_oracle(cv, orc, seed):
         assert err <= 1e-9 * np.abs(ref).max(), (theta, err / np.abs(ref).max())
 
 
+@pytest.mark.parametrize("case", ["huge", "tiny", "mass_range"])
+def test_repulsion_extreme_scales_vs_oracle(cv, orc, case):
+    """Root side^2 outside 1e-200..1e300 takes the per-level side^2 table
+    instead of the one-add exponent form of the preorder node encoding
+    (leaves / aggregates must still always pass the opening test there);
+    masses over 18 decades stress the fixed-point cell-sum scales."""
+    rng = np.random.default_rng({"huge": 11, "tiny": 12, "mass_range": 13}[case])
+    n = 400
+    pos = rng.uniform(-1, 1, (n, 2))
+    mass = rng.uniform(1, 10, n)
+    if case == "huge":
+        pos = pos * 1e152          # side^2 ~ 1e305: table path
+    elif case == "tiny":
+        pos = pos * 1e-101         # side^2 ~ 1e-201: table path, all pairs coincident
+    else:
+        pos = pos * 50.0
+        mass = 10.0 ** rng.uniform(-9, 9, n)
+    for theta in (0.5, 0.9):
+        ref = orc.repulsion_forces(pos, mass, 80.0, theta)
+        out = cv.repulsion_forces(pos, mass, 80.0, theta)
+        assert np.all(np.isfinite(out))
+        scale = np.abs(ref).max()
+        assert np.max(np.abs(out - ref)) <= 1e-9 * scale, (case, theta)
+
+
 def test_repulsion_long_tie_runs_vs_oracle(cv, orc):
     """Thousands of bodies inside one level-16 cell (tiny clouds next to far
     outliers) exercise the tree sort's tie fix-up: shared-memory runs
