@@ -189,14 +189,21 @@ __global__ void keys_kernel(const double2 *__restrict__ pos, long long n,
         double cx = g.cx, cy = g.cy, h = g.half;
         unsigned long long rest = 0;
         unsigned top = 0;
+        // two loops (top digits, then the rest) instead of a per-level
+        // test of which word the digit goes to
+        int dpt = 0;
 #pragma unroll 4
-        for (int dpt = 0; dpt < MAX_DEPTH; ++dpt) {
+        for (; dpt < top_digits; ++dpt) {
             int qx = p.x >= cx, qy = p.y >= cy;
-            unsigned digit = 3u - (unsigned)(qx + 2 * qy);
-            if (dpt < top_digits)
-                top = (top << 2) | digit;
-            else
-                rest = (rest << 2) | digit;
+            top = (top << 2) | (3u - (unsigned)(qx + 2 * qy));
+            h = 0.5 * h;
+            cx = qx ? cx + h : cx - h;
+            cy = qy ? cy + h : cy - h;
+        }
+#pragma unroll 4
+        for (; dpt < MAX_DEPTH; ++dpt) {
+            int qx = p.x >= cx, qy = p.y >= cy;
+            rest = (rest << 2) | (3u - (unsigned)(qx + 2 * qy));
             h = 0.5 * h;
             cx = qx ? cx + h : cx - h;
             cy = qy ? cy + h : cy - h;
