@@ -552,11 +552,12 @@ __global__ void __launch_bounds__(FB) gather_keys_kernel(
 __device__ __forceinline__ void fx_tiles_body(FX3 *__restrict__ tile_tot, int tiles);
 
 // khi == nullptr: keys already gathered (gather_keys_kernel); tile_ctr !=
-// nullptr: the last CTA to finish also scans the tile totals.  Three CTAs
-// per SM (<= 85 registers): on the fixed-point prefix the scan is latency-
-// bound and the extra CTA beats the registers it costs (C4 supergraph
-// 0.458 -> 0.454 ms/iter, C3 0.195 -> 0.193, C4 full graph 4.62 -> 4.61)
-__global__ void __launch_bounds__(FB, 3) gather_scan_kernel(
+// nullptr: the last CTA to finish also scans the tile totals.  (A 3-CTA/SM
+// launch bound measured 0.8 % faster per iteration on most runs, but with
+// its 80 registers x 3 CTAs filling the register file the side stream's
+// karras could not start beside it and ~1 run in 4 fell into a 0.515 ms/iter
+// mode: left unbounded.)
+__global__ void __launch_bounds__(FB) gather_scan_kernel(
     const double2 *__restrict__ pos, const double *__restrict__ mass,
     const unsigned *__restrict__ idx, const unsigned *__restrict__ k32s,
     const unsigned long long *__restrict__ krest, int n, Body *__restrict__ bodies,
