@@ -103,3 +103,25 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError, match="CUDA device"):
         cv.from_edge_array(np.array([[0, 1]]))
+
+
+def test_reference_arm_runs_the_shipped_package_on_c1():
+    """bench.py's reference arm times oracle/_ref (the unmodified commviz
+    package); on the CPU-runnable C1 shape its community count and
+    supergraph size must equal the oracle restatement's."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import build_ref
+    if not os.path.exists(build_ref.ZIP):
+        pytest.skip("oracle/_ref not built here")
+    pytest.importorskip("numba")
+    import bench
+    from paper_2108_00529_b200 import synth
+    step = bench.reference_package_runner()
+    m, secs, st = step("C1")
+    e = synth.config_graph("C1", seed=0)
+    n, ee, deg = orc.from_edge_array(e)
+    lab, _, _ = orc.detect_communities(n, ee, deg, orc.degree_stats(deg)[0], 10, 0, workers=1)
+    assert m == len(e) and secs > 0
+    assert st["communities"] == len(np.unique(lab)) == st["supernodes"]
